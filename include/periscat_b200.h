@@ -1,0 +1,148 @@
+/*
+ * periscat_b200 -- C ABI of the B200 (sm_100a) hot path of the periscat
+ * solver (arXiv 1412.7466): the per-iteration matrix-vector product of the
+ * S-preconditioned Schur-complement GMRES solve for the inclusions'
+ * outgoing cylindrical-harmonic coefficients beta.
+ *
+ * Every entry point replaces one operation of the reference's Python solver
+ * API.  The reference package specifies these modules in SPEC.md but ships
+ * only the empty-grating modules, so the cited interface is
+ * the SPEC signature (SPEC.md line) or the present reference function
+ * (/root/reference/pkg/src/periscat/<file>:<line>).
+ *
+ * Conventions
+ *   - complex values are interleaved (re, im) doubles == numpy complex128;
+ *   - coefficient vectors are row-major [rhs][inclusion][n + p], n = -p..p
+ *     (the reference's order layout, geometry.py:382-385);
+ *   - "host" pointers are read during the call only; "device" pointers are
+ *     CUDA device memory owned by the caller (e.g. torch tensors);
+ *   - stream may be NULL (legacy default stream) or a cudaStream_t;
+ *   - calls on one context must be serialised; one context per GPU/process;
+ *   - every function returns PS_OK or an error code; ps_last_error() gives
+ *     the message.
+ */
+#ifndef PERISCAT_B200_H
+#define PERISCAT_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PS_OK 0
+#define PS_ERR_ARG 1         /* bad argument (ValueError in the reference)        */
+#define PS_ERR_DOMAIN 2      /* overlapping disks               */
+#define PS_ERR_NUMERICAL 3   /* NaN/Inf in a Krylov vector           */
+#define PS_ERR_CUDA 4        /* CUDA runtime failure                               */
+#define PS_ERR_STATE 5       /* call order (e.g. "not factorized", eg:267-268)     */
+#define PS_ERR_UNSUPPORTED 6 /* expansion order outside the compiled range         */
+
+typedef struct ps_ctx ps_ctx;
+
+/* ---- lifetime ---------------------------------------------------------- */
+int ps_version(void);
+int ps_create(ps_ctx** out, int device);
+void ps_destroy(ps_ctx* ctx);
+const char* ps_last_error(const ps_ctx* ctx);
+/* largest multipole order p the kernels are compiled for */
+int ps_max_order(void);
+
+/* ---- problem data (host inputs, uploaded once per solve) --------------- */
+
+/* Inclusion centres, multipole order p, near-field copies P, period d,
+ * middle-layer wavenumber k2.  Replaces the (centers, k, p) arguments of
+ * multiscat.apply_T and ProblemConfig.multipole_order /
+ * near_field_copies / period / k2 (geometry.py:323-333).
+ * Returns PS_ERR_DOMAIN if two enclosing centres (or a centre and a phased
+ * copy) coincide.  Resets the owned-target range to [0, M). */
+int ps_set_geometry(ps_ctx* ctx, int M, int p, int copies, double period, double k2,
+                    const double* centers_host /* [M][2] */);
+
+/* Owned target inclusions [t_begin, t_end) for target sharding across ranks
+ * ("apply_T parallel over target particles"). */
+int ps_set_target_range(ps_ctx* ctx, int t_begin, int t_end);
+
+/* Bloch phases alpha = exp(i kappa d) per right-hand side (geometry.py:373-375). */
+int ps_set_rhs_bloch(ps_ctx* ctx, int nrhs, const double* bloch_host /* complex [nrhs] */);
+
+/* Scattering matrix (scatmat.ScatteringMatrix): diagonal s_n
+ * (disks) or dense s_{ln} with per-inclusion rotation phases
+ * (rotate_scattering_matrix; rot_host may be NULL). */
+int ps_set_smatrix(ps_ctx* ctx, const double* S_host /* complex [L] or [L][L] */,
+                   int diagonal, const double* rot_host /* [M] or NULL */);
+
+/* Layer coupling geometry (curves of empty_grating.build_geometry,
+ * empty_grating.py:113-119): Gamma1 / Gamma2 nodes as rows (x, y, nx, ny,
+ * arc weight), the layer-2 left-wall nodes (x, y), the layer-2 expansion
+ * centre x2 (geometry.py:398-406), J-expansion order Q and Rayleigh-Bloch
+ * orders per direction nrb. */
+int ps_set_layers(ps_ctx* ctx, int n1, const double* g1_host, int n2, const double* g2_host,
+                  int nw, const double* w2_host, const double* x2_host, int Q, int nrb);
+
+/* SVD factors of the column-scaled empty-grating matrix for right-hand side
+ * irhs (empty_grating.factorize, empty_grating.py:259-261, numpy
+ * u, s, vh = svd(A, full_matrices=False)), its column scaling, the
+ * regularisation eps (geometry.py:338) and the incident right-hand side f
+ * (empty_grating.py:241-245).  Only the rows the particle field touches and
+ * the columns B reads (and c, d) are kept on the device; apply_pinv
+ * (empty_grating.py:264-273) is then two restricted GEMVs. */
+int ps_set_pinv(ps_ctx* ctx, int irhs, int nrow, int ncol, const double* U_host,
+                const double* s_host, const double* Vh_host, const double* col_scale_host,
+                double eps, const double* f_host, int col_c, int col_d);
+
+/* ---- hot path (device pointers) ---------------------------------------- */
+
+/* a = T beta: all-pairs Graf M2L over the 2P+1 phased copies, self term
+ * excluded (multiscat.apply_T).  beta [nrhs][M][L] for ALL
+ * inclusions; out [nrhs][t_end-t_begin][L] for the owned targets. */
+int ps_apply_T(ps_ctx* ctx, const void* beta_dev, void* out_dev, void* stream);
+
+/* g = C beta restricted to sources [s_begin, s_end): particle field values
+ * and normal derivatives on Gamma1 (negated), Gamma2 and the telescoped L2
+ * wall discrepancy (multiscat.multipole_to_targets_block).
+ * g [nrhs][nrow_c], overwritten. */
+int ps_apply_C(ps_ctx* ctx, const void* beta_dev, void* g_dev, int s_begin, int s_end,
+               void* stream);
+
+/* y = v_own - S (T v - B_phys A^+ g), g = C v already reduced over ranks
+ * (solver.apply_schur_operator).  v [nrhs][M][L] full,
+ * y [nrhs][Mt][L]. */
+int ps_apply_schur_g(ps_ctx* ctx, const void* v_dev, const void* g_dev, void* y_dev,
+                     void* stream);
+
+/* Single-rank convenience: g = C v over all sources, then ps_apply_schur_g. */
+int ps_apply_schur(ps_ctx* ctx, const void* v_dev, void* y_dev, void* stream);
+
+/* rhs = S B_phys A^+ f for the owned targets, [nrhs][Mt][L]. */
+int ps_schur_rhs(ps_ctx* ctx, void* rhs_dev, void* stream);
+
+/* x_empty restricted to (B columns, c, d) = A^+ (f - g), g = C beta reduced
+ * over ranks (solve_full recovery).  x [nrhs][ncol_b + 2 nrb]. */
+int ps_recover(ps_ctx* ctx, const void* g_dev, void* x_dev, void* stream);
+
+/* ---- GMRES building blocks (device-resident Arnoldi) --- */
+
+/* h[r][i] = <V_i^r, w^r> for i < k, over this rank's n entries:
+ * V [kmax][nrhs][n] (Krylov-index major), w [nrhs][n], h [nrhs][k] (complex). */
+int ps_block_dot(ps_ctx* ctx, int nrhs, int n, int k, int kmax, const void* V_dev,
+                 const void* w_dev, void* h_dev, void* stream);
+/* w^r -= sum_i h[r][i] V_i^r */
+int ps_block_axpy(ps_ctx* ctx, int nrhs, int n, int k, int kmax, const void* V_dev,
+                  const void* h_dev, void* w_dev, void* stream);
+/* nrm2[r] = sum |w^r|^2 (partial over this rank) */
+int ps_norm2(ps_ctx* ctx, int nrhs, int n, const void* w_dev, double* nrm2_dev, void* stream);
+
+/* Whole unrestarted GMRES on one device (single rank): zero initial guess,
+ * CGS2 Arnoldi, Givens least squares on the device; stops per RHS at
+ * relative residual <= tol or maxit.  rhs/x [nrhs][M][L];
+ * iters_host [nrhs]; hist_host [nrhs][maxit+1] (may be NULL). */
+int ps_gmres(ps_ctx* ctx, const void* rhs_dev, void* x_dev, double tol, int maxit,
+             int* iters_host, double* hist_host, void* stream);
+
+/* ---- roofline denominator ---------------------------------------------- */
+/* DFMA-chain FP64 throughput of the device (TFLOP/s, 2 flops per FMA). */
+int ps_dfma_peak(int device, double* tflops, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PERISCAT_B200_H */

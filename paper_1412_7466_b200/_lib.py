@@ -1,0 +1,90 @@
+"""ctypes binding of libperiscat_b200.so (include/periscat_b200.h).
+
+The product path has no CPU fallback: if the shared library is missing or
+no CUDA device is present, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libperiscat_b200.so")
+
+PS_OK, PS_ERR_ARG, PS_ERR_DOMAIN, PS_ERR_NUMERICAL, PS_ERR_CUDA, PS_ERR_STATE, PS_ERR_UNSUPPORTED = range(7)
+
+# symbol -> (restype, argtypes)
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_D = ctypes.c_double
+_DP = ctypes.POINTER(ctypes.c_double)
+_IP = ctypes.POINTER(ctypes.c_int)
+SIGNATURES = {
+    "ps_version": (_I, []),
+    "ps_max_order": (_I, []),
+    "ps_create": (_I, [ctypes.POINTER(_P), _I]),
+    "ps_destroy": (None, [_P]),
+    "ps_last_error": (ctypes.c_char_p, [_P]),
+    "ps_set_geometry": (_I, [_P, _I, _I, _I, _D, _D, _P]),
+    "ps_set_target_range": (_I, [_P, _I, _I]),
+    "ps_set_rhs_bloch": (_I, [_P, _I, _P]),
+    "ps_set_smatrix": (_I, [_P, _P, _I, _P]),
+    "ps_set_layers": (_I, [_P, _I, _P, _I, _P, _I, _P, _P, _I, _I]),
+    "ps_set_pinv": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _D, _P, _I, _I]),
+    "ps_apply_T": (_I, [_P, _P, _P, _P]),
+    "ps_apply_C": (_I, [_P, _P, _P, _I, _I, _P]),
+    "ps_apply_schur_g": (_I, [_P, _P, _P, _P, _P]),
+    "ps_apply_schur": (_I, [_P, _P, _P, _P]),
+    "ps_schur_rhs": (_I, [_P, _P, _P]),
+    "ps_recover": (_I, [_P, _P, _P, _P]),
+    "ps_block_dot": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "ps_block_axpy": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "ps_norm2": (_I, [_P, _I, _I, _P, _P, _P]),
+    "ps_gmres": (_I, [_P, _P, _P, _D, _I, _IP, _DP, _P]),
+    "ps_dfma_peak": (_I, [_I, _DP, _DP]),
+}
+
+_lib = None
+
+
+class PeriscatError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class DomainError(PeriscatError, ValueError):
+    pass
+
+
+class NumericalError(PeriscatError, FloatingPointError):
+    pass
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and type the shared library.  Raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} missing: build it with `python -m paper_1412_7466_b200.build` "
+                          "(the CUDA path has no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(ctx, rc: int):
+    if rc == PS_OK:
+        return
+    msg = load().ps_last_error(ctx)
+    msg = msg.decode() if msg else ""
+    if rc == PS_ERR_DOMAIN:
+        raise DomainError(rc, msg)
+    if rc == PS_ERR_NUMERICAL:
+        raise NumericalError(rc, msg)
+    raise PeriscatError(rc, msg)

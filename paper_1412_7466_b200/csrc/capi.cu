@@ -1,0 +1,433 @@
+// extern "C" entry points of include/periscat_b200.h.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "coupling.cuh"
+#include "ctx.cuh"
+#include "gmres.cuh"
+#include "m2l.cuh"
+
+using ps::C;
+using ps::Ctx;
+
+namespace {
+
+template <typename T>
+int dev_upload(Ctx* c, T** dst, const T* src, size_t n) {
+  if (*dst) {
+    cudaFree(*dst);
+    *dst = nullptr;
+  }
+  if (n == 0) return PS_OK;
+  PS_CUDA_TRY(c, cudaMalloc(reinterpret_cast<void**>(dst), n * sizeof(T)));
+  if (src) PS_CUDA_TRY(c, cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  return PS_OK;
+}
+
+int set_device(Ctx* c) {
+  PS_CUDA_TRY(c, cudaSetDevice(c->device));
+  return PS_OK;
+}
+
+// bloch^l for l = -(copies+1) .. copies+1 per RHS (the telescoped wall rows
+// of C need the two extreme powers, lp:211-237).
+int upload_blochpow(Ctx* c) {
+  const int np = 2 * c->copies + 3;
+  std::vector<double2> h((size_t)c->nrhs * np);
+  for (int r = 0; r < c->nrhs; ++r) {
+    const std::complex<double> b(c->rhs[r].bloch.x, c->rhs[r].bloch.y);
+    for (int i = 0; i < np; ++i) {
+      const int l = i - (c->copies + 1);
+      const std::complex<double> v = std::pow(b, (double)l);
+      h[(size_t)r * np + i] = make_double2(v.real(), v.imag());
+    }
+  }
+  return dev_upload(c, &c->d_blochpow, h.data(), h.size());
+}
+
+}  // namespace
+
+extern "C" {
+
+int ps_version(void) { return 1; }
+
+int ps_max_order(void) { return ps::m2l_max_order(); }
+
+int ps_create(ps_ctx** out, int device) {
+  if (!out) return PS_ERR_ARG;
+  Ctx* c = new Ctx();
+  c->device = device;
+  *out = reinterpret_cast<ps_ctx*>(c);
+  if (int rc = set_device(c)) return rc;
+  int sms = 0;
+  PS_CUDA_TRY(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  c->sm_count = sms;
+  c->rhs.resize(1);
+  return upload_blochpow(c);
+}
+
+void ps_destroy(ps_ctx* h) {
+  if (!h) return;
+  Ctx* c = C(h);
+  cudaSetDevice(c->device);
+  void* ptrs[] = {c->d_centers, c->d_S, c->d_rot, c->d_g1, c->d_g2, c->d_w2, c->d_blochpow,
+                  c->d_partial, c->d_work};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& r : c->rhs) {
+    void* rp[] = {r.d_Uh, r.d_sinv, r.d_Vb, r.d_cscale, r.d_f};
+    for (void* p : rp)
+      if (p) cudaFree(p);
+  }
+  ps::gmres_release(c);
+  delete c;
+}
+
+const char* ps_last_error(const ps_ctx* h) {
+  return h ? reinterpret_cast<const Ctx*>(h)->err.c_str() : "null context";
+}
+
+int ps_set_geometry(ps_ctx* h, int M, int p, int copies, double period, double k2,
+                    const double* centers) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (M < 0 || p < 0 || copies < 0 || !(period > 0) || !(k2 > 0) || (M > 0 && !centers)) {
+    c->err = "ps_set_geometry: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (p > ps::m2l_max_order()) {
+    c->err = "ps_set_geometry: p=" + std::to_string(p) + " exceeds compiled maximum " +
+             std::to_string(ps::m2l_max_order());
+    return PS_ERR_UNSUPPORTED;
+  }
+  // coincident centres (incl. phased copies) make the translation singular
+  // (SPEC.md:458, 506).  Disk overlap itself is the caller's geometry
+  // contract (ParticleSet.min_gap, geometry.py:131-144).
+  for (int i = 0; i < M; ++i)
+    for (int j = i; j < M; ++j)
+      for (int l = -copies; l <= copies; ++l) {
+        if (i == j && l == 0) continue;
+        const double dx = centers[2 * i] - centers[2 * j] - l * period;
+        const double dy = centers[2 * i + 1] - centers[2 * j + 1];
+        if (dx == 0.0 && dy == 0.0) {
+          c->err = "ps_set_geometry: coincident centres " + std::to_string(i) + ", " +
+                   std::to_string(j) + " (copy " + std::to_string(l) + ")";
+          return PS_ERR_DOMAIN;
+        }
+      }
+  if (int rc = set_device(c)) return rc;
+  c->M = M;
+  c->p = p;
+  c->L = 2 * p + 1;
+  c->copies = copies;
+  c->period = period;
+  c->k2 = k2;
+  c->t_begin = 0;
+  c->t_end = M;
+  c->h_centers.assign(centers, centers + 2 * (size_t)M);
+  if (int rc = dev_upload(c, &c->d_centers, centers, 2 * (size_t)M)) return rc;
+  return upload_blochpow(c);
+}
+
+int ps_set_target_range(ps_ctx* h, int t_begin, int t_end) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (t_begin < 0 || t_end < t_begin || t_end > c->M) {
+    c->err = "ps_set_target_range: bad range";
+    return PS_ERR_ARG;
+  }
+  c->t_begin = t_begin;
+  c->t_end = t_end;
+  return PS_OK;
+}
+
+int ps_set_rhs_bloch(ps_ctx* h, int nrhs, const double* bloch) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (nrhs < 1 || !bloch) {
+    c->err = "ps_set_rhs_bloch: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  if ((int)c->rhs.size() > nrhs) {
+    for (size_t r = nrhs; r < c->rhs.size(); ++r) {
+      auto& d = c->rhs[r];
+      void* rp[] = {d.d_Uh, d.d_sinv, d.d_Vb, d.d_cscale, d.d_f};
+      for (void* q : rp)
+        if (q) cudaFree(q);
+    }
+  }
+  c->rhs.resize(nrhs);
+  c->nrhs = nrhs;
+  for (int r = 0; r < nrhs; ++r) c->rhs[r].bloch = make_double2(bloch[2 * r], bloch[2 * r + 1]);
+  return upload_blochpow(c);
+}
+
+int ps_set_smatrix(ps_ctx* h, const double* S, int diagonal, const double* rot) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (c->p < 0 || !S) {
+    c->err = "ps_set_smatrix: set geometry first / null S";
+    return c->p < 0 ? PS_ERR_STATE : PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  c->s_diag = diagonal ? 1 : 0;
+  const size_t n = diagonal ? (size_t)c->L : (size_t)c->L * c->L;
+  if (int rc = dev_upload(c, &c->d_S, reinterpret_cast<const double2*>(S), n)) return rc;
+  if (!diagonal && rot) return dev_upload(c, &c->d_rot, rot, (size_t)c->M);
+  if (c->d_rot) {
+    cudaFree(c->d_rot);
+    c->d_rot = nullptr;
+  }
+  return PS_OK;
+}
+
+int ps_set_layers(ps_ctx* h, int n1, const double* g1, int n2, const double* g2, int nw,
+                  const double* w2, const double* x2, int Q, int nrb) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (n1 <= 0 || n2 <= 0 || nw <= 0 || Q < 0 || nrb <= 0 || !g1 || !g2 || !w2 || !x2) {
+    c->err = "ps_set_layers: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  c->n1 = n1;
+  c->n2 = n2;
+  c->nw = nw;
+  c->Q = Q;
+  c->nrb = nrb;
+  c->x2[0] = x2[0];
+  c->x2[1] = x2[1];
+  c->nrow_c = 2 * n1 + 2 * n2 + 2 * nw;
+  c->ncol_b = 2 * n1 + 2 * n2 + 2 * Q + 1;
+  if (int rc = dev_upload(c, &c->d_g1, g1, 5 * (size_t)n1)) return rc;
+  if (int rc = dev_upload(c, &c->d_g2, g2, 5 * (size_t)n2)) return rc;
+  if (int rc = dev_upload(c, &c->d_w2, w2, 2 * (size_t)nw)) return rc;
+  c->have_layers = 1;
+  return PS_OK;
+}
+
+int ps_set_pinv(ps_ctx* h, int irhs, int nrow, int ncol, const double* U, const double* s,
+                const double* Vh, const double* col_scale, double eps, const double* f, int col_c,
+                int col_d) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (!c->have_layers) {
+    c->err = "ps_set_pinv: call ps_set_layers first";
+    return PS_ERR_STATE;
+  }
+  if (irhs < 0 || irhs >= c->nrhs || nrow < c->nrow_c || ncol < c->ncol_b || !U || !s || !Vh ||
+      !col_scale || !f || !(eps > 0) || col_c < 0 || col_d < 0 || col_c + c->nrb > ncol ||
+      col_d + c->nrb > ncol) {
+    c->err = "ps_set_pinv: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  auto& R = c->rhs[irhs];
+  const int nsv = ncol;   // reduced SVD of an nrow x ncol matrix, nrow >= ncol
+  c->nsv = nsv;
+  const int nrc = c->nrow_c;
+  const int nout = c->ncol_b + 2 * c->nrb;
+  // Uh[k][i] = conj(U[i][k]) for the C rows i < nrow_c
+  std::vector<double2> uh((size_t)nsv * nrc);
+  for (int k = 0; k < nsv; ++k)
+    for (int i = 0; i < nrc; ++i) {
+      const double* u = U + 2 * ((size_t)i * ncol + k);
+      uh[(size_t)k * nrc + i] = make_double2(u[0], -u[1]);
+    }
+  std::vector<double> sinv(nsv);
+  for (int k = 0; k < nsv; ++k) sinv[k] = std::fmin(1.0 / s[k], 1.0 / eps);
+  // Vb[o][k] = conj(Vh[k][col(o)]) for the output columns (B cols, c, d)
+  std::vector<int> outcol(nout);
+  for (int o = 0; o < c->ncol_b; ++o) outcol[o] = o;
+  for (int o = 0; o < c->nrb; ++o) {
+    outcol[c->ncol_b + o] = col_c + o;
+    outcol[c->ncol_b + c->nrb + o] = col_d + o;
+  }
+  std::vector<double2> vb((size_t)nout * nsv);
+  std::vector<double> cs(nout);
+  for (int o = 0; o < nout; ++o) {
+    cs[o] = col_scale[outcol[o]];
+    for (int k = 0; k < nsv; ++k) {
+      const double* v = Vh + 2 * ((size_t)k * ncol + outcol[o]);
+      vb[(size_t)o * nsv + k] = make_double2(v[0], -v[1]);
+    }
+  }
+  std::vector<double2> fr(nrc);
+  for (int i = 0; i < nrc; ++i) fr[i] = make_double2(f[2 * i], f[2 * i + 1]);
+  if (int rc = dev_upload(c, &R.d_Uh, uh.data(), uh.size())) return rc;
+  if (int rc = dev_upload(c, &R.d_sinv, sinv.data(), sinv.size())) return rc;
+  if (int rc = dev_upload(c, &R.d_Vb, vb.data(), vb.size())) return rc;
+  if (int rc = dev_upload(c, &R.d_cscale, cs.data(), cs.size())) return rc;
+  if (int rc = dev_upload(c, &R.d_f, fr.data(), fr.size())) return rc;
+  return PS_OK;
+}
+
+int ps_apply_T(ps_ctx* h, const void* beta, void* out, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (c->p < 0) {
+    c->err = "ps_apply_T: geometry not set";
+    return PS_ERR_STATE;
+  }
+  if (!beta || !out) {
+    c->err = "ps_apply_T: null pointer";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  const int np = 2 * c->copies + 3;
+  const size_t in_stride = (size_t)c->M * c->L, out_stride = (size_t)(c->t_end - c->t_begin) * c->L;
+  for (int r = 0; r < c->nrhs; ++r) {
+    int rc = ps::m2l_apply(c, reinterpret_cast<const double2*>(beta) + r * in_stride,
+                           c->d_blochpow + (size_t)r * np + 1,
+                           reinterpret_cast<double2*>(out) + r * out_stride, 0, nullptr, nullptr,
+                           st);
+    if (rc) return rc;
+  }
+  return PS_OK;
+}
+
+int ps_apply_C(ps_ctx* h, const void* beta, void* g, int s_begin, int s_end, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (c->p < 0 || !c->have_layers) {
+    c->err = "ps_apply_C: geometry/layers not set";
+    return PS_ERR_STATE;
+  }
+  if (!beta || !g || s_begin < 0 || s_end > c->M || s_end < s_begin) {
+    c->err = "ps_apply_C: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::apply_C(c, reinterpret_cast<const double2*>(beta), reinterpret_cast<double2*>(g),
+                     s_begin, s_end, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_apply_schur_g(ps_ctx* h, const void* v, const void* g, void* y, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (c->p < 0 || !c->d_S) {
+    c->err = "ps_apply_schur_g: geometry / scattering matrix not set";
+    return PS_ERR_STATE;
+  }
+  if (!v || !y) {
+    c->err = "ps_apply_schur_g: null pointer";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::apply_schur_g(c, reinterpret_cast<const double2*>(v),
+                           reinterpret_cast<const double2*>(g), reinterpret_cast<double2*>(y),
+                           reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_apply_schur(ps_ctx* h, const void* v, void* y, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (c->p < 0 || !c->d_S) {
+    c->err = "ps_apply_schur: geometry / scattering matrix not set";
+    return PS_ERR_STATE;
+  }
+  if (!v || !y) {
+    c->err = "ps_apply_schur: null pointer";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::apply_schur(c, reinterpret_cast<const double2*>(v), reinterpret_cast<double2*>(y),
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_schur_rhs(ps_ctx* h, void* rhs, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (c->p < 0 || !c->d_S || !c->have_layers || !c->rhs[0].d_Uh) {
+    c->err = "ps_schur_rhs: geometry / S / layers / pinv not set";
+    return PS_ERR_STATE;
+  }
+  if (!rhs) {
+    c->err = "ps_schur_rhs: null pointer";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::schur_rhs(c, reinterpret_cast<double2*>(rhs), reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_recover(ps_ctx* h, const void* g, void* x, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (!c->have_layers || !c->rhs[0].d_Uh) {
+    c->err = "ps_recover: layers / pinv not set";
+    return PS_ERR_STATE;
+  }
+  if (!g || !x) {
+    c->err = "ps_recover: null pointer";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::recover(c, reinterpret_cast<const double2*>(g), reinterpret_cast<double2*>(x),
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_block_dot(ps_ctx* h, int nrhs, int n, int k, int kmax, const void* V, const void* w,
+                 void* hout, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (nrhs < 1 || n < 0 || k < 0 || k > kmax || !V || !w || !hout) {
+    c->err = "ps_block_dot: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::block_dot(c, nrhs, n, k, kmax, reinterpret_cast<const double2*>(V),
+                       reinterpret_cast<const double2*>(w), reinterpret_cast<double2*>(hout),
+                       reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_block_axpy(ps_ctx* h, int nrhs, int n, int k, int kmax, const void* V, const void* hin,
+                  void* w, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (nrhs < 1 || n < 0 || k < 0 || k > kmax || !V || !w || !hin) {
+    c->err = "ps_block_axpy: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::block_axpy(c, nrhs, n, k, kmax, reinterpret_cast<const double2*>(V),
+                        reinterpret_cast<const double2*>(hin), reinterpret_cast<double2*>(w),
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_norm2(ps_ctx* h, int nrhs, int n, const void* w, double* nrm2, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (nrhs < 1 || n < 0 || !w || !nrm2) {
+    c->err = "ps_norm2: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::norm2(c, nrhs, n, reinterpret_cast<const double2*>(w), nrm2,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_gmres(ps_ctx* h, const void* rhs, void* x, double tol, int maxit, int* iters,
+             double* hist, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (c->p < 0 || !c->d_S) {
+    c->err = "ps_gmres: geometry / scattering matrix not set";
+    return PS_ERR_STATE;
+  }
+  if (!rhs || !x || !iters || maxit < 1 || !(tol > 0)) {
+    c->err = "ps_gmres: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::gmres(c, reinterpret_cast<const double2*>(rhs), reinterpret_cast<double2*>(x), tol,
+                   maxit, iters, hist, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

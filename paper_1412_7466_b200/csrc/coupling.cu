@@ -1,0 +1,606 @@
+// Schur-complement correction of the preconditioned operator
+//   K v = v - S (T v - B_phys A^+ C v)          (B = -B_phys)
+// (solver.apply_schur_operator).
+//
+//   K3 c_kernel   : g = C beta -- particle field values / normal derivatives on
+//                   Gamma1 (negated), Gamma2 and the telescoped L2 wall rows
+//                   (multiscat.multipole_to_targets_block, SPEC.md:494-502;
+//                   wall telescoping as layerpot.wall_discrepancy_blocks,
+//                   layerpot.py:211-237).
+//   K4 pinv_*     : A^+ g = col_scale .* V (Sigma^+ (U^* g)) restricted to the
+//                   rows C touches and the columns B reads
+//                   (empty_grating.apply_pinv, empty_grating.py:264-273).
+//   K5 b_kernel   : local coefficients at every owned inclusion of the layer-2
+//                   field: phased single/double layers on Gamma1, Gamma2 at k2
+//                   plus the L2L of the a2 J-expansion
+//                   (multiscat.source_to_local_block).
+//
+// All three reuse the translation-symbol generator of K1: with
+// w_n = H_n(k r) e^{i n theta},
+//   (d/dx + i d/dy) w_n = -k w_{n+1},  (d/dx - i d/dy) w_n = k w_{n-1},
+// so a field gradient and a double-layer (dipole) source are both two extra
+// symbol orders of the same row.
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "coupling.cuh"
+#include "m2l.cuh"
+#include "symbols.cuh"
+
+namespace ps {
+
+namespace {
+
+constexpr int kCT = 128;   // threads per CTA for K3 / K5
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+
+// deterministic block reduction of two complex values over kCT threads
+__device__ void block_sum2(double2& a, double2& b, double2* sh /*[2*kCT]*/) {
+  sh[threadIdx.x] = a;
+  sh[kCT + threadIdx.x] = b;
+  __syncthreads();
+  for (int s = kCT / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sh[threadIdx.x].x += sh[threadIdx.x + s].x;
+      sh[threadIdx.x].y += sh[threadIdx.x + s].y;
+      sh[kCT + threadIdx.x].x += sh[kCT + threadIdx.x + s].x;
+      sh[kCT + threadIdx.x].y += sh[kCT + threadIdx.x + s].y;
+    }
+    __syncthreads();
+  }
+  a = sh[0];
+  b = sh[kCT];
+}
+
+// ---------------------------------------------------------------- K3: C beta
+struct CArgs {
+  const double* centers;   // [M][2]
+  const double2* beta;     // [M][L]
+  const double2* bpow;     // bloch^l, l = -(P+1)..P+1 (index l + P + 1)
+  const double* g1;        // [n1][5]
+  const double* g2;        // [n2][5]
+  const double* w2;        // [nw][2]
+  double2* g;              // [nrow_c]
+  int n1, n2, nw, copies, s_begin, s_end;
+  double period, k2;
+};
+
+template <int P>
+__global__ void __launch_bounds__(kCT) c_kernel(CArgs a) {
+  constexpr int NU = P + 1;
+  constexpr int L = 2 * P + 1;
+  __shared__ double jbuf[(NU + 1) * kCT];
+  __shared__ double2 red[2 * kCT];
+  const int row = blockIdx.x;              // target node index over g1, g2, wall
+  double tx, ty, nx, ny, sgn;
+  int kind;                                // 0 interface, 1 wall
+  int rv, rd;
+  if (row < a.n1) {
+    const double* q = a.g1 + 5 * row;
+    tx = q[0]; ty = q[1]; nx = q[2]; ny = q[3]; sgn = -1.0; kind = 0;
+    rv = row; rd = a.n1 + row;
+  } else if (row < a.n1 + a.n2) {
+    const int i = row - a.n1;
+    const double* q = a.g2 + 5 * i;
+    tx = q[0]; ty = q[1]; nx = q[2]; ny = q[3]; sgn = 1.0; kind = 0;
+    rv = 2 * a.n1 + i; rd = 2 * a.n1 + a.n2 + i;
+  } else {
+    const int i = row - a.n1 - a.n2;
+    tx = a.w2[2 * i]; ty = a.w2[2 * i + 1]; nx = 1.0; ny = 0.0; sgn = 1.0; kind = 1;
+    rv = 2 * a.n1 + 2 * a.n2 + i; rd = rv + a.nw;
+  }
+  const int P_ = a.copies;
+  // source images: interface rows use l = -P..P with weight bloch^l; the
+  // wall rows use the two telescoped extremes
+  //   +bloch^{P+1} at shift +P d  and  -bloch^{-P} at shift -(P+1) d.
+  const int nl = kind == 0 ? 2 * P_ + 1 : 2;
+  const int ns = a.s_end - a.s_begin;
+  const double hk = 0.5 * a.k2;
+  // D_nu coefficient of w_nu in the normal derivative:
+  //   dn = sum_n beta_n [ (k/2)(nx + i ny) w_{n-1}... ] -> see below
+  const double2 cp = make_double2(hk * nx, hk * ny);    // (k/2)(nx + i ny)
+  const double2 cm = make_double2(-hk * nx, hk * ny);   // (k/2)(-nx + i ny)
+  double2 val = make_double2(0, 0), der = make_double2(0, 0);
+  double* jb = jbuf + threadIdx.x;
+  for (int it = threadIdx.x; it < ns * nl; it += kCT) {
+    const int j = a.s_begin + it / nl;
+    const int li = it % nl;
+    int l;
+    double2 wgt;
+    if (kind == 0) {
+      l = li - P_;
+      wgt = a.bpow[l + P_ + 1];
+    } else if (li == 0) {
+      l = P_;
+      wgt = a.bpow[2 * P_ + 2];
+    } else {
+      l = -(P_ + 1);
+      const double2 b = a.bpow[1];
+      wgt = make_double2(-b.x, -b.y);
+    }
+    const double dx = tx - a.centers[2 * j] - (double)l * a.period;
+    const double dy = ty - a.centers[2 * j + 1];
+    const double rho = hypot(dx, dy);
+    const double inv = 1.0 / rho;
+    const double2* bj = a.beta + (size_t)j * L;
+    double2 pv = make_double2(0, 0), pd = make_double2(0, 0);
+    hankel_symbols<NU>(
+        a.k2 * rho, dx * inv, dy * inv, [&](int nu, double v) { jb[nu * kCT] = v; },
+        [&](int nu) { return jb[nu * kCT]; },
+        [&](int nu, double re, double im) {
+          const double2 w = make_double2(re, im);
+          if (nu >= -P && nu <= P) pv = cfma(bj[nu + P], w, pv);
+          // d/dn w-coefficient: (k/2)[(nx - i ny)... expressed per nu:
+          //   dx u = (k/2) sum_n beta_n (w_{n-1} - w_{n+1})
+          //   dy u = (ik/2) sum_n beta_n (w_{n+1} + w_{n-1})
+          // coefficient of w_nu: from n = nu+1 (w_{n-1}) and n = nu-1 (w_{n+1})
+          //   nx (k/2)(b_{nu+1} - b_{nu-1}) + ny (ik/2)(b_{nu-1} + b_{nu+1})
+          //   = b_{nu+1} (k/2)(nx + i ny) + b_{nu-1} (k/2)(-nx + i ny)
+          double2 dcoef = make_double2(0, 0);
+          if (nu + 1 >= -P && nu + 1 <= P) dcoef = cmul(bj[nu + 1 + P], cp);
+          if (nu - 1 >= -P && nu - 1 <= P) dcoef = cfma(bj[nu - 1 + P], cm, dcoef);
+          pd = cfma(dcoef, w, pd);
+        });
+    val = cfma(wgt, pv, val);
+    der = cfma(wgt, pd, der);
+  }
+  block_sum2(val, der, red);
+  if (threadIdx.x == 0) {
+    a.g[rv] = make_double2(sgn * val.x, sgn * val.y);
+    a.g[rd] = make_double2(sgn * der.x, sgn * der.y);
+  }
+}
+
+// ---------------------------------------------------------------- K4: A^+ g
+// h[k] = sinv[k] * sum_i Uh[k][i] g[i]      (one warp per k)
+__global__ void pinv_uh(const double2* __restrict__ Uh, const double* __restrict__ sinv,
+                        const double2* __restrict__ g, int nsv, int nrc, double2* __restrict__ h) {
+  const int k = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (k >= nsv) return;
+  const double2* u = Uh + (size_t)k * nrc;
+  double2 s = make_double2(0, 0);
+  for (int i = lane; i < nrc; i += 32) s = cfma(u[i], g[i], s);
+  for (int o = 16; o > 0; o >>= 1) {
+    s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+    s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+  }
+  if (lane == 0) h[k] = make_double2(s.x * sinv[k], s.y * sinv[k]);
+}
+
+// x[o] = cscale[o] * sum_k Vb[o][k] h[k]     (one warp per output column)
+__global__ void pinv_v(const double2* __restrict__ Vb, const double* __restrict__ cs,
+                       const double2* __restrict__ h, int nout, int nsv, double2* __restrict__ x) {
+  const int o = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (o >= nout) return;
+  const double2* v = Vb + (size_t)o * nsv;
+  double2 s = make_double2(0, 0);
+  for (int k = lane; k < nsv; k += 32) s = cfma(v[k], h[k], s);
+  for (int d = 16; d > 0; d >>= 1) {
+    s.x += __shfl_xor_sync(0xffffffffu, s.x, d);
+    s.y += __shfl_xor_sync(0xffffffffu, s.y, d);
+  }
+  if (lane == 0) x[o] = make_double2(s.x * cs[o], s.y * cs[o]);
+}
+
+// g_out = f - g_in  (recovery right-hand side)
+__global__ void f_minus(const double2* __restrict__ f, const double2* __restrict__ g, int n,
+                        double2* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = make_double2(f[i].x - g[i].x, f[i].y - g[i].y);
+}
+
+// ---------------------------------------------------------------- K5: B_phys x
+struct BArgs {
+  const double* centers;   // [M][2]
+  const double2* x;        // [ncol_b] physical empty-grating unknowns
+  const double2* bpow;     // bloch^l (index l + P + 1)
+  const double* g1;
+  const double* g2;
+  double2* out;            // [nt][L]
+  int n1, n2, copies, t_begin, nt, Q;
+  double period, k2, x2x, x2y;
+};
+
+template <int P>
+struct BShape {
+  static constexpr int NU = P + 1;
+  static constexpr int NSP = 2 * NU + 1;           // odd: conflict-free row stride
+  static constexpr int L = 2 * P + 1;
+};
+
+template <int P>
+__global__ void __launch_bounds__(kCT) b_kernel(BArgs a) {
+  using S = BShape<P>;
+  constexpr int NU = S::NU, NSP = S::NSP, L = S::L;
+  static_assert(L <= kCT / 2, "two output groups of kCT/2 threads");
+  extern __shared__ double2 bsm[];
+  double2* sym = bsm;                      // [kCT][NSP]
+  double2* coef = bsm + kCT * NSP;         // [kCT][3]: cs, cdp, cdm
+  __shared__ double2 fin[kCT];
+  const int mloc = blockIdx.x;
+  const int m = a.t_begin + mloc;
+  const double xm = a.centers[2 * m], ym = a.centers[2 * m + 1];
+  const int nl = 2 * a.copies + 1;
+  const int nsrc = (a.n1 + a.n2) * nl;
+  const int grp = threadIdx.x / (kCT / 2), np = threadIdx.x % (kCT / 2);   // output n' = np - P
+  double2 acc = make_double2(0, 0);
+  const double hk = 0.5 * a.k2;
+  for (int base = 0; base < nsrc; base += kCT) {
+    const int it = base + threadIdx.x;
+    double2* row = sym + (size_t)threadIdx.x * NSP;
+    if (it < nsrc) {
+      const int node = it / nl;
+      const int l = it % nl - a.copies;
+      const bool on1 = node < a.n1;
+      const double* q = on1 ? a.g1 + 5 * node : a.g2 + 5 * (node - a.n1);
+      const int mu_col = on1 ? node : 2 * a.n1 + (node - a.n1);
+      const int sg_col = on1 ? a.n1 + node : 2 * a.n1 + a.n2 + (node - a.n1);
+      const double2 wl = a.bpow[l + a.copies + 1];
+      const double w = q[4];
+      // (i/4) bloch^l w * density
+      const double2 iw = make_double2(-0.25 * w * wl.y, 0.25 * w * wl.x);
+      const double2 cs = cmul(iw, a.x[sg_col]);
+      const double2 cd = cmul(iw, a.x[mu_col]);
+      const double nx = q[2], ny = q[3];
+      // dipole coefficients: beta_1 = (k/2)(nx - i ny), beta_-1 = -(k/2)(nx + i ny)
+      coef[3 * threadIdx.x + 0] = cs;
+      coef[3 * threadIdx.x + 1] = cmul(cd, make_double2(hk * nx, -hk * ny));
+      coef[3 * threadIdx.x + 2] = cmul(cd, make_double2(-hk * nx, -hk * ny));
+      const double dx = xm - q[0] - (double)l * a.period;
+      const double dy = ym - q[1];
+      const double rho = hypot(dx, dy);
+      const double inv = 1.0 / rho;
+      double2* r0 = row + NU;
+      hankel_symbols<NU>(
+          a.k2 * rho, dx * inv, dy * inv, [&](int nu, double v) { r0[nu].x = v; },
+          [&](int nu) { return r0[nu].x; },
+          [&](int nu, double re, double im) { r0[nu] = make_double2(re, im); });
+    } else {
+      coef[3 * threadIdx.x + 0] = make_double2(0, 0);
+      coef[3 * threadIdx.x + 1] = make_double2(0, 0);
+      coef[3 * threadIdx.x + 2] = make_double2(0, 0);
+      for (int q = 0; q < NSP; ++q) row[q] = make_double2(0, 0);
+    }
+    __syncthreads();
+    if (np < L) {
+      const int nprime = np - P;
+      const int lim = min(kCT / 2, nsrc - base - grp * (kCT / 2));
+      for (int yy = 0; yy < lim; ++yy) {
+        const int y = grp * (kCT / 2) + yy;
+        const double2* rr = sym + (size_t)y * NSP + NU;
+        acc = cfma(coef[3 * y + 0], rr[-nprime], acc);
+        acc = cfma(coef[3 * y + 1], rr[1 - nprime], acc);
+        acc = cfma(coef[3 * y + 2], rr[-1 - nprime], acc);
+      }
+    }
+    __syncthreads();
+  }
+  // combine the two groups
+  fin[threadIdx.x] = acc;
+  __syncthreads();
+  if (grp == 0 && np < L) {
+    acc.x += fin[threadIdx.x + kCT / 2].x;
+    acc.y += fin[threadIdx.x + kCT / 2].y;
+    fin[threadIdx.x] = acc;
+  }
+  __syncthreads();
+  // B_pm: L2L of the a2 expansion about x2:
+  //   a[n'] += sum_q a2_q J_{q-n'}(k2 rho) e^{i(q-n') phi},  (rho, phi) = polar(x_m - x2)
+  const int NQ = a.Q + P;
+  double2* jl = sym;                         // [2*NQ+1] signed orders, reuse
+  if (threadIdx.x == 0) {
+    const double dx = xm - a.x2x, dy = ym - a.x2y;
+    const double rho = hypot(dx, dy);
+    double2* j0 = jl + NQ;
+    if (rho == 0.0) {
+      for (int nu = -NQ; nu <= NQ; ++nu) j0[nu] = make_double2(nu == 0 ? 1.0 : 0.0, 0.0);
+    } else {
+      const double z = a.k2 * rho;
+      double inv_norm, y0, y1;
+      bessel_jy_sweep(z, NQ, [&](int nu, double v) { j0[nu].x = v; }, &inv_norm, &y0, &y1);
+      const double c = dx / rho, s = dy / rho;
+      double pr = 1.0, pi = 0.0;
+      j0[0] = make_double2(j0[0].x * inv_norm, 0.0);
+      for (int nu = 1; nu <= NQ; ++nu) {
+        const double npr = fma(pr, c, -pi * s);
+        const double npi = fma(pr, s, pi * c);
+        pr = npr;
+        pi = npi;
+        const double J = j0[nu].x * inv_norm;
+        const double sg = (nu & 1) ? -1.0 : 1.0;
+        j0[nu] = make_double2(J * pr, J * pi);
+        j0[-nu] = make_double2(sg * J * pr, -sg * J * pi);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < L) {
+    const int nprime = threadIdx.x - P;
+    double2 s = fin[threadIdx.x];
+    const double2* a2 = a.x + 2 * a.n1 + 2 * a.n2;   // a2 column block
+    for (int qq = -a.Q; qq <= a.Q; ++qq) s = cfma(a2[qq + a.Q], jl[NQ + qq - nprime], s);
+    a.out[(size_t)mloc * L + threadIdx.x] = s;
+  }
+}
+
+// y[m][r] = v[m][r] + sgn sum_n e^{i rot_m (r-n)} s[r][n] u[m][n]  (dense S)
+__global__ void dense_s_epilogue(const double2* __restrict__ S, const double* __restrict__ rot,
+                                 const double2* __restrict__ v_own, const double2* __restrict__ u,
+                                 int t_begin, int L, double sgn, double2* __restrict__ y) {
+  extern __shared__ double2 us[];
+  const int mloc = blockIdx.x;
+  for (int n = threadIdx.x; n < L; n += blockDim.x) us[n] = u[(size_t)mloc * L + n];
+  __syncthreads();
+  const double phi = rot ? rot[t_begin + mloc] : 0.0;
+  for (int r = threadIdx.x; r < L; r += blockDim.x) {
+    double2 s = make_double2(0, 0);
+    for (int n = 0; n < L; ++n) {
+      double2 e = S[(size_t)r * L + n];
+      if (rot) {
+        double sn, cn;
+        sincos(phi * (double)(r - n), &sn, &cn);
+        e = cmul(e, make_double2(cn, sn));
+      }
+      s = cfma(e, us[n], s);
+    }
+    const double2 vv = v_own ? v_own[(size_t)mloc * L + r] : make_double2(0, 0);
+    y[(size_t)mloc * L + r] = make_double2(fma(sgn, s.x, vv.x), fma(sgn, s.y, vv.y));
+  }
+}
+
+template <int P>
+int launch_c(Ctx* c, const double2* beta, const double2* bpow, double2* g, int s0, int s1,
+             cudaStream_t st) {
+  CArgs a;
+  a.centers = c->d_centers;
+  a.beta = beta;
+  a.bpow = bpow;
+  a.g1 = c->d_g1;
+  a.g2 = c->d_g2;
+  a.w2 = c->d_w2;
+  a.g = g;
+  a.n1 = c->n1;
+  a.n2 = c->n2;
+  a.nw = c->nw;
+  a.copies = c->copies;
+  a.s_begin = s0;
+  a.s_end = s1;
+  a.period = c->period;
+  a.k2 = c->k2;
+  c_kernel<P><<<c->n1 + c->n2 + c->nw, kCT, 0, st>>>(a);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  return PS_OK;
+}
+
+template <int P>
+int launch_b(Ctx* c, const double2* x, const double2* bpow, double2* out, cudaStream_t st) {
+  using S = BShape<P>;
+  BArgs a;
+  a.centers = c->d_centers;
+  a.x = x;
+  a.bpow = bpow;
+  a.g1 = c->d_g1;
+  a.g2 = c->d_g2;
+  a.out = out;
+  a.n1 = c->n1;
+  a.n2 = c->n2;
+  a.copies = c->copies;
+  a.t_begin = c->t_begin;
+  a.nt = c->t_end - c->t_begin;
+  a.Q = c->Q;
+  a.period = c->period;
+  a.k2 = c->k2;
+  a.x2x = c->x2[0];
+  a.x2y = c->x2[1];
+  if (a.nt <= 0) return PS_OK;
+  size_t smem = (size_t)kCT * S::NSP * sizeof(double2) + (size_t)kCT * 3 * sizeof(double2);
+  const size_t need_jl = (size_t)(2 * (c->Q + P) + 1) * sizeof(double2);
+  if (smem < need_jl + 3 * kCT * sizeof(double2)) smem = need_jl + 3 * kCT * sizeof(double2);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    PS_CUDA_TRY(c, cudaFuncSetAttribute(b_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    attr = smem;
+  }
+  b_kernel<P><<<a.nt, kCT, smem, st>>>(a);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  return PS_OK;
+}
+
+int dispatch_c(Ctx* c, const double2* beta, const double2* bpow, double2* g, int s0, int s1,
+               cudaStream_t st) {
+  switch (c->p) {
+#define PS_CASE(P) \
+  case P:          \
+    return launch_c<P>(c, beta, bpow, g, s0, s1, st);
+    PS_M2L_ORDERS(PS_CASE)
+#undef PS_CASE
+    default:
+      c->err = "apply_C: order not compiled";
+      return PS_ERR_UNSUPPORTED;
+  }
+}
+
+int dispatch_b(Ctx* c, const double2* x, const double2* bpow, double2* out, cudaStream_t st) {
+  switch (c->p) {
+#define PS_CASE(P) \
+  case P:          \
+    return launch_b<P>(c, x, bpow, out, st);
+    PS_M2L_ORDERS(PS_CASE)
+#undef PS_CASE
+    default:
+      c->err = "apply_B: order not compiled";
+      return PS_ERR_UNSUPPORTED;
+  }
+}
+
+// workspace layout per RHS: g [nrc] | h [nsv] | x [nout] | bsub [Mt*L] | u [Mt*L]
+struct Work {
+  double2 *g, *h, *x, *bsub, *u;
+};
+
+int work(Ctx* c, int r, Work* w) {
+  const size_t nrc = c->nrow_c, nsv = c->nsv > 0 ? c->nsv : 1;
+  const size_t nout = c->ncol_b + 2 * c->nrb;
+  const size_t mtl = (size_t)(c->t_end - c->t_begin) * c->L;
+  const size_t per = nrc + nsv + nout + 2 * mtl + 8;
+  const size_t need = per * c->nrhs;
+  if (c->work_elems < need) {
+    if (c->d_work) cudaFree(c->d_work);
+    c->d_work = nullptr;
+    c->work_elems = 0;
+    PS_CUDA_TRY(c, cudaMalloc(&c->d_work, need * sizeof(double2)));
+    c->work_elems = need;
+  }
+  double2* b = c->d_work + per * r;
+  w->g = b;
+  w->h = w->g + nrc;
+  w->x = w->h + nsv;
+  w->bsub = w->x + nout;
+  w->u = w->bsub + mtl;
+  return PS_OK;
+}
+
+int pinv(Ctx* c, int r, const double2* g, double2* x, int nout, cudaStream_t st) {
+  const RhsData& R = c->rhs[r];
+  Work w;
+  if (int rc = work(c, r, &w)) return rc;
+  pinv_uh<<<(c->nsv + 7) / 8, 256, 0, st>>>(R.d_Uh, R.d_sinv, g, c->nsv, c->nrow_c, w.h);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  pinv_v<<<(nout + 7) / 8, 256, 0, st>>>(R.d_Vb, R.d_cscale, w.h, nout, c->nsv, x);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  return PS_OK;
+}
+
+const double2* bpow_of(Ctx* c, int r) { return c->d_blochpow + (size_t)r * (2 * c->copies + 3); }
+
+}  // namespace
+
+int apply_C(Ctx* c, const double2* beta, double2* g, int s0, int s1, cudaStream_t st) {
+  const size_t in_stride = (size_t)c->M * c->L;
+  for (int r = 0; r < c->nrhs; ++r) {
+    if (int rc = dispatch_c(c, beta + r * in_stride, bpow_of(c, r), g + (size_t)r * c->nrow_c, s0,
+                            s1, st))
+      return rc;
+  }
+  return PS_OK;
+}
+
+// B_phys A^+ g for RHS r into w.bsub
+static int b_pinv(Ctx* c, int r, const double2* g, Work* w, cudaStream_t st) {
+  if (int rc = pinv(c, r, g, w->x, c->ncol_b, st)) return rc;
+  return dispatch_b(c, w->x, bpow_of(c, r), w->bsub, st);
+}
+
+static int s_apply(Ctx* c, const double2* v_own, const double2* u, double2* y, cudaStream_t st,
+                   double sgn = -1.0) {
+  // dense-S epilogue: y = v_own + sgn S u
+  const int nt = c->t_end - c->t_begin;
+  if (nt <= 0) return PS_OK;
+  dense_s_epilogue<<<nt, 64, c->L * sizeof(double2), st>>>(c->d_S, c->d_rot, v_own, u,
+                                                          c->t_begin, c->L, sgn, y);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  return PS_OK;
+}
+
+int apply_schur_g(Ctx* c, const double2* v, const double2* g, double2* y, cudaStream_t st) {
+  const size_t in_stride = (size_t)c->M * c->L;
+  const size_t out_stride = (size_t)(c->t_end - c->t_begin) * c->L;
+  const bool coupled = c->have_layers && c->rhs[0].d_Uh && g;
+  for (int r = 0; r < c->nrhs; ++r) {
+    Work w;
+    if (int rc = work(c, r, &w)) return rc;
+    const double2* bsub = nullptr;
+    if (coupled) {
+      if (int rc = b_pinv(c, r, g + (size_t)r * c->nrow_c, &w, st)) return rc;
+      bsub = w.bsub;
+    }
+    const double2* vr = v + r * in_stride;
+    const double2* v_own = vr + (size_t)c->t_begin * c->L;
+    if (c->s_diag) {
+      if (int rc = m2l_apply(c, vr, bpow_of(c, r) + 1, y + r * out_stride, 1, v_own, bsub, st))
+        return rc;
+    } else {
+      if (int rc = m2l_apply(c, vr, bpow_of(c, r) + 1, w.u, 2, v_own, bsub, st)) return rc;
+      if (int rc = s_apply(c, v_own, w.u, y + r * out_stride, st)) return rc;
+    }
+  }
+  return PS_OK;
+}
+
+int apply_schur(Ctx* c, const double2* v, double2* y, cudaStream_t st) {
+  const bool coupled = c->have_layers && c->rhs[0].d_Uh;
+  if (!coupled) return apply_schur_g(c, v, nullptr, y, st);
+  const size_t in_stride = (size_t)c->M * c->L;
+  const size_t out_stride = (size_t)(c->t_end - c->t_begin) * c->L;
+  const int nrhs = c->nrhs;
+  for (int r = 0; r < nrhs; ++r) {
+    Work w;
+    if (int rc = work(c, r, &w)) return rc;
+    if (int rc = dispatch_c(c, v + r * in_stride, bpow_of(c, r), w.g, 0, c->M, st)) return rc;
+  }
+  for (int r = 0; r < nrhs; ++r) {
+    Work w;
+    if (int rc = work(c, r, &w)) return rc;
+    if (int rc = b_pinv(c, r, w.g, &w, st)) return rc;
+    const double2* vr = v + r * in_stride;
+    const double2* v_own = vr + (size_t)c->t_begin * c->L;
+    if (c->s_diag) {
+      if (int rc = m2l_apply(c, vr, bpow_of(c, r) + 1, y + r * out_stride, 1, v_own, w.bsub, st))
+        return rc;
+    } else {
+      if (int rc = m2l_apply(c, vr, bpow_of(c, r) + 1, w.u, 2, v_own, w.bsub, st)) return rc;
+      if (int rc = s_apply(c, v_own, w.u, y + r * out_stride, st)) return rc;
+    }
+  }
+  return PS_OK;
+}
+
+__global__ void diag_s_apply(const double2* __restrict__ s, const double2* __restrict__ u, int n,
+                             int L, double2* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = cmul(s[i % L], u[i]);
+}
+
+int schur_rhs(Ctx* c, double2* rhs, cudaStream_t st) {
+  const int nt = c->t_end - c->t_begin;
+  const size_t out_stride = (size_t)nt * c->L;
+  for (int r = 0; r < c->nrhs; ++r) {
+    Work w;
+    if (int rc = work(c, r, &w)) return rc;
+    if (int rc = b_pinv(c, r, c->rhs[r].d_f, &w, st)) return rc;
+    const int n = nt * c->L;
+    if (n == 0) continue;
+    if (c->s_diag) {
+      diag_s_apply<<<(n + 255) / 256, 256, 0, st>>>(c->d_S, w.bsub, n, c->L, rhs + r * out_stride);
+      PS_CUDA_TRY(c, cudaGetLastError());
+    } else {
+      if (int rc = s_apply(c, nullptr, w.bsub, rhs + r * out_stride, st, 1.0)) return rc;
+    }
+  }
+  return PS_OK;
+}
+
+int recover(Ctx* c, const double2* g, double2* x, cudaStream_t st) {
+  const int nout = c->ncol_b + 2 * c->nrb;
+  for (int r = 0; r < c->nrhs; ++r) {
+    Work w;
+    if (int rc = work(c, r, &w)) return rc;
+    f_minus<<<(c->nrow_c + 255) / 256, 256, 0, st>>>(c->rhs[r].d_f, g + (size_t)r * c->nrow_c,
+                                                     c->nrow_c, w.g);
+    PS_CUDA_TRY(c, cudaGetLastError());
+    if (int rc = pinv(c, r, w.g, x + (size_t)r * nout, nout, st)) return rc;
+  }
+  return PS_OK;
+}
+
+}  // namespace ps

@@ -1,0 +1,82 @@
+// Internal state behind the opaque ps_ctx handle of include/periscat_b200.h.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/periscat_b200.h"
+
+namespace ps {
+
+struct Dev2 {  // tiny RAII-free device buffer record (freed in ps_destroy)
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct RhsData {          // per right-hand side (incidence angle)
+  double2 bloch{1.0, 0.0};
+  // A^+ factors restricted to what the Schur correction touches
+  double2* d_Uh = nullptr;    // [nsv][nrow_c]  = conj(U)^T restricted to C rows
+  double* d_sinv = nullptr;   // [nsv]  min(1/s, 1/eps)
+  double2* d_Vb = nullptr;    // [ncol_b + 2*nrb][nsv] = conj(Vh)^T rows (B cols, c, d)
+  double* d_cscale = nullptr; // [ncol_b + 2*nrb]
+  double2* d_f = nullptr;     // [nrow_c] rhs f restricted to C rows
+};
+
+struct Ctx {
+  int device = 0;
+  int sm_count = 148;
+  std::string err;
+
+  // geometry (all M inclusions; sources)
+  int M = 0, p = -1, L = 0, copies = 1;
+  double period = 1.0, k2 = 1.0;
+  double* d_centers = nullptr;  // [M][2]
+  std::vector<double> h_centers;
+  int t_begin = 0, t_end = 0;   // owned targets [t_begin, t_end)
+
+  // scattering matrix
+  int s_diag = 1;
+  double2* d_S = nullptr;       // [L] or [L][L]
+  double* d_rot = nullptr;      // [M] rotations (dense only), may be null
+
+  // layer coupling (shared by all RHS)
+  int have_layers = 0;
+  int n1 = 0, n2 = 0, nw = 0, Q = 0;
+  double x2[2] = {0, 0};
+  double* d_g1 = nullptr;   // [n1][5]: x, y, nx, ny, w
+  double* d_g2 = nullptr;   // [n2][5]
+  double* d_w2 = nullptr;   // [nw][2] left-wall L2 nodes
+  int nrow_c = 0;           // 2*n1 + 2*n2 + 2*nw
+  int ncol_b = 0;           // 2*n1 + 2*n2 + (2Q+1)
+  int nrb = 0;              // Rayleigh-Bloch orders per direction (c, d)
+  int nsv = 0;              // number of singular values
+
+  // right-hand sides
+  int nrhs = 1;
+  std::vector<RhsData> rhs;
+  double2* d_blochpow = nullptr;  // [nrhs][2*copies+3]: bloch^l, l=-(copies+1)..copies+1
+
+  // workspaces
+  double2* d_partial = nullptr;
+  size_t partial_elems = 0;
+  double2* d_work = nullptr;       // misc per-call workspace
+  size_t work_elems = 0;
+
+  std::vector<void*> owned;        // everything cudaMalloc'ed
+};
+
+inline Ctx* C(ps_ctx* h) { return reinterpret_cast<Ctx*>(h); }
+
+}  // namespace ps
+
+#define PS_CUDA_TRY(ctx, call)                                                 \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) {                                                   \
+      (ctx)->err = std::string(#call) + ": " + cudaGetErrorString(e_);         \
+      return PS_ERR_CUDA;                                                      \
+    }                                                                          \
+  } while (0)

@@ -1,0 +1,341 @@
+// K1: all-pairs Graf M2L translation (multiscat.apply_T, SPEC.md:504-512,
+// PAPER.md:690-692 + 758-763; pinned formula SURVEY.md A.1):
+//
+//   a_m[m'] = sum_{l=-P..P} sum_{j, (l,j) != (0,m)} bloch^l
+//             sum_n beta_j[n] H_{n-m'}(k2 rho) e^{i(n-m') phi},
+//   (rho, phi) = polar(x_m - x_j - l d e_x).
+//
+// Work decomposition (one CTA per SM, persistent over a contiguous range of
+// the (target tile x source batch) work list):
+//   * a target tile is kTT = 8 targets, a source batch kS = 8 source images;
+//   * 2 producer warps build the 64 symbol rows t_{-2p..2p} of the next batch
+//     into shared memory (one pair per lane, bessel.cuh/symbols.cuh) and stage
+//     the batch's bloch-weighted beta vectors;
+//   * 8 consumer warps (one per source image of the current batch) apply the
+//     Toeplitz sums: lane (b, t) owns rows [b*BO, b*BO+BO) of target t and
+//     streams the L columns with a BO-deep sliding window of symbols held in
+//     registers, so every column step is 2 LDS.128 (beta broadcast + one
+//     symbol) against 4*BO DFMA;
+//   * the two roles are double-buffered around one __syncthreads per batch;
+//   * at a tile boundary the 8 consumer warps reduce their accumulators
+//     through shared memory and write one partial per (CTA, tile segment);
+//     m2l_reduce sums the partials in CTA order (deterministic) and applies
+//     the Schur epilogue y = v - S (a - b).
+#include <cuda_runtime.h>
+
+#include "ctx.cuh"
+#include "m2l.cuh"
+#include "symbols.cuh"
+
+namespace ps {
+
+namespace {
+
+constexpr int kTT = 8;                 // targets per tile
+constexpr int kNB = 4;                 // row blocks (lanes) per target
+constexpr int kS = 8;                  // source images per batch = consumer warps
+constexpr int kPW = 2;                 // producer warps
+constexpr int kThreads = (kS + kPW) * 32;
+static_assert(kTT * kNB == 32, "one consumer warp covers a full target tile");
+static_assert(kTT * kS == kPW * 32, "one pair per producer lane");
+
+template <int P>
+struct Shape {
+  static constexpr int L = 2 * P + 1;
+  static constexpr int NS = 4 * P + 1;
+  static constexpr int BO = (L + kNB - 1) / kNB;
+  static constexpr int ROWS = BO * kNB;
+  static constexpr int FP = ROWS - L;          // zero pad in front of t_{-2p}
+  static constexpr int NSP = FP + NS + 1;      // + one tail slot for the prefetch
+  static constexpr int SYM = kS * NSP * kTT;   // double2 per symbol buffer
+  static constexpr int BET = kS * L;           // double2 per beta buffer
+  static constexpr size_t SMEM = 2 * (size_t)(SYM + BET) * sizeof(double2);
+};
+
+struct Args {
+  const double* centers;   // [M][2]
+  const double2* beta;     // [M][L]
+  const double2* bpow;     // [2*copies+1]
+  double2* partial;        // [G][maxseg][kTT][L]
+  int M, t_begin, nt, copies, ncp, nimg, nbatch, maxseg;
+  long long W;
+  double period, k2;
+};
+
+__device__ __forceinline__ long long work_begin(long long W, int G, int c) {
+  return (W * (long long)c) / G;
+}
+
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync 1, %0;" ::"r"(kS * 32) : "memory");
+}
+
+template <int P>
+__device__ __forceinline__ void produce(const Args& a, long long w, double2* sym, double2* bet,
+                                        int pi) {
+  using S = Shape<P>;
+  const int tile = (int)(w / a.nbatch);
+  const int sb = (int)(w % a.nbatch) * kS;
+  const int s = pi / kTT, t = pi % kTT;
+  const int mloc = tile * kTT + t;
+  const int g = sb + s;
+  double2* col = sym + (size_t)s * S::NSP * kTT + t;   // slot stride kTT
+  bool live = (mloc < a.nt) && (g < a.nimg);
+  double dx = 0.0, dy = 0.0;
+  if (live) {
+    const int m = a.t_begin + mloc;
+    const int j = g / a.ncp;
+    const int l = g % a.ncp - a.copies;
+    const double2 cm = reinterpret_cast<const double2*>(a.centers)[m];
+    const double2 cj = reinterpret_cast<const double2*>(a.centers)[j];
+    dx = cm.x - cj.x - (double)l * a.period;
+    dy = cm.y - cj.y;
+    live = !(l == 0 && j == m);
+  }
+  if (!live) {
+    for (int q = S::FP; q < S::FP + S::NS; ++q) col[q * kTT] = make_double2(0.0, 0.0);
+  } else {
+    const double rho = hypot(dx, dy);
+    const double inv = 1.0 / rho;
+    double2* base = col + (S::FP + 2 * P) * kTT;
+    hankel_symbols<2 * P>(
+        a.k2 * rho, dx * inv, dy * inv,
+        [&](int nu, double v) { base[nu * kTT].x = v; },
+        [&](int nu) { return base[nu * kTT].x; },
+        [&](int nu, double re, double im) { base[nu * kTT] = make_double2(re, im); });
+  }
+  // bloch-weighted beta of the batch's source images
+  for (int idx = pi; idx < kS * S::L; idx += kPW * 32) {
+    const int s2 = idx / S::L, n = idx % S::L;
+    const int g2 = sb + s2;
+    double2 v = make_double2(0.0, 0.0);
+    if (g2 < a.nimg) {
+      const int j2 = g2 / a.ncp;
+      const double2 b = a.beta[(size_t)j2 * S::L + n];
+      const double2 wgt = a.bpow[g2 % a.ncp];
+      v.x = fma(b.x, wgt.x, -b.y * wgt.y);
+      v.y = fma(b.x, wgt.y, b.y * wgt.x);
+    }
+    bet[idx] = v;
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void consume(const double2* __restrict__ sym,
+                                        const double2* __restrict__ bet,
+                                        double2 (&acc)[Shape<P>::BO], int b, int t) {
+  using S = Shape<P>;
+  constexpr int BO = S::BO;
+  constexpr int R0 = S::FP + 2 * P;              // slot of nu = 0 - 0 at step 0
+  constexpr int MODB = 64 * BO;                  // keeps ring indices non-negative
+  const double2* sp = sym + (size_t)(R0 - b * BO) * kTT + t;
+  double2 w[BO];
+#pragma unroll
+  for (int i = 0; i < BO; ++i) w[(R0 - i + MODB) % BO] = sp[-i * kTT];
+#pragma unroll
+  for (int n = 0; n < S::L; ++n) {
+    const double2 nxt = sp[(n + 1) * kTT];
+    const double2 bb = bet[n];
+    const double nby = -bb.y;
+#pragma unroll
+    for (int i = 0; i < BO; ++i) {
+      const double2 tt = w[(R0 + n - i + MODB) % BO];
+      acc[i].x = fma(bb.x, tt.x, acc[i].x);
+      acc[i].x = fma(nby, tt.y, acc[i].x);
+      acc[i].y = fma(bb.x, tt.y, acc[i].y);
+      acc[i].y = fma(bb.y, tt.x, acc[i].y);
+    }
+    w[(R0 + n + 1 + MODB) % BO] = nxt;
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(kThreads, 1) m2l_kernel(Args a) {
+  using S = Shape<P>;
+  constexpr int BO = S::BO;
+  extern __shared__ double2 smem[];
+  double2* sym0 = smem;
+  double2* sym1 = smem + S::SYM;
+  double2* bet0 = smem + 2 * S::SYM;
+  double2* bet1 = bet0 + S::BET;
+
+  const int G = gridDim.x;
+  const long long w0 = work_begin(a.W, G, blockIdx.x);
+  const long long w1 = work_begin(a.W, G, blockIdx.x + 1);
+  if (w0 >= w1) return;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp >= kS;
+  const int pi = threadIdx.x - kS * 32;
+
+  // zero the pad slots of both symbol buffers once (only padded rows read them)
+  for (int idx = threadIdx.x; idx < 2 * kS * kTT * (S::FP + 1); idx += kThreads) {
+    const int buf = idx / (kS * kTT * (S::FP + 1));
+    const int r = idx % (kS * kTT * (S::FP + 1));
+    const int s = r / (kTT * (S::FP + 1));
+    const int r2 = r % (kTT * (S::FP + 1));
+    const int q = r2 / kTT, t = r2 % kTT;
+    const int slot = q < S::FP ? q : S::FP + S::NS;
+    (buf ? sym1 : sym0)[((size_t)s * S::NSP + slot) * kTT + t] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  if (producer) produce<P>(a, w0, sym0, bet0, pi);
+  __syncthreads();
+
+  double2 acc[BO];
+#pragma unroll
+  for (int i = 0; i < BO; ++i) acc[i] = make_double2(0.0, 0.0);
+  const int b = lane / kTT, t = lane % kTT;
+  int seg = 0;
+
+  for (long long w = w0; w < w1; ++w) {
+    const int cur = (int)((w - w0) & 1);
+    double2* symc = cur ? sym1 : sym0;
+    double2* betc = cur ? bet1 : bet0;
+    if (producer) {
+      if (w + 1 < w1) produce<P>(a, w + 1, cur ? sym0 : sym1, cur ? bet0 : bet1, pi);
+    } else {
+      consume<P>(symc + (size_t)warp * S::NSP * kTT, betc + warp * S::L, acc, b, t);
+      const bool flush = (w + 1 == w1) || ((w + 1) % a.nbatch == 0);
+      if (flush) {
+        // cross-warp reduction through the (now idle) current symbol buffer
+        consumer_bar();
+        double2* red = symc;   // [kS][kTT][ROWS]
+#pragma unroll
+        for (int i = 0; i < BO; ++i)
+          red[((size_t)warp * kTT + t) * S::ROWS + b * BO + i] = acc[i];
+        consumer_bar();
+        const int tile = (int)(w / a.nbatch);
+        double2* dst = a.partial + ((size_t)blockIdx.x * a.maxseg + seg) * kTT * S::L;
+        for (int idx = threadIdx.x; idx < kTT * S::L; idx += kS * 32) {
+          const int tt = idx / S::L, r = idx % S::L;
+          double2 sum = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int ww = 0; ww < kS; ++ww) {
+            const double2 v = red[((size_t)ww * kTT + tt) * S::ROWS + r];
+            sum.x += v.x;
+            sum.y += v.y;
+          }
+          dst[idx] = sum;
+        }
+        (void)tile;
+        ++seg;
+#pragma unroll
+        for (int i = 0; i < BO; ++i) acc[i] = make_double2(0.0, 0.0);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Sum the per-(CTA, tile-segment) partials of every owned target in CTA order
+// and apply the epilogue:
+//   mode 0: out = a
+//   mode 1: out = v_own - s .* (a - bsub)        (diagonal S)
+//   mode 2: out = a - bsub                       (dense S applied afterwards)
+__global__ void m2l_reduce(const double2* __restrict__ partial, int G, long long W, int nbatch,
+                           int maxseg, int nt, int L, int mode, const double2* __restrict__ v_own,
+                           const double2* __restrict__ sdiag, const double2* __restrict__ bsub,
+                           double2* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nt * L) return;
+  const int mloc = idx / L, r = idx % L;
+  const int tile = mloc / kTT, t = mloc % kTT;
+  const long long wa = (long long)tile * nbatch, wb = wa + nbatch;
+  int c = (int)((wa * G) / W);
+  if (c >= G) c = G - 1;
+  while (c > 0 && work_begin(W, G, c) > wa) --c;
+  while (c < G - 1 && work_begin(W, G, c + 1) <= wa) ++c;
+  double2 sum = make_double2(0.0, 0.0);
+  for (; c < G; ++c) {
+    const long long c0 = work_begin(W, G, c), c1 = work_begin(W, G, c + 1);
+    if (c0 >= wb) break;
+    if (c1 <= c0 || c1 <= wa) continue;
+    const int seg = tile - (int)(c0 / nbatch);
+    const double2 v = partial[(((size_t)c * maxseg + seg) * kTT + t) * L + r];
+    sum.x += v.x;
+    sum.y += v.y;
+  }
+  if (mode == 0) {
+    out[idx] = sum;
+    return;
+  }
+  if (bsub) {
+    sum.x -= bsub[idx].x;
+    sum.y -= bsub[idx].y;
+  }
+  if (mode == 2) {
+    out[idx] = sum;
+    return;
+  }
+  const double2 s = sdiag[r];
+  const double2 vv = v_own[idx];
+  out[idx] = make_double2(vv.x - fma(s.x, sum.x, -s.y * sum.y), vv.y - fma(s.x, sum.y, s.y * sum.x));
+}
+
+template <int P>
+int launch_p(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
+             const double2* v_own, const double2* bsub, cudaStream_t st) {
+  using S = Shape<P>;
+  Args a;
+  a.centers = ctx->d_centers;
+  a.beta = beta;
+  a.bpow = bpow;
+  a.M = ctx->M;
+  a.t_begin = ctx->t_begin;
+  a.nt = ctx->t_end - ctx->t_begin;
+  a.copies = ctx->copies;
+  a.ncp = 2 * ctx->copies + 1;
+  a.nimg = ctx->M * a.ncp;
+  a.nbatch = (a.nimg + kS - 1) / kS;
+  const int ntiles = (a.nt + kTT - 1) / kTT;
+  a.W = (long long)ntiles * a.nbatch;
+  a.period = ctx->period;
+  a.k2 = ctx->k2;
+  if (a.nt <= 0) return PS_OK;
+  int G = ctx->sm_count;
+  if ((long long)G > a.W) G = (int)a.W;
+  a.maxseg = (int)((a.W / G + 1) / a.nbatch) + 2;
+  const size_t need = (size_t)G * a.maxseg * kTT * S::L;
+  if (ctx->partial_elems < need) {
+    if (ctx->d_partial) cudaFree(ctx->d_partial);
+    ctx->d_partial = nullptr;
+    ctx->partial_elems = 0;
+    PS_CUDA_TRY(ctx, cudaMalloc(&ctx->d_partial, need * sizeof(double2)));
+    ctx->partial_elems = need;
+  }
+  a.partial = ctx->d_partial;
+  static bool attr_done = false;
+  if (!attr_done) {
+    PS_CUDA_TRY(ctx, cudaFuncSetAttribute(m2l_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)S::SMEM));
+    attr_done = true;
+  }
+  m2l_kernel<P><<<G, kThreads, S::SMEM, st>>>(a);
+  PS_CUDA_TRY(ctx, cudaGetLastError());
+  const int n = a.nt * S::L;
+  m2l_reduce<<<(n + 255) / 256, 256, 0, st>>>(ctx->d_partial, G, a.W, a.nbatch, a.maxseg, a.nt,
+                                              S::L, mode, v_own, ctx->d_S, bsub, out);
+  PS_CUDA_TRY(ctx, cudaGetLastError());
+  return PS_OK;
+}
+
+}  // namespace
+
+int m2l_max_order() { return PS_M2L_MAX_P; }
+
+int m2l_apply(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
+              const double2* v_own, const double2* bsub, cudaStream_t st) {
+  switch (ctx->p) {
+#define PS_CASE(P) \
+  case P:          \
+    return launch_p<P>(ctx, beta, bpow, out, mode, v_own, bsub, st);
+    PS_M2L_ORDERS(PS_CASE)
+#undef PS_CASE
+    default:
+      ctx->err = "apply_T: multipole order p=" + std::to_string(ctx->p) + " not compiled";
+      return PS_ERR_UNSUPPORTED;
+  }
+}
+
+}  // namespace ps

@@ -1,0 +1,17 @@
+#pragma once
+#include <cuda_runtime.h>
+
+#include "ctx.cuh"
+
+// Multipole orders p the M2L kernel is instantiated for.
+#define PS_M2L_MAX_P 25
+#define PS_M2L_ORDERS(X)                                                                 \
+  X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) \
+  X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25)
+
+namespace ps {
+int m2l_max_order();
+// out: [nt][L] for the owned targets; see m2l.cu for the epilogue modes.
+int m2l_apply(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
+              const double2* v_own, const double2* bsub, cudaStream_t st);
+}  // namespace ps

@@ -1,0 +1,222 @@
+"""Device context: one ``ps_ctx`` per (process, GPU) holding the uploaded
+geometry, scattering matrix, layer-coupling data and SVD factors.
+
+Memory and streams come from PyTorch (complex128 CUDA tensors, the current
+stream); all arithmetic runs in libperiscat_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .grating import factorize
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _c128(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
+
+
+def _f64(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class Engine:
+    """Thin owner of a ps_ctx.  All tensors passed in must be complex128 on
+    ``self.device`` and contiguous."""
+
+    def __init__(self, device: int | torch.device | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1412_7466_b200 needs a CUDA device (no CPU fallback)")
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        self.lib = _lib.load()
+        self.ctx = ctypes.c_void_p()
+        rc = self.lib.ps_create(ctypes.byref(self.ctx), self.device.index)
+        _lib.check(self.ctx, rc)
+        self.M = 0
+        self.p = -1
+        self.L = 0
+        self.nrhs = 1
+        self.t_range = (0, 0)
+        self.coupled = False
+        self.nrow_c = 0
+        self.nout = 0
+        self.ncol_b = 0
+        self.nrb = 0
+
+    def close(self):
+        if self.ctx:
+            self.lib.ps_destroy(self.ctx)
+            self.ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        _lib.check(self.ctx, rc)
+
+    # ---------------------------------------------------------------- setup
+    def set_geometry(self, centers, p: int, k2: float, period: float = 1.0, copies: int = 1):
+        c = _f64(centers).reshape(-1, 2)
+        self._check(self.lib.ps_set_geometry(self.ctx, c.shape[0], int(p), int(copies),
+                                             float(period), float(k2), _ptr(c)))
+        self.M, self.p, self.L = c.shape[0], int(p), 2 * int(p) + 1
+        self.copies = int(copies)
+        self.t_range = (0, self.M)
+
+    def set_target_range(self, t0: int, t1: int):
+        self._check(self.lib.ps_set_target_range(self.ctx, int(t0), int(t1)))
+        self.t_range = (int(t0), int(t1))
+
+    @property
+    def n_own(self) -> int:
+        return self.t_range[1] - self.t_range[0]
+
+    def set_bloch(self, bloch):
+        b = _c128(np.atleast_1d(bloch))
+        self._check(self.lib.ps_set_rhs_bloch(self.ctx, b.size, _ptr(b)))
+        self.nrhs = b.size
+
+    def set_smatrix(self, S, rot=None):
+        S = _c128(S)
+        diag = 1 if S.ndim == 1 else 0
+        r = None if rot is None else _f64(rot)
+        self._check(self.lib.ps_set_smatrix(self.ctx, _ptr(S), diag,
+                                            None if r is None else _ptr(r)))
+
+    def set_layers(self, system):
+        """Curves + expansion centre of a (reference or fixture) empty-grating system."""
+        cv = system.curves
+        g = []
+        for name in ("g1", "g2"):
+            c = cv[name]
+            g.append(_f64(np.column_stack([c.nodes, c.normals, c.arc_weights])))
+        w2 = _f64(cv["L2"].nodes)
+        x2 = _f64(system.centers[2])
+        cfg = system.config
+        Q = int(cfg.j_expansion_order)
+        nrb = int(cfg.rb_modes_per_direction)
+        self._check(self.lib.ps_set_layers(self.ctx, g[0].shape[0], _ptr(g[0]), g[1].shape[0],
+                                           _ptr(g[1]), w2.shape[0], _ptr(w2), _ptr(x2), Q, nrb))
+        n1, n2, nw = g[0].shape[0], g[1].shape[0], w2.shape[0]
+        self.nrow_c = 2 * n1 + 2 * n2 + 2 * nw
+        self.ncol_b = 2 * n1 + 2 * n2 + 2 * Q + 1
+        self.nrb = nrb
+        self.nout = self.ncol_b + 2 * nrb
+        self._layer_cols = system.cols
+
+    def set_pinv(self, irhs: int, system):
+        """Upload the SVD factors of one RHS's system (computed if absent)."""
+        factorize(system)
+        u, s, vh = system.svd
+        u, s, vh = _c128(u), _f64(s), _c128(vh)
+        cs = _f64(system.col_scale)
+        f = _c128(system.rhs)
+        eps = float(system.config.regularization)
+        self._check(self.lib.ps_set_pinv(self.ctx, int(irhs), u.shape[0], u.shape[1], _ptr(u),
+                                         _ptr(s), _ptr(vh), _ptr(cs), eps, _ptr(f),
+                                         system.cols["c"].start, system.cols["d"].start))
+        self.coupled = True
+
+    # ---------------------------------------------------------------- apply
+    def _dev(self, x, shape):
+        if not isinstance(x, torch.Tensor) or x.device != self.device or x.dtype != torch.complex128 \
+                or not x.is_contiguous():
+            raise TypeError(f"expected a contiguous complex128 tensor on {self.device}")
+        if tuple(x.shape) != tuple(shape):
+            raise ValueError(f"expected shape {tuple(shape)}, got {tuple(x.shape)}")
+        return ctypes.c_void_p(x.data_ptr())
+
+    def empty_own(self):
+        return torch.empty((self.nrhs, self.n_own, self.L), dtype=torch.complex128,
+                           device=self.device)
+
+    def apply_T(self, beta: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        out = self.empty_own() if out is None else out
+        b = self._dev(beta, (self.nrhs, self.M, self.L))
+        o = self._dev(out, (self.nrhs, self.n_own, self.L))
+        self._check(self.lib.ps_apply_T(self.ctx, b, o, _stream(self.device)))
+        return out
+
+    def apply_C(self, beta: torch.Tensor, s_range=None, out=None) -> torch.Tensor:
+        s0, s1 = (0, self.M) if s_range is None else s_range
+        out = torch.empty((self.nrhs, self.nrow_c), dtype=torch.complex128,
+                          device=self.device) if out is None else out
+        b = self._dev(beta, (self.nrhs, self.M, self.L))
+        o = self._dev(out, (self.nrhs, self.nrow_c))
+        self._check(self.lib.ps_apply_C(self.ctx, b, o, int(s0), int(s1), _stream(self.device)))
+        return out
+
+    def apply_schur(self, v: torch.Tensor, out=None, g: torch.Tensor | None = None) -> torch.Tensor:
+        out = self.empty_own() if out is None else out
+        vp = self._dev(v, (self.nrhs, self.M, self.L))
+        o = self._dev(out, (self.nrhs, self.n_own, self.L))
+        if g is None:
+            self._check(self.lib.ps_apply_schur(self.ctx, vp, o, _stream(self.device)))
+        else:
+            gp = self._dev(g, (self.nrhs, self.nrow_c))
+            self._check(self.lib.ps_apply_schur_g(self.ctx, vp, gp, o, _stream(self.device)))
+        return out
+
+    def schur_rhs(self, out=None) -> torch.Tensor:
+        out = self.empty_own() if out is None else out
+        o = self._dev(out, (self.nrhs, self.n_own, self.L))
+        self._check(self.lib.ps_schur_rhs(self.ctx, o, _stream(self.device)))
+        return out
+
+    def recover(self, g: torch.Tensor, out=None) -> torch.Tensor:
+        out = torch.empty((self.nrhs, self.nout), dtype=torch.complex128,
+                          device=self.device) if out is None else out
+        gp = self._dev(g, (self.nrhs, self.nrow_c))
+        o = self._dev(out, (self.nrhs, self.nout))
+        self._check(self.lib.ps_recover(self.ctx, gp, o, _stream(self.device)))
+        return out
+
+    def gmres(self, rhs: torch.Tensor, tol: float = 1e-10, maxit: int = 150):
+        x = torch.empty_like(rhs)
+        r = self._dev(rhs, (self.nrhs, self.M, self.L))
+        xp = self._dev(x, (self.nrhs, self.M, self.L))
+        iters = (ctypes.c_int * self.nrhs)()
+        hist = np.full((self.nrhs, maxit + 1), np.nan)
+        self._check(self.lib.ps_gmres(self.ctx, r, xp, float(tol), int(maxit), iters,
+                                      hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                      _stream(self.device)))
+        return x, list(iters), hist
+
+    # GMRES building blocks for the multi-rank driver
+    def block_dot(self, V: torch.Tensor, w: torch.Tensor, k: int, h: torch.Tensor):
+        kmax, nrhs, n = V.shape
+        self._check(self.lib.ps_block_dot(self.ctx, nrhs, n, int(k), kmax,
+                                          ctypes.c_void_p(V.data_ptr()),
+                                          ctypes.c_void_p(w.data_ptr()),
+                                          ctypes.c_void_p(h.data_ptr()), _stream(self.device)))
+        return h
+
+    def block_axpy(self, V: torch.Tensor, h: torch.Tensor, k: int, w: torch.Tensor):
+        kmax, nrhs, n = V.shape
+        self._check(self.lib.ps_block_axpy(self.ctx, nrhs, n, int(k), kmax,
+                                           ctypes.c_void_p(V.data_ptr()),
+                                           ctypes.c_void_p(h.data_ptr()),
+                                           ctypes.c_void_p(w.data_ptr()), _stream(self.device)))
+        return w
+
+    def norm2(self, w: torch.Tensor, out: torch.Tensor):
+        nrhs, n = w.shape
+        self._check(self.lib.ps_norm2(self.ctx, nrhs, n, ctypes.c_void_p(w.data_ptr()),
+                                      ctypes.c_void_p(out.data_ptr()), _stream(self.device)))
+        return out

@@ -1,0 +1,133 @@
+"""Coupled solve on the B200 (solver).
+
+``SchurOperator`` is the device-resident S-preconditioned Schur operator
+    K v = v - S T v + S B_phys A^+ C v         (paper B = -B_phys)
+for one or more right-hand sides (incidence angles sharing k2); ``gmres``
+runs the device GMRES of libperiscat_b200.so; ``solve_full`` mirrors
+SPEC.md:559-567.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import postproc
+from .engine import Engine
+from .scatmat import disk_scattering_matrix
+
+
+class SchurOperator:
+    def __init__(self, systems, centers, p: int, smat=None, radius: float | None = None,
+                 rot=None, device=None, target_range=None, coupled: bool = True,
+                 engine: Engine | None = None):
+        if not isinstance(systems, (list, tuple)):
+            systems = [systems]
+        self.systems = list(systems)
+        cfg = self.systems[0].config
+        self.config = cfg
+        for s in self.systems[1:]:
+            if (s.config.k2, s.config.period, s.config.near_field_copies) != \
+                    (cfg.k2, cfg.period, cfg.near_field_copies):
+                raise ValueError("batched right-hand sides must share k2, period and copies")
+        if smat is None:
+            if radius is None:
+                raise ValueError("give a scattering matrix or a disk radius")
+            smat = disk_scattering_matrix(radius, cfg.k2, cfg.kp, p)
+        self.smat = np.asarray(smat, dtype=complex)
+        self.eng = engine or Engine(device)
+        eng = self.eng
+        self.centers = np.ascontiguousarray(np.asarray(centers, dtype=float).reshape(-1, 2))
+        eng.set_geometry(self.centers, p, cfg.k2, cfg.period, cfg.near_field_copies)
+        eng.set_bloch([s.config.bloch_phase for s in self.systems])
+        eng.set_smatrix(self.smat, rot)
+        self.coupled = coupled
+        if coupled:
+            eng.set_layers(self.systems[0])
+            for r, s in enumerate(self.systems):
+                eng.set_pinv(r, s)
+        if target_range is not None:
+            eng.set_target_range(*target_range)
+        self.M, self.p, self.L, self.nrhs = eng.M, p, eng.L, eng.nrhs
+        self.device = eng.device
+
+    @property
+    def shape(self):
+        return (self.nrhs, self.M, self.L)
+
+    def __call__(self, v: torch.Tensor, out=None, g=None) -> torch.Tensor:
+        return self.eng.apply_schur(v, out=out, g=g)
+
+    def apply_T(self, v: torch.Tensor, out=None) -> torch.Tensor:
+        return self.eng.apply_T(v, out=out)
+
+    def rhs(self) -> torch.Tensor:
+        if not self.coupled:
+            raise RuntimeError("uncoupled operator has no layer right-hand side")
+        return self.eng.schur_rhs()
+
+    def recover(self, beta: torch.Tensor):
+        """x_empty restricted to (B columns, c, d) = A^+ (f - C beta) per RHS."""
+        g = self.eng.apply_C(beta)
+        x = self.eng.recover(g)
+        return x
+
+    def split_cd(self, x: torch.Tensor):
+        nb, nrb = self.eng.ncol_b, self.eng.nrb
+        xh = x.cpu().numpy()
+        return xh[:, nb:nb + nrb], xh[:, nb + nrb:nb + 2 * nrb]
+
+
+def apply_schur_operator(op: SchurOperator, beta):
+    """returns K beta.  Host arrays round-trip through the device."""
+    on_host = not isinstance(beta, torch.Tensor)
+    v = torch.as_tensor(np.asarray(beta, dtype=complex).reshape(op.shape) if on_host else beta)
+    v = v.to(device=op.device, dtype=torch.complex128).contiguous()
+    y = op(v)
+    return y.cpu().numpy() if on_host else y
+
+
+def gmres(op: SchurOperator, rhs, tol: float = 1e-10, maxit: int = 150):
+    """Unrestarted device GMRES.  Returns (x, iterations per
+    RHS, residual history per RHS)."""
+    on_host = not isinstance(rhs, torch.Tensor)
+    r = torch.as_tensor(np.asarray(rhs, dtype=complex).reshape(op.shape) if on_host else rhs)
+    r = r.to(device=op.device, dtype=torch.complex128).contiguous()
+    x, its, hist = op.eng.gmres(r, tol, maxit)
+    hist_l = [h[~np.isnan(h)].tolist() for h in hist]
+    return (x.cpu().numpy() if on_host else x), its, hist_l
+
+
+@dataclass
+class Solution:
+    beta: np.ndarray          # [nrhs][M][L]
+    c: np.ndarray             # [nrhs][nrb]
+    d: np.ndarray             # [nrhs][nrb]
+    iterations: list
+    history: list
+    flux: list = field(default_factory=list)
+    timings: dict = field(default_factory=dict)
+
+
+def solve_full(systems, centers, p: int, radius: float | None = None, smat=None, rot=None,
+               tol: float | None = None, maxit: int | None = None, device=None) -> Solution:
+    """beta from GMRES on (I - S T - S B A^+ C) beta = -S B A^+ f,
+    then x_empty = A^+ (f - C beta); flux balance per RHS."""
+    import time
+    t0 = time.perf_counter()
+    op = SchurOperator(systems, centers, p, smat=smat, radius=radius, rot=rot, device=device)
+    torch.cuda.synchronize(op.device)
+    t1 = time.perf_counter()
+    cfg = op.config
+    tol = cfg.gmres_tol if tol is None else tol
+    maxit = cfg.gmres_maxit if maxit is None else maxit
+    rhs = op.rhs()
+    beta, its, hist = gmres(op, rhs, tol, maxit)
+    x = op.recover(beta)
+    c, d = op.split_cd(x)
+    torch.cuda.synchronize(op.device)
+    t2 = time.perf_counter()
+    flux = [postproc.flux_error(c[r], d[r], s.config) for r, s in enumerate(op.systems)]
+    return Solution(beta.cpu().numpy(), c, d, its, hist, flux,
+                    dict(setup=t1 - t0, solve=t2 - t1))
