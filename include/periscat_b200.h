@@ -138,6 +138,14 @@ int ps_norm2(ps_ctx* ctx, int nrhs, int n, const void* w_dev, double* nrm2_dev, 
 int ps_gmres(ps_ctx* ctx, const void* rhs_dev, void* x_dev, double tol, int maxit,
              int* iters_host, double* hist_host, void* stream);
 
+/* ---- instrumentation ---------------------------------------------------- */
+/* Record CUDA events around every K1 (M2L) launch of this context. */
+int ps_profile(ps_ctx* ctx, int enable);
+/* Kernel launches issued so far, and total/launch count of timed K1 runs
+ * (synchronises on the recorded events). */
+int ps_stats(ps_ctx* ctx, long long* launches, double* k1_ms, long long* k1_count);
+int ps_stats_reset(ps_ctx* ctx);
+
 /* ---- roofline denominator ---------------------------------------------- */
 /* DFMA-chain FP64 throughput of the device (TFLOP/s, 2 flops per FMA). */
 int ps_dfma_peak(int device, double* tflops, double* ms);

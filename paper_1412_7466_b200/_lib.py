@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libperiscat_b200.so")
+LIB_PATH = os.environ.get("PS_LIB", os.path.join(_HERE, "libperiscat_b200.so"))
 
 PS_OK, PS_ERR_ARG, PS_ERR_DOMAIN, PS_ERR_NUMERICAL, PS_ERR_CUDA, PS_ERR_STATE, PS_ERR_UNSUPPORTED = range(7)
 
@@ -42,6 +42,9 @@ SIGNATURES = {
     "ps_norm2": (_I, [_P, _I, _I, _P, _P, _P]),
     "ps_gmres": (_I, [_P, _P, _P, _D, _I, _IP, _DP, _P]),
     "ps_dfma_peak": (_I, [_I, _DP, _DP]),
+    "ps_profile": (_I, [_P, _I]),
+    "ps_stats": (_I, [_P, ctypes.POINTER(ctypes.c_longlong), _DP, ctypes.POINTER(ctypes.c_longlong)]),
+    "ps_stats_reset": (_I, [_P]),
 }
 
 _lib = None

@@ -27,35 +27,38 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    if not force and out == LIB and not _stale():
         return LIB
     objs = []
     t0 = time.time()
     procs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(CSRC, src.replace(".cu", f".{os.getpid()}.o"))
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                             text=True)))
         objs.append(obj)
     log = []
     for src, p in procs:
-        out, _ = p.communicate()
-        log.append(f"== {src}\n{out}")
+        txt, _ = p.communicate()
+        log.append(f"== {src}\n{txt}")
         if p.returncode != 0:
-            sys.stderr.write(out)
+            sys.stderr.write(txt)
             raise RuntimeError(f"nvcc failed on {src}")
     with open(os.path.join(CSRC, "ptxas.log"), "w") as fh:
         fh.write("\n".join(log))
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs]
     subprocess.run(cmd, check=True)
     for o in objs:
         os.remove(o)
     if verbose:
-        print(f"built {LIB} in {time.time() - t0:.1f}s")
-    return LIB
+        print(f"built {out} in {time.time() - t0:.1f}s")
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    build(force="--force" in sys.argv or bool(defs), verbose=True,
+          out=outs[0] if outs else LIB, defines=defs)

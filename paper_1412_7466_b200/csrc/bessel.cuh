@@ -39,6 +39,23 @@ static __constant__ double c_inv_int[128] = {
     0.0, 1.0, 0.5, 1.0 / 3.0, PS_I4(4), PS_I4(8), PS_I4(12), PS_I16(16),
     PS_I16(32), PS_I16(48), PS_I16(64), PS_I16(80), PS_I16(96), PS_I16(112)};
 #endif
+// (-1)^k / k
+#define PS_S4(k) (((k) & 1) ? -1.0 : 1.0) / (k), (((k) + 1) & 1 ? -1.0 : 1.0) / ((k) + 1), \
+                 (((k) + 2) & 1 ? -1.0 : 1.0) / ((k) + 2), (((k) + 3) & 1 ? -1.0 : 1.0) / ((k) + 3)
+#define PS_S16(k) PS_S4(k), PS_S4((k) + 4), PS_S4((k) + 8), PS_S4((k) + 12)
+#ifdef __CUDACC__
+static __constant__ double c_sinv_int[128] = {
+    0.0, -1.0, 0.5, -1.0 / 3.0, PS_S4(4), PS_S4(8), PS_S4(12), PS_S16(16),
+    PS_S16(32), PS_S16(48), PS_S16(64), PS_S16(80), PS_S16(96), PS_S16(112)};
+#endif
+PS_HD double sinv_int(int k) {
+#if defined(__CUDA_ARCH__)
+  return k < 128 ? c_sinv_int[k] : ((k & 1) ? -1.0 : 1.0) / (double)k;
+#else
+  return ((k & 1) ? -1.0 : 1.0) / (double)k;
+#endif
+}
+
 PS_HD double inv_int(int k) {
 #if defined(__CUDA_ARCH__)
   return k < 128 ? c_inv_int[k] : 1.0 / (double)k;
@@ -102,6 +119,41 @@ PS_HD void bessel_jy_sweep(double z, int nmax, Store store, double* inv_norm,
   *y0 = c * (lg * J0) - 2.0 * c * (s0 * inv);
   *y1 = c * (lg * J1) - c * J0 / z + c * (s1 * inv);
   *inv_norm = inv;
+}
+
+// Even Miller start index sufficient for J_0, J_1 (and the Neumann sums) to
+// double accuracy; callers may pass any larger even value (e.g. a warp max).
+PS_HD int miller_start_j01(double z) {
+  double zc = z > 1.0 ? z : 1.0;
+  int n = (int)(z + 18.0 + 6.0 * cbrt(zc));
+  return (n + 1) & ~1;
+}
+
+// J0, J1, Y0, Y1 of z > 0 from a Miller sweep started at even N (no stores).
+PS_HD void bessel_jy01(double z, int N, double* j0, double* j1, double* y0, double* y1) {
+  const double tz = 2.0 / z;
+  double jp1 = 0.0, j = 1e-280;
+  double sum_even = 0.0, s0 = 0.0, s1 = 0.0;
+  double dnu = (double)N;        // exact small integers: no drift in nu * 2/z
+  for (int nu = N; nu >= 2; nu -= 2) {
+    const double sk = sinv_int(nu >> 1);   // (-1)^k / k, k = nu/2
+    sum_even += j;
+    s0 = fma(sk, j, s0);
+    const double jm1 = fma(dnu * tz, j, -jp1);
+    const double jm2 = fma((dnu - 1.0) * tz, jm1, -j);
+    s1 = fma(sk, jm1 - jp1, s1);
+    jp1 = jm1;
+    j = jm2;
+    dnu -= 2.0;
+  }
+  const double inv = 1.0 / (j + 2.0 * sum_even);
+  const double J0 = j * inv, J1 = jp1 * inv;
+  const double lg = log(0.5 * z) + kEulerGamma;
+  const double c = 2.0 / kPi;
+  *j0 = J0;
+  *j1 = J1;
+  *y0 = c * (lg * J0) - 2.0 * c * (s0 * inv);
+  *y1 = c * (lg * J1) - c * J0 / z + c * (s1 * inv);
 }
 
 }  // namespace ps

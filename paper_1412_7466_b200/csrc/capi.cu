@@ -413,6 +413,46 @@ int ps_norm2(ps_ctx* h, int nrhs, int n, const void* w, double* nrm2, void* stre
                    reinterpret_cast<cudaStream_t>(stream));
 }
 
+int ps_profile(ps_ctx* h, int enable) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  c->profile = enable ? 1 : 0;
+  return PS_OK;
+}
+
+int ps_stats(ps_ctx* h, long long* launches, double* k1_ms, long long* k1_count) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  // fold completed K1 event pairs into the running total
+  for (auto& e : c->k1_events) {
+    PS_CUDA_TRY(c, cudaEventSynchronize(e.second));
+    float ms = 0.f;
+    PS_CUDA_TRY(c, cudaEventElapsedTime(&ms, e.first, e.second));
+    c->k1_ms += ms;
+    c->k1_count += 1;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  c->k1_events.clear();
+  if (launches) *launches = c->launches;
+  if (k1_ms) *k1_ms = c->k1_ms;
+  if (k1_count) *k1_count = c->k1_count;
+  return PS_OK;
+}
+
+int ps_stats_reset(ps_ctx* h) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  long long l;
+  double m;
+  long long k;
+  if (int rc = ps_stats(h, &l, &m, &k)) return rc;
+  c->launches = 0;
+  c->k1_ms = 0.0;
+  c->k1_count = 0;
+  return PS_OK;
+}
+
 int ps_gmres(ps_ctx* h, const void* rhs, void* x, double tol, int maxit, int* iters,
              double* hist, void* stream) {
   if (!h) return PS_ERR_ARG;

@@ -41,25 +41,13 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
   return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
 }
 
-// deterministic block reduction of two complex values over kCT threads
-__device__ void block_sum2(double2& a, double2& b, double2* sh /*[2*kCT]*/) {
-  sh[threadIdx.x] = a;
-  sh[kCT + threadIdx.x] = b;
-  __syncthreads();
-  for (int s = kCT / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      sh[threadIdx.x].x += sh[threadIdx.x + s].x;
-      sh[threadIdx.x].y += sh[threadIdx.x + s].y;
-      sh[kCT + threadIdx.x].x += sh[kCT + threadIdx.x + s].x;
-      sh[kCT + threadIdx.x].y += sh[kCT + threadIdx.x + s].y;
-    }
-    __syncthreads();
-  }
-  a = sh[0];
-  b = sh[kCT];
-}
-
 // ---------------------------------------------------------------- K3: C beta
+// grid (target node, source split).  With w_nu = H_nu(k r) e^{i nu theta} about a
+// source image evaluated at the node:
+//   u     = sum_n beta_n w_n
+//   du/dn = (k/2)[(nx + i ny) sum_nu beta_{nu+1} w_nu + (-nx + i ny) sum_nu beta_{nu-1} w_nu]
+// so each pair accumulates three sums (val, S+, S-) and the node normal is
+// applied once per CTA.
 struct CArgs {
   const double* centers;   // [M][2]
   const double2* beta;     // [M][L]
@@ -67,8 +55,8 @@ struct CArgs {
   const double* g1;        // [n1][5]
   const double* g2;        // [n2][5]
   const double* w2;        // [nw][2]
-  double2* g;              // [nrow_c]
-  int n1, n2, nw, copies, s_begin, s_end;
+  double2* gpart;          // [nsplit][nrow_c]
+  int n1, n2, nw, copies, s_begin, s_end, nrow_c;
   double period, k2;
 };
 
@@ -76,8 +64,7 @@ template <int P>
 __global__ void __launch_bounds__(kCT) c_kernel(CArgs a) {
   constexpr int NU = P + 1;
   constexpr int L = 2 * P + 1;
-  __shared__ double jbuf[(NU + 1) * kCT];
-  __shared__ double2 red[2 * kCT];
+  __shared__ double2 red[3 * kCT];
   const int row = blockIdx.x;              // target node index over g1, g2, wall
   double tx, ty, nx, ny, sgn;
   int kind;                                // 0 interface, 1 wall
@@ -97,19 +84,15 @@ __global__ void __launch_bounds__(kCT) c_kernel(CArgs a) {
     rv = 2 * a.n1 + 2 * a.n2 + i; rd = rv + a.nw;
   }
   const int P_ = a.copies;
-  // source images: interface rows use l = -P..P with weight bloch^l; the
-  // wall rows use the two telescoped extremes
-  //   +bloch^{P+1} at shift +P d  and  -bloch^{-P} at shift -(P+1) d.
+  // interface rows: l = -P..P, weight bloch^l; wall rows: the telescoped
+  // extremes +bloch^{P+1} at shift +P d and -bloch^{-P} at shift -(P+1) d
   const int nl = kind == 0 ? 2 * P_ + 1 : 2;
-  const int ns = a.s_end - a.s_begin;
-  const double hk = 0.5 * a.k2;
-  // D_nu coefficient of w_nu in the normal derivative:
-  //   dn = sum_n beta_n [ (k/2)(nx + i ny) w_{n-1}... ] -> see below
-  const double2 cp = make_double2(hk * nx, hk * ny);    // (k/2)(nx + i ny)
-  const double2 cm = make_double2(-hk * nx, hk * ny);   // (k/2)(-nx + i ny)
-  double2 val = make_double2(0, 0), der = make_double2(0, 0);
-  double* jb = jbuf + threadIdx.x;
-  for (int it = threadIdx.x; it < ns * nl; it += kCT) {
+  const int npair = (a.s_end - a.s_begin) * nl;
+  const int per = (npair + gridDim.y - 1) / gridDim.y;
+  const int p0 = blockIdx.y * per;
+  const int p1 = min(npair, p0 + per);
+  double2 val = make_double2(0, 0), sp = make_double2(0, 0), sm = make_double2(0, 0);
+  for (int it = p0 + threadIdx.x; it < p1; it += kCT) {
     const int j = a.s_begin + it / nl;
     const int li = it % nl;
     int l;
@@ -130,32 +113,58 @@ __global__ void __launch_bounds__(kCT) c_kernel(CArgs a) {
     const double rho = hypot(dx, dy);
     const double inv = 1.0 / rho;
     const double2* bj = a.beta + (size_t)j * L;
-    double2 pv = make_double2(0, 0), pd = make_double2(0, 0);
-    hankel_symbols<NU>(
-        a.k2 * rho, dx * inv, dy * inv, [&](int nu, double v) { jb[nu * kCT] = v; },
-        [&](int nu) { return jb[nu * kCT]; },
-        [&](int nu, double re, double im) {
-          const double2 w = make_double2(re, im);
-          if (nu >= -P && nu <= P) pv = cfma(bj[nu + P], w, pv);
-          // d/dn w-coefficient: (k/2)[(nx - i ny)... expressed per nu:
-          //   dx u = (k/2) sum_n beta_n (w_{n-1} - w_{n+1})
-          //   dy u = (ik/2) sum_n beta_n (w_{n+1} + w_{n-1})
-          // coefficient of w_nu: from n = nu+1 (w_{n-1}) and n = nu-1 (w_{n+1})
-          //   nx (k/2)(b_{nu+1} - b_{nu-1}) + ny (ik/2)(b_{nu-1} + b_{nu+1})
-          //   = b_{nu+1} (k/2)(nx + i ny) + b_{nu-1} (k/2)(-nx + i ny)
-          double2 dcoef = make_double2(0, 0);
-          if (nu + 1 >= -P && nu + 1 <= P) dcoef = cmul(bj[nu + 1 + P], cp);
-          if (nu - 1 >= -P && nu - 1 <= P) dcoef = cfma(bj[nu - 1 + P], cm, dcoef);
-          pd = cfma(dcoef, w, pd);
-        });
+    double2 pv = make_double2(0, 0), pp = make_double2(0, 0), pm = make_double2(0, 0);
+    const double zz = a.k2 * rho;
+    hankel_symbols<NU>(zz, dx * inv, dy * inv, miller_start_j01(zz),
+                       [&](int nu, double re, double im) {
+                         const double2 w = make_double2(re, im);
+                         if (nu >= -P && nu <= P) pv = cfma(__ldg(bj + nu + P), w, pv);
+                         if (nu + 1 >= -P && nu + 1 <= P) pp = cfma(__ldg(bj + nu + 1 + P), w, pp);
+                         if (nu - 1 >= -P && nu - 1 <= P) pm = cfma(__ldg(bj + nu - 1 + P), w, pm);
+                       });
     val = cfma(wgt, pv, val);
-    der = cfma(wgt, pd, der);
+    sp = cfma(wgt, pp, sp);
+    sm = cfma(wgt, pm, sm);
   }
-  block_sum2(val, der, red);
+  // deterministic block reduction of (val, S+, S-)
+  red[threadIdx.x] = val;
+  red[kCT + threadIdx.x] = sp;
+  red[2 * kCT + threadIdx.x] = sm;
+  __syncthreads();
+  for (int st = kCT / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        red[q * kCT + threadIdx.x].x += red[q * kCT + threadIdx.x + st].x;
+        red[q * kCT + threadIdx.x].y += red[q * kCT + threadIdx.x + st].y;
+      }
+    }
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
-    a.g[rv] = make_double2(sgn * val.x, sgn * val.y);
-    a.g[rd] = make_double2(sgn * der.x, sgn * der.y);
+    const double hk = 0.5 * a.k2;
+    const double2 cp = make_double2(hk * nx, hk * ny);    // (k/2)(nx + i ny)
+    const double2 cm = make_double2(-hk * nx, hk * ny);   // (k/2)(-nx + i ny)
+    const double2 v = red[0];
+    const double2 d = cfma(cm, red[2 * kCT], cmul(cp, red[kCT]));
+    double2* gp = a.gpart + (size_t)blockIdx.y * a.nrow_c;
+    gp[rv] = make_double2(sgn * v.x, sgn * v.y);
+    gp[rd] = make_double2(sgn * d.x, sgn * d.y);
   }
+}
+
+// g[i] = sum_s gpart[s][i]  (fixed split order)
+__global__ void sum_splits(const double2* __restrict__ part, int nsplit, int n,
+                           double2* __restrict__ g) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2 s = make_double2(0, 0);
+  for (int q = 0; q < nsplit; ++q) {
+    const double2 v = part[(size_t)q * n + i];
+    s.x += v.x;
+    s.y += v.y;
+  }
+  g[i] = s;
 }
 
 // ---------------------------------------------------------------- K4: A^+ g
@@ -199,14 +208,23 @@ __global__ void f_minus(const double2* __restrict__ f, const double2* __restrict
 }
 
 // ---------------------------------------------------------------- K5: B_phys x
+// grid (owned inclusion m, source chunk).  A source is an interface node y of
+// Gamma1/Gamma2 in copy l: single layer = monopole (i/4) bloch^l w sigma,
+// double layer = dipole with outgoing coefficients
+//   beta_1 = (k/2)(nx - i ny) c_d,  beta_-1 = -(k/2)(nx + i ny) c_d,
+// (c_d = (i/4) bloch^l w mu), translated to x_m with the M2L symbols
+// t_nu of (x_m - y_l):  a[n'] += c_s t_{-n'} + beta_1 t_{1-n'} + beta_-1 t_{-1-n'}.
+// Chunk c = 0 additionally adds the L2L of the a2 J-expansion (B_pm).
+constexpr int kBT = 64;    // threads (= sources per chunk) for K5
+
 struct BArgs {
   const double* centers;   // [M][2]
   const double2* x;        // [ncol_b] physical empty-grating unknowns
   const double2* bpow;     // bloch^l (index l + P + 1)
   const double* g1;
   const double* g2;
-  double2* out;            // [nt][L]
-  int n1, n2, copies, t_begin, nt, Q;
+  double2* bpart;          // [nchunk][nt][L]
+  int n1, n2, copies, t_begin, nt, Q, nchunk;
   double period, k2, x2x, x2y;
 };
 
@@ -215,27 +233,30 @@ struct BShape {
   static constexpr int NU = P + 1;
   static constexpr int NSP = 2 * NU + 1;           // odd: conflict-free row stride
   static constexpr int L = 2 * P + 1;
+  static constexpr int NQMAX = 36 + P;             // sized for Q <= 36 (ProblemConfig default)
+  static constexpr size_t SMEM_SYM = (size_t)kBT * NSP * sizeof(double2);
+  static constexpr size_t SMEM_JL = (size_t)(2 * NQMAX + 1) * sizeof(double2);
+  static constexpr size_t SMEM = (SMEM_SYM > SMEM_JL ? SMEM_SYM : SMEM_JL) + 3 * kBT * sizeof(double2);
 };
 
 template <int P>
-__global__ void __launch_bounds__(kCT) b_kernel(BArgs a) {
+__global__ void __launch_bounds__(kBT) b_kernel(BArgs a) {
   using S = BShape<P>;
   constexpr int NU = S::NU, NSP = S::NSP, L = S::L;
-  static_assert(L <= kCT / 2, "two output groups of kCT/2 threads");
+  static_assert(L <= kBT, "one output order per thread");
   extern __shared__ double2 bsm[];
-  double2* sym = bsm;                      // [kCT][NSP]
-  double2* coef = bsm + kCT * NSP;         // [kCT][3]: cs, cdp, cdm
-  __shared__ double2 fin[kCT];
+  double2* sym = bsm;                                   // [kBT][NSP]
+  double2* coef = bsm + (S::SMEM_SYM > S::SMEM_JL ? kBT * NSP : 2 * S::NQMAX + 1);   // [kBT][3]
   const int mloc = blockIdx.x;
   const int m = a.t_begin + mloc;
+  const int chunk = blockIdx.y;
   const double xm = a.centers[2 * m], ym = a.centers[2 * m + 1];
   const int nl = 2 * a.copies + 1;
   const int nsrc = (a.n1 + a.n2) * nl;
-  const int grp = threadIdx.x / (kCT / 2), np = threadIdx.x % (kCT / 2);   // output n' = np - P
-  double2 acc = make_double2(0, 0);
   const double hk = 0.5 * a.k2;
-  for (int base = 0; base < nsrc; base += kCT) {
-    const int it = base + threadIdx.x;
+  const int it = chunk * kBT + threadIdx.x;
+  const int nlive = min(kBT, nsrc - chunk * kBT);
+  {
     double2* row = sym + (size_t)threadIdx.x * NSP;
     if (it < nsrc) {
       const int node = it / nl;
@@ -246,13 +267,10 @@ __global__ void __launch_bounds__(kCT) b_kernel(BArgs a) {
       const int sg_col = on1 ? a.n1 + node : 2 * a.n1 + a.n2 + (node - a.n1);
       const double2 wl = a.bpow[l + a.copies + 1];
       const double w = q[4];
-      // (i/4) bloch^l w * density
-      const double2 iw = make_double2(-0.25 * w * wl.y, 0.25 * w * wl.x);
-      const double2 cs = cmul(iw, a.x[sg_col]);
+      const double2 iw = make_double2(-0.25 * w * wl.y, 0.25 * w * wl.x);   // (i/4) bloch^l w
       const double2 cd = cmul(iw, a.x[mu_col]);
       const double nx = q[2], ny = q[3];
-      // dipole coefficients: beta_1 = (k/2)(nx - i ny), beta_-1 = -(k/2)(nx + i ny)
-      coef[3 * threadIdx.x + 0] = cs;
+      coef[3 * threadIdx.x + 0] = cmul(iw, a.x[sg_col]);
       coef[3 * threadIdx.x + 1] = cmul(cd, make_double2(hk * nx, -hk * ny));
       coef[3 * threadIdx.x + 2] = cmul(cd, make_double2(-hk * nx, -hk * ny));
       const double dx = xm - q[0] - (double)l * a.period;
@@ -260,76 +278,77 @@ __global__ void __launch_bounds__(kCT) b_kernel(BArgs a) {
       const double rho = hypot(dx, dy);
       const double inv = 1.0 / rho;
       double2* r0 = row + NU;
-      hankel_symbols<NU>(
-          a.k2 * rho, dx * inv, dy * inv, [&](int nu, double v) { r0[nu].x = v; },
-          [&](int nu) { return r0[nu].x; },
-          [&](int nu, double re, double im) { r0[nu] = make_double2(re, im); });
-    } else {
-      coef[3 * threadIdx.x + 0] = make_double2(0, 0);
-      coef[3 * threadIdx.x + 1] = make_double2(0, 0);
-      coef[3 * threadIdx.x + 2] = make_double2(0, 0);
-      for (int q = 0; q < NSP; ++q) row[q] = make_double2(0, 0);
-    }
-    __syncthreads();
-    if (np < L) {
-      const int nprime = np - P;
-      const int lim = min(kCT / 2, nsrc - base - grp * (kCT / 2));
-      for (int yy = 0; yy < lim; ++yy) {
-        const int y = grp * (kCT / 2) + yy;
-        const double2* rr = sym + (size_t)y * NSP + NU;
-        acc = cfma(coef[3 * y + 0], rr[-nprime], acc);
-        acc = cfma(coef[3 * y + 1], rr[1 - nprime], acc);
-        acc = cfma(coef[3 * y + 2], rr[-1 - nprime], acc);
-      }
-    }
-    __syncthreads();
-  }
-  // combine the two groups
-  fin[threadIdx.x] = acc;
-  __syncthreads();
-  if (grp == 0 && np < L) {
-    acc.x += fin[threadIdx.x + kCT / 2].x;
-    acc.y += fin[threadIdx.x + kCT / 2].y;
-    fin[threadIdx.x] = acc;
-  }
-  __syncthreads();
-  // B_pm: L2L of the a2 expansion about x2:
-  //   a[n'] += sum_q a2_q J_{q-n'}(k2 rho) e^{i(q-n') phi},  (rho, phi) = polar(x_m - x2)
-  const int NQ = a.Q + P;
-  double2* jl = sym;                         // [2*NQ+1] signed orders, reuse
-  if (threadIdx.x == 0) {
-    const double dx = xm - a.x2x, dy = ym - a.x2y;
-    const double rho = hypot(dx, dy);
-    double2* j0 = jl + NQ;
-    if (rho == 0.0) {
-      for (int nu = -NQ; nu <= NQ; ++nu) j0[nu] = make_double2(nu == 0 ? 1.0 : 0.0, 0.0);
-    } else {
-      const double z = a.k2 * rho;
-      double inv_norm, y0, y1;
-      bessel_jy_sweep(z, NQ, [&](int nu, double v) { j0[nu].x = v; }, &inv_norm, &y0, &y1);
-      const double c = dx / rho, s = dy / rho;
-      double pr = 1.0, pi = 0.0;
-      j0[0] = make_double2(j0[0].x * inv_norm, 0.0);
-      for (int nu = 1; nu <= NQ; ++nu) {
-        const double npr = fma(pr, c, -pi * s);
-        const double npi = fma(pr, s, pi * c);
-        pr = npr;
-        pi = npi;
-        const double J = j0[nu].x * inv_norm;
-        const double sg = (nu & 1) ? -1.0 : 1.0;
-        j0[nu] = make_double2(J * pr, J * pi);
-        j0[-nu] = make_double2(sg * J * pr, -sg * J * pi);
-      }
+      const double zz = a.k2 * rho;
+      hankel_symbols<NU>(zz, dx * inv, dy * inv, miller_start_j01(zz),
+                         [&](int nu, double re, double im) { r0[nu] = make_double2(re, im); });
     }
   }
   __syncthreads();
+  double2 out = make_double2(0, 0);
   if (threadIdx.x < L) {
     const int nprime = threadIdx.x - P;
-    double2 s = fin[threadIdx.x];
-    const double2* a2 = a.x + 2 * a.n1 + 2 * a.n2;   // a2 column block
-    for (int qq = -a.Q; qq <= a.Q; ++qq) s = cfma(a2[qq + a.Q], jl[NQ + qq - nprime], s);
-    a.out[(size_t)mloc * L + threadIdx.x] = s;
+    // six independent chains: (monopole, dipole+, dipole-) x (even, odd source)
+    double2 c0 = make_double2(0, 0), c1 = c0, c2 = c0, c3 = c0, c4 = c0, c5 = c0;
+    int y = 0;
+    for (; y + 1 < nlive; y += 2) {
+      const double2* r = sym + (size_t)y * NSP + NU;
+      const double2* r2 = r + NSP;
+      c0 = cfma(coef[3 * y + 0], r[-nprime], c0);
+      c1 = cfma(coef[3 * y + 1], r[1 - nprime], c1);
+      c2 = cfma(coef[3 * y + 2], r[-1 - nprime], c2);
+      c3 = cfma(coef[3 * y + 3], r2[-nprime], c3);
+      c4 = cfma(coef[3 * y + 4], r2[1 - nprime], c4);
+      c5 = cfma(coef[3 * y + 5], r2[-1 - nprime], c5);
+    }
+    if (y < nlive) {
+      const double2* r = sym + (size_t)y * NSP + NU;
+      c0 = cfma(coef[3 * y + 0], r[-nprime], c0);
+      c1 = cfma(coef[3 * y + 1], r[1 - nprime], c1);
+      c2 = cfma(coef[3 * y + 2], r[-1 - nprime], c2);
+    }
+    out = make_double2(((c0.x + c3.x) + (c1.x + c4.x)) + (c2.x + c5.x),
+                       ((c0.y + c3.y) + (c1.y + c4.y)) + (c2.y + c5.y));
   }
+  if (chunk == 0) {
+    // B_pm: L2L of the a2 expansion about x2:
+    //   a[n'] += sum_q a2_q J_{q-n'}(k2 rho) e^{i(q-n') phi},  (rho, phi) = polar(x_m - x2)
+    __syncthreads();
+    const int NQ = a.Q + P;
+    double2* jl = sym;                         // [2*NQ+1] signed orders, reuse
+    if (threadIdx.x == 0) {
+      const double dx = xm - a.x2x, dy = ym - a.x2y;
+      const double rho = hypot(dx, dy);
+      double2* j0 = jl + NQ;
+      if (rho == 0.0) {
+        for (int nu = -NQ; nu <= NQ; ++nu) j0[nu] = make_double2(nu == 0 ? 1.0 : 0.0, 0.0);
+      } else {
+        const double z = a.k2 * rho;
+        double inv_norm, y0, y1;
+        bessel_jy_sweep(z, NQ, [&](int nu, double v) { j0[nu].x = v; }, &inv_norm, &y0, &y1);
+        const double c = dx / rho, s = dy / rho;
+        double pr = 1.0, pi = 0.0;
+        j0[0] = make_double2(j0[0].x * inv_norm, 0.0);
+        for (int nu = 1; nu <= NQ; ++nu) {
+          const double npr = fma(pr, c, -pi * s);
+          const double npi = fma(pr, s, pi * c);
+          pr = npr;
+          pi = npi;
+          const double J = j0[nu].x * inv_norm;
+          const double sg = (nu & 1) ? -1.0 : 1.0;
+          j0[nu] = make_double2(J * pr, J * pi);
+          j0[-nu] = make_double2(sg * J * pr, -sg * J * pi);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < L) {
+      const int nprime = threadIdx.x - P;
+      const double2* a2 = a.x + 2 * a.n1 + 2 * a.n2;   // a2 column block
+      for (int qq = -a.Q; qq <= a.Q; ++qq) out = cfma(a2[qq + a.Q], jl[NQ + qq - nprime], out);
+    }
+  }
+  if (threadIdx.x < L)
+    a.bpart[((size_t)chunk * a.nt + mloc) * L + threadIdx.x] = out;
 }
 
 // y[m][r] = v[m][r] + sgn sum_n e^{i rot_m (r-n)} s[r][n] u[m][n]  (dense S)
@@ -357,9 +376,22 @@ __global__ void dense_s_epilogue(const double2* __restrict__ S, const double* __
   }
 }
 
+int c_splits(const Ctx* c, int s0, int s1) {
+  const long long npair = (long long)(s1 - s0) * (2 * c->copies + 1);
+  long long ns = (npair + 4 * kCT - 1) / (4 * kCT);   // ~4 pairs per thread
+  if (ns < 1) ns = 1;
+  if (ns > 512) ns = 512;
+  return (int)ns;
+}
+
+int b_chunks(const Ctx* c) {
+  const int nsrc = (c->n1 + c->n2) * (2 * c->copies + 1);
+  return (nsrc + kBT - 1) / kBT;
+}
+
 template <int P>
-int launch_c(Ctx* c, const double2* beta, const double2* bpow, double2* g, int s0, int s1,
-             cudaStream_t st) {
+int launch_c(Ctx* c, const double2* beta, const double2* bpow, double2* gpart, double2* g, int s0,
+             int s1, cudaStream_t st) {
   CArgs a;
   a.centers = c->d_centers;
   a.beta = beta;
@@ -367,61 +399,73 @@ int launch_c(Ctx* c, const double2* beta, const double2* bpow, double2* g, int s
   a.g1 = c->d_g1;
   a.g2 = c->d_g2;
   a.w2 = c->d_w2;
-  a.g = g;
+  a.gpart = gpart;
   a.n1 = c->n1;
   a.n2 = c->n2;
   a.nw = c->nw;
   a.copies = c->copies;
   a.s_begin = s0;
   a.s_end = s1;
+  a.nrow_c = c->nrow_c;
   a.period = c->period;
   a.k2 = c->k2;
-  c_kernel<P><<<c->n1 + c->n2 + c->nw, kCT, 0, st>>>(a);
+  const int ns = c_splits(c, s0, s1);
+  c_kernel<P><<<dim3(c->n1 + c->n2 + c->nw, ns), kCT, 0, st>>>(a);
   PS_CUDA_TRY(c, cudaGetLastError());
+  sum_splits<<<(c->nrow_c + 255) / 256, 256, 0, st>>>(gpart, ns, c->nrow_c, g);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  c->launches += 2;
   return PS_OK;
 }
 
 template <int P>
-int launch_b(Ctx* c, const double2* x, const double2* bpow, double2* out, cudaStream_t st) {
+int launch_b(Ctx* c, const double2* x, const double2* bpow, double2* bpart, double2* out,
+             cudaStream_t st) {
   using S = BShape<P>;
+  if (c->Q > 36) {
+    c->err = "apply_B: J-expansion order Q > 36 not supported";
+    return PS_ERR_UNSUPPORTED;
+  }
   BArgs a;
   a.centers = c->d_centers;
   a.x = x;
   a.bpow = bpow;
   a.g1 = c->d_g1;
   a.g2 = c->d_g2;
-  a.out = out;
+  a.bpart = bpart;
   a.n1 = c->n1;
   a.n2 = c->n2;
   a.copies = c->copies;
   a.t_begin = c->t_begin;
   a.nt = c->t_end - c->t_begin;
   a.Q = c->Q;
+  a.nchunk = b_chunks(c);
   a.period = c->period;
   a.k2 = c->k2;
   a.x2x = c->x2[0];
   a.x2y = c->x2[1];
   if (a.nt <= 0) return PS_OK;
-  size_t smem = (size_t)kCT * S::NSP * sizeof(double2) + (size_t)kCT * 3 * sizeof(double2);
-  const size_t need_jl = (size_t)(2 * (c->Q + P) + 1) * sizeof(double2);
-  if (smem < need_jl + 3 * kCT * sizeof(double2)) smem = need_jl + 3 * kCT * sizeof(double2);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
+  static bool attr = false;
+  if (!attr && S::SMEM > 48 * 1024) {
     PS_CUDA_TRY(c, cudaFuncSetAttribute(b_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
-    attr = smem;
+                                        (int)S::SMEM));
+    attr = true;
   }
-  b_kernel<P><<<a.nt, kCT, smem, st>>>(a);
+  b_kernel<P><<<dim3(a.nt, a.nchunk), kBT, S::SMEM, st>>>(a);
   PS_CUDA_TRY(c, cudaGetLastError());
+  const int n = a.nt * S::L;
+  sum_splits<<<(n + 255) / 256, 256, 0, st>>>(bpart, a.nchunk, n, out);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  c->launches += 2;
   return PS_OK;
 }
 
-int dispatch_c(Ctx* c, const double2* beta, const double2* bpow, double2* g, int s0, int s1,
-               cudaStream_t st) {
+int dispatch_c(Ctx* c, const double2* beta, const double2* bpow, double2* gpart, double2* g,
+               int s0, int s1, cudaStream_t st) {
   switch (c->p) {
 #define PS_CASE(P) \
   case P:          \
-    return launch_c<P>(c, beta, bpow, g, s0, s1, st);
+    return launch_c<P>(c, beta, bpow, gpart, g, s0, s1, st);
     PS_M2L_ORDERS(PS_CASE)
 #undef PS_CASE
     default:
@@ -430,11 +474,12 @@ int dispatch_c(Ctx* c, const double2* beta, const double2* bpow, double2* g, int
   }
 }
 
-int dispatch_b(Ctx* c, const double2* x, const double2* bpow, double2* out, cudaStream_t st) {
+int dispatch_b(Ctx* c, const double2* x, const double2* bpow, double2* bpart, double2* out,
+               cudaStream_t st) {
   switch (c->p) {
 #define PS_CASE(P) \
   case P:          \
-    return launch_b<P>(c, x, bpow, out, st);
+    return launch_b<P>(c, x, bpow, bpart, out, st);
     PS_M2L_ORDERS(PS_CASE)
 #undef PS_CASE
     default:
@@ -443,16 +488,18 @@ int dispatch_b(Ctx* c, const double2* x, const double2* bpow, double2* out, cuda
   }
 }
 
-// workspace layout per RHS: g [nrc] | h [nsv] | x [nout] | bsub [Mt*L] | u [Mt*L]
+// workspace layout per RHS:
+//   g [nrc] | h [nsv] | x [nout] | bsub [Mt*L] | u [Mt*L] | gpart [512*nrc] | bpart [nchunk*Mt*L]
 struct Work {
-  double2 *g, *h, *x, *bsub, *u;
+  double2 *g, *h, *x, *bsub, *u, *gpart, *bpart;
 };
 
 int work(Ctx* c, int r, Work* w) {
   const size_t nrc = c->nrow_c, nsv = c->nsv > 0 ? c->nsv : 1;
   const size_t nout = c->ncol_b + 2 * c->nrb;
   const size_t mtl = (size_t)(c->t_end - c->t_begin) * c->L;
-  const size_t per = nrc + nsv + nout + 2 * mtl + 8;
+  const size_t nch = c->have_layers ? (size_t)b_chunks(c) : 0;
+  const size_t per = nrc + nsv + nout + 2 * mtl + 512 * nrc + nch * mtl + 8;
   const size_t need = per * c->nrhs;
   if (c->work_elems < need) {
     if (c->d_work) cudaFree(c->d_work);
@@ -467,6 +514,8 @@ int work(Ctx* c, int r, Work* w) {
   w->x = w->h + nsv;
   w->bsub = w->x + nout;
   w->u = w->bsub + mtl;
+  w->gpart = w->u + mtl;
+  w->bpart = w->gpart + 512 * nrc;
   return PS_OK;
 }
 
@@ -478,6 +527,7 @@ int pinv(Ctx* c, int r, const double2* g, double2* x, int nout, cudaStream_t st)
   PS_CUDA_TRY(c, cudaGetLastError());
   pinv_v<<<(nout + 7) / 8, 256, 0, st>>>(R.d_Vb, R.d_cscale, w.h, nout, c->nsv, x);
   PS_CUDA_TRY(c, cudaGetLastError());
+  c->launches += 2;
   return PS_OK;
 }
 
@@ -488,8 +538,10 @@ const double2* bpow_of(Ctx* c, int r) { return c->d_blochpow + (size_t)r * (2 * 
 int apply_C(Ctx* c, const double2* beta, double2* g, int s0, int s1, cudaStream_t st) {
   const size_t in_stride = (size_t)c->M * c->L;
   for (int r = 0; r < c->nrhs; ++r) {
-    if (int rc = dispatch_c(c, beta + r * in_stride, bpow_of(c, r), g + (size_t)r * c->nrow_c, s0,
-                            s1, st))
+    Work w;
+    if (int rc = work(c, r, &w)) return rc;
+    if (int rc = dispatch_c(c, beta + r * in_stride, bpow_of(c, r), w.gpart,
+                            g + (size_t)r * c->nrow_c, s0, s1, st))
       return rc;
   }
   return PS_OK;
@@ -498,7 +550,7 @@ int apply_C(Ctx* c, const double2* beta, double2* g, int s0, int s1, cudaStream_
 // B_phys A^+ g for RHS r into w.bsub
 static int b_pinv(Ctx* c, int r, const double2* g, Work* w, cudaStream_t st) {
   if (int rc = pinv(c, r, g, w->x, c->ncol_b, st)) return rc;
-  return dispatch_b(c, w->x, bpow_of(c, r), w->bsub, st);
+  return dispatch_b(c, w->x, bpow_of(c, r), w->bpart, w->bsub, st);
 }
 
 static int s_apply(Ctx* c, const double2* v_own, const double2* u, double2* y, cudaStream_t st,
@@ -509,6 +561,7 @@ static int s_apply(Ctx* c, const double2* v_own, const double2* u, double2* y, c
   dense_s_epilogue<<<nt, 64, c->L * sizeof(double2), st>>>(c->d_S, c->d_rot, v_own, u,
                                                           c->t_begin, c->L, sgn, y);
   PS_CUDA_TRY(c, cudaGetLastError());
+  c->launches += 1;
   return PS_OK;
 }
 
@@ -546,7 +599,8 @@ int apply_schur(Ctx* c, const double2* v, double2* y, cudaStream_t st) {
   for (int r = 0; r < nrhs; ++r) {
     Work w;
     if (int rc = work(c, r, &w)) return rc;
-    if (int rc = dispatch_c(c, v + r * in_stride, bpow_of(c, r), w.g, 0, c->M, st)) return rc;
+    if (int rc = dispatch_c(c, v + r * in_stride, bpow_of(c, r), w.gpart, w.g, 0, c->M, st))
+      return rc;
   }
   for (int r = 0; r < nrhs; ++r) {
     Work w;
@@ -583,6 +637,7 @@ int schur_rhs(Ctx* c, double2* rhs, cudaStream_t st) {
     if (c->s_diag) {
       diag_s_apply<<<(n + 255) / 256, 256, 0, st>>>(c->d_S, w.bsub, n, c->L, rhs + r * out_stride);
       PS_CUDA_TRY(c, cudaGetLastError());
+      c->launches += 1;
     } else {
       if (int rc = s_apply(c, nullptr, w.bsub, rhs + r * out_stride, st, 1.0)) return rc;
     }
@@ -598,6 +653,7 @@ int recover(Ctx* c, const double2* g, double2* x, cudaStream_t st) {
     f_minus<<<(c->nrow_c + 255) / 256, 256, 0, st>>>(c->rhs[r].d_f, g + (size_t)r * c->nrow_c,
                                                      c->nrow_c, w.g);
     PS_CUDA_TRY(c, cudaGetLastError());
+    c->launches += 1;
     if (int rc = pinv(c, r, w.g, x + (size_t)r * nout, nout, st)) return rc;
   }
   return PS_OK;

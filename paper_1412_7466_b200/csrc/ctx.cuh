@@ -66,6 +66,14 @@ struct Ctx {
   size_t work_elems = 0;
 
   std::vector<void*> owned;        // everything cudaMalloc'ed
+
+  // instrumentation (ps_stats): kernel launches issued by this context and,
+  // when enabled, CUDA-event time of every K1 (m2l_kernel) launch
+  long long launches = 0;
+  int profile = 0;
+  double k1_ms = 0.0;
+  long long k1_count = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k1_events;
 };
 
 inline Ctx* C(ps_ctx* h) { return reinterpret_cast<Ctx*>(h); }

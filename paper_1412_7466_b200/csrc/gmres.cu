@@ -306,6 +306,7 @@ static int dot_impl(Ctx* c, int nrhs, long long n, int k, const double2* V, cons
   if (k == 0) return PS_OK;
   const int nc = nchunks(n);
   dim3 grid(nc, k, nrhs);
+  c->launches += 2;
   dot_partial<<<grid, kDotThreads, 0, st>>>(V, w, nrhs, n, k, nc, active, part);
   PS_CUDA_TRY(c, cudaGetLastError());
   dot_final<<<(nrhs * k + 127) / 128, 128, 0, st>>>(part, nrhs, k, nc, h, ldh, accumulate);
@@ -319,6 +320,7 @@ static int axpy_impl(Ctx* c, int nrhs, long long n, int k, const double2* V, con
   int bx = (int)((n + 255) / 256);
   if (bx > 4 * c->sm_count) bx = 4 * c->sm_count;
   dim3 grid(bx, nrhs);
+  c->launches += 1;
   axpy_block<<<grid, 256, k * sizeof(double2), st>>>(V, h, ldh, nrhs, n, k, sgn, active, w);
   PS_CUDA_TRY(c, cudaGetLastError());
   return PS_OK;
@@ -327,6 +329,7 @@ static int axpy_impl(Ctx* c, int nrhs, long long n, int k, const double2* V, con
 static int norm_impl(Ctx* c, int nrhs, long long n, const double2* w, double* out,
                      double2* part, cudaStream_t st) {
   const int nc = nchunks(n);
+  c->launches += 2;
   norm2_partial<<<dim3(nc, nrhs), kDotThreads, 0, st>>>(w, n, nc, part);
   PS_CUDA_TRY(c, cudaGetLastError());
   norm2_final<<<(nrhs + 127) / 128, 128, 0, st>>>(part, nrhs, nc, out);
@@ -397,6 +400,7 @@ int gmres(Ctx* c, const double2* rhs, double2* x, double tol, int maxit, int* it
 
   // init: V_0 = b / ||b||
   if (int rc = norm_impl(c, nrhs, n, rhs, nrm2, part, st)) return rc;
+  c->launches += 2;   // init_state, scale_into
   init_state<<<(nrhs + 127) / 128, 128, 0, st>>>(s, nrhs, maxit, nrm2);
   scale_into<<<dim3((int)std::min<long long>((n + 255) / 256, 4LL * c->sm_count), nrhs), 256, 0,
                st>>>(rhs, nrm2, n, nullptr, V);
@@ -432,6 +436,7 @@ int gmres(Ctx* c, const double2* rhs, double2* x, double tol, int maxit, int* it
     cadd_rows<<<(nrhs * (k + 1) + 127) / 128, 128, 0, st>>>(hcol, y, nrhs, k + 1, maxit + 1);
     PS_CUDA_TRY(c, cudaGetLastError());
     if (int rc = norm_impl(c, nrhs, n, w, nrm2, part, st)) return rc;
+    c->launches += 3;   // cadd_rows, givens_step, scale_into
     givens_step<<<(nrhs + 127) / 128, 128, 0, st>>>(s, nrhs, k, maxit, hcol, maxit + 1, nrm2);
     PS_CUDA_TRY(c, cudaGetLastError());
     scale_into<<<dim3(bx, nrhs), 256, 0, st>>>(w, nrm2, n, s.active, Vk1);
@@ -459,12 +464,14 @@ int gmres(Ctx* c, const double2* rhs, double2* x, double tol, int maxit, int* it
     if (changed) {
       PS_CUDA_TRY(c, cudaMemcpyAsync(flags_dev, active.data(), nrhs * sizeof(int),
                                      cudaMemcpyHostToDevice, st));
+      c->launches += 1;
       set_flags<<<(nrhs + 127) / 128, 128, 0, st>>>(s.active, flags_dev, nrhs);
       PS_CUDA_TRY(c, cudaGetLastError());
     }
   }
   // x = sum_i y_i V_i
   PS_CUDA_TRY(c, cudaMemcpyAsync(kk_dev, kk.data(), nrhs * sizeof(int), cudaMemcpyHostToDevice, st));
+  c->launches += 1;
   back_solve<<<(nrhs + 127) / 128, 128, 0, st>>>(s, nrhs, kk_dev, maxit, y, maxit + 1);
   PS_CUDA_TRY(c, cudaGetLastError());
   PS_CUDA_TRY(c, cudaMemsetAsync(x, 0, n2 * sizeof(double2), st));

@@ -34,10 +34,15 @@ namespace {
 constexpr int kTT = 8;                 // targets per tile
 constexpr int kNB = 4;                 // row blocks (lanes) per target
 constexpr int kS = 8;                  // source images per batch = consumer warps
-constexpr int kPW = 2;                 // producer warps
+#ifndef PS_K1_PW
+#define PS_K1_PW 4
+#endif
+constexpr int kPW = PS_K1_PW;          // producer warps (one per SM sub-partition at 4)
 constexpr int kThreads = (kS + kPW) * 32;
+constexpr int kPairs = kTT * kS;       // symbol rows per batch
+constexpr int kPairsPerWarp = kPairs / kPW;
 static_assert(kTT * kNB == 32, "one consumer warp covers a full target tile");
-static_assert(kTT * kS == kPW * 32, "one pair per producer lane");
+static_assert(kPairs % kPW == 0 && kPairsPerWarp <= 32, "at most one pair per producer lane");
 
 template <int P>
 struct Shape {
@@ -76,33 +81,37 @@ __device__ __forceinline__ void produce(const Args& a, long long w, double2* sym
   using S = Shape<P>;
   const int tile = (int)(w / a.nbatch);
   const int sb = (int)(w % a.nbatch) * kS;
-  const int s = pi / kTT, t = pi % kTT;
-  const int mloc = tile * kTT + t;
-  const int g = sb + s;
-  double2* col = sym + (size_t)s * S::NSP * kTT + t;   // slot stride kTT
-  bool live = (mloc < a.nt) && (g < a.nimg);
-  double dx = 0.0, dy = 0.0;
-  if (live) {
-    const int m = a.t_begin + mloc;
-    const int j = g / a.ncp;
-    const int l = g % a.ncp - a.copies;
-    const double2 cm = reinterpret_cast<const double2*>(a.centers)[m];
-    const double2 cj = reinterpret_cast<const double2*>(a.centers)[j];
-    dx = cm.x - cj.x - (double)l * a.period;
-    dy = cm.y - cj.y;
-    live = !(l == 0 && j == m);
-  }
-  if (!live) {
-    for (int q = S::FP; q < S::FP + S::NS; ++q) col[q * kTT] = make_double2(0.0, 0.0);
-  } else {
-    const double rho = hypot(dx, dy);
-    const double inv = 1.0 / rho;
+  const int pw = pi >> 5, lane = pi & 31;
+  if (lane < kPairsPerWarp) {
+    const int pair = pw * kPairsPerWarp + lane;
+    const int s = pair / kTT, t = pair % kTT;
+    const int mloc = tile * kTT + t;
+    const int g = sb + s;
+    double2* col = sym + (size_t)s * S::NSP * kTT + t;   // slot stride kTT
+    bool live = (mloc < a.nt) && (g < a.nimg);
+    double dx = 1.0, dy = 0.0;
+    if (live) {
+      const int m = a.t_begin + mloc;
+      const int j = g / a.ncp;
+      const int l = g % a.ncp - a.copies;
+      const double2 cm = reinterpret_cast<const double2*>(a.centers)[m];
+      const double2 cj = reinterpret_cast<const double2*>(a.centers)[j];
+      dx = cm.x - cj.x - (double)l * a.period;
+      dy = cm.y - cj.y;
+      live = !(l == 0 && j == m);
+    }
+    const double rho = live ? hypot(dx, dy) : 1.0;
+    const double z = a.k2 * rho;
+    // warp-uniform Miller start: no divergence, uniform constant-bank index
+    int N = live ? miller_start_j01(z) : 2;
+    constexpr unsigned kMask = kPairsPerWarp == 32 ? 0xffffffffu : ((1u << kPairsPerWarp) - 1u);
+    N = __reduce_max_sync(kMask, N);
+    const double inv = live ? 1.0 / rho : 0.0;  // dead pairs (self term, padding): c = s = 0
     double2* base = col + (S::FP + 2 * P) * kTT;
-    hankel_symbols<2 * P>(
-        a.k2 * rho, dx * inv, dy * inv,
-        [&](int nu, double v) { base[nu * kTT].x = v; },
-        [&](int nu) { return base[nu * kTT].x; },
-        [&](int nu, double re, double im) { base[nu * kTT] = make_double2(re, im); });
+    hankel_symbols<2 * P>(z, dx * inv, dy * inv, N, [&](int nu, double re, double im) {
+      if (nu == 0 && !live) re = im = 0.0;
+      base[nu * kTT] = make_double2(re, im);
+    });
   }
   // bloch-weighted beta of the batch's source images
   for (int idx = pi; idx < kS * S::L; idx += kPW * 32) {
@@ -311,8 +320,19 @@ int launch_p(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
                                           (int)S::SMEM));
     attr_done = true;
   }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->profile) {
+    PS_CUDA_TRY(ctx, cudaEventCreate(&e0));
+    PS_CUDA_TRY(ctx, cudaEventCreate(&e1));
+    PS_CUDA_TRY(ctx, cudaEventRecord(e0, st));
+  }
   m2l_kernel<P><<<G, kThreads, S::SMEM, st>>>(a);
   PS_CUDA_TRY(ctx, cudaGetLastError());
+  if (ctx->profile) {
+    PS_CUDA_TRY(ctx, cudaEventRecord(e1, st));
+    ctx->k1_events.push_back({e0, e1});
+  }
+  ctx->launches += 2;
   const int n = a.nt * S::L;
   m2l_reduce<<<(n + 255) / 256, 256, 0, st>>>(ctx->d_partial, G, a.W, a.nbatch, a.maxseg, a.nt,
                                               S::L, mode, v_own, ctx->d_S, bsub, out);

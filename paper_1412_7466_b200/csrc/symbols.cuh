@@ -1,55 +1,61 @@
 // Translation symbols t_nu = H^(1)_nu(z) e^{i nu phi}, nu in [-NU, NU].
 //
-// One thread generates the full symbol row of one (target, source) pair:
-// Miller sweep for J (bessel.cuh), Neumann seeds + upward recurrence for Y,
-// phase powers by complex recurrence, negative orders by
-// H_{-nu} = (-1)^nu H_nu (reference: specialfn._signed_order, sf:79-83).
-// The reference path builds the same numbers with scipy H0/H1 + upward
-// recurrence (sf:54-67) and np.exp(1j*nu*phi).
+// Same algorithm as the reference (specialfn.hankel1_orders,
+// /root/reference/pkg/src/periscat/specialfn.py:54-67): H_0, H_1 seed an
+// upward recurrence H_{nu+1} = (2 nu / z) H_nu - H_{nu-1}; negative orders by
+// H_{-nu} = (-1)^nu H_nu (_signed_order, sf:79-83).  The seeds come from a
+// Miller sweep for J_0, J_1 with Neumann series for Y_0, Y_1 (bessel.cuh)
+// instead of scipy/AMOS; the phases e^{i nu phi} by complex recurrence from
+// e^{i phi} = (dx + i dy) / rho (no sincos).
 #pragma once
 #include "bessel.cuh"
 
 namespace ps {
 
-// jst(nu, v): store unnormalised J_nu (nu <= NU); jld(nu): load it back;
-// out(nu, re, im): final symbol for signed order nu.
-template <int NU, typename JStore, typename JLoad, typename Out>
-PS_HD void hankel_symbols(double z, double c, double s, JStore jst, JLoad jld, Out out) {
-  double inv, y0, y1;
-  bessel_jy_sweep(z, NU > 1 ? NU : 1, jst, &inv, &y0, &y1);
-  // nu = 0
-  double ym1 = y0, yc = y1;          // Y_{nu-1}, Y_nu  (after the nu=0 step)
-  double pr = 1.0, pi = 0.0;         // e^{i nu phi}
-  {
-    const double J = jld(0) * inv;
-    out(0, J, y0);
-  }
+// out(nu, re, im) is called for nu = 0, then (nu, -nu) pairs, nu = 1..NU.
+// N: even Miller start >= miller_start_j01(z).  With c = s = 0 every order
+// but nu = 0 comes out exactly zero (used for dead pairs).
+template <int NU, typename Out>
+PS_HD void hankel_symbols(double z, double c, double s, int N, Out out) {
+  double j0, j1, y0, y1;
+  bessel_jy01(z, N, &j0, &j1, &y0, &y1);
+  out(0, j0, y0);
+  double hmr = j0, hmi = y0;     // H_{nu-1}
+  double hr = j1, hi = y1;       // H_nu
+  double pr = c, pi = s;         // e^{i nu phi}
   const double tz = 2.0 / z;
   double dnu = 1.0;
-#pragma unroll 4
-  for (int nu = 1; nu <= NU; ++nu) {
-    // phase e^{i nu phi}
-    const double npr = fma(pr, c, -pi * s);
-    const double npi = fma(pr, s, pi * c);
-    pr = npr;
-    pi = npi;
-    const double J = jld(nu) * inv;
-    const double Y = yc;
-    // H_nu e^{i nu phi}
-    const double ar = fma(J, pr, -Y * pi);
-    const double ai = fma(J, pi, Y * pr);
-    // H_nu e^{-i nu phi} * (-1)^nu
-    const double sg = (nu & 1) ? -1.0 : 1.0;
-    const double br = sg * fma(J, pr, Y * pi);
-    const double bi = sg * fma(Y, pr, -J * pi);
+  int nu = 1;
+  // one order: emit t_nu, t_-nu (sign (-1)^nu folded into the static flag)
+  auto step = [&](bool odd) {
+    const double ar = fma(hr, pr, -hi * pi);
+    const double ai = fma(hr, pi, hi * pr);
+    const double br = fma(hr, pr, hi * pi);
+    const double bi = fma(hi, pr, -hr * pi);
     out(nu, ar, ai);
-    out(-nu, br, bi);
-    // Y_{nu+1} = (2 nu / z) Y_nu - Y_{nu-1}
-    const double yn = fma(dnu * tz, yc, -ym1);
-    ym1 = yc;
-    yc = yn;
+    if (odd)
+      out(-nu, -br, -bi);
+    else
+      out(-nu, br, bi);
+    const double cf = dnu * tz;
+    const double nr = fma(cf, hr, -hmr);
+    const double ni = fma(cf, hi, -hmi);
+    hmr = hr;
+    hmi = hi;
+    hr = nr;
+    hi = ni;
     dnu += 1.0;
+    const double qr = fma(pr, c, -pi * s);
+    const double qi = fma(pr, s, pi * c);
+    pr = qr;
+    pi = qi;
+    ++nu;
+  };
+  for (int it = 0; it < NU / 2; ++it) {
+    step(true);
+    step(false);
   }
+  if (NU & 1) step(true);
 }
 
 }  // namespace ps

@@ -198,6 +198,18 @@ class Engine:
                                       _stream(self.device)))
         return x, list(iters), hist
 
+    # instrumentation
+    def profile(self, enable: bool = True):
+        self._check(self.lib.ps_profile(self.ctx, 1 if enable else 0))
+
+    def stats(self) -> dict:
+        n, ms, cnt = ctypes.c_longlong(), ctypes.c_double(), ctypes.c_longlong()
+        self._check(self.lib.ps_stats(self.ctx, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(cnt)))
+        return dict(launches=n.value, k1_ms=ms.value, k1_count=cnt.value)
+
+    def stats_reset(self):
+        self._check(self.lib.ps_stats_reset(self.ctx))
+
     # GMRES building blocks for the multi-rank driver
     def block_dot(self, V: torch.Tensor, w: torch.Tensor, k: int, h: torch.Tensor):
         kmax, nrhs, n = V.shape

@@ -1,0 +1,200 @@
+"""Target-inclusion sharding across ranks.
+
+Rank r owns target inclusions [M r / G, M (r+1) / G): their rows of the
+coefficient vector, of T, S and B, and their slices of the Krylov basis.
+Per Schur matvec:
+  1. all-gather beta (NCCL over NVLink) -> full vector on every rank;
+  2. partial g = C beta over the rank's own SOURCE inclusions, all-reduce;
+  3. local y = v_own - S (T v - B A^+ g)  (K1 over all sources, own targets).
+GMRES dot products are local partial sums followed by an all-reduce; the
+Hessenberg least-squares bookkeeping (O(k) scalars) is replicated.
+
+The same driver runs on CPU tensors with the gloo backend (tests) and on
+CUDA tensors with NCCL (bench / solve), where the orthogonalisation uses the
+C-ABI block kernels.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def shard_range(M: int, rank: int, world: int) -> tuple[int, int]:
+    return (M * rank) // world, (M * (rank + 1)) // world
+
+
+def shard_sizes(M: int, world: int) -> list[int]:
+    return [shard_range(M, r, world)[1] - shard_range(M, r, world)[0] for r in range(world)]
+
+
+def all_gather_rows(v_own: torch.Tensor, M: int, group=None) -> torch.Tensor:
+    """[nrhs][M_own][L] on every rank -> [nrhs][M][L] (rows in rank order)."""
+    world = dist.get_world_size(group)
+    if world == 1:
+        return v_own
+    sizes = shard_sizes(M, world)
+    vr = torch.view_as_real(v_own.contiguous())          # complex -> (..., 2) float64
+    if len(set(sizes)) == 1 and v_own.is_cuda:
+        buf = torch.empty((world,) + tuple(vr.shape), dtype=vr.dtype, device=vr.device)
+        dist.all_gather_into_tensor(buf, vr, group=group)
+        full = buf.permute(1, 0, 2, 3, 4).reshape(v_own.shape[0], M, v_own.shape[2], 2)
+        return torch.view_as_complex(full.contiguous())
+    parts = [torch.empty((v_own.shape[0], s, v_own.shape[2], 2), dtype=vr.dtype,
+                         device=vr.device) for s in sizes]
+    dist.all_gather(parts, vr, group=group)
+    return torch.view_as_complex(torch.cat(parts, dim=1).contiguous())
+
+
+def all_reduce_(t: torch.Tensor, group=None) -> torch.Tensor:
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        if t.is_complex():
+            tr = torch.view_as_real(t)
+            dist.all_reduce(tr, group=group)
+        else:
+            dist.all_reduce(t, group=group)
+    return t
+
+
+class ShardedSchur:
+    """Distributed S-preconditioned Schur operator on top of a SchurOperator
+    whose engine owns targets shard_range(M, rank, world)."""
+
+    def __init__(self, op, group=None):
+        self.op = op
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.t0, self.t1 = shard_range(op.M, self.rank, self.world)
+        self.s_range = (self.t0, self.t1)     # own sources for the C partial sum
+
+    def __call__(self, v_own: torch.Tensor, out=None) -> torch.Tensor:
+        v_full = all_gather_rows(v_own, self.op.M, self.group)
+        if not self.op.coupled:
+            return self.op(v_full, out=out)
+        g = self.op.eng.apply_C(v_full, s_range=self.s_range)
+        all_reduce_(g, self.group)
+        return self.op(v_full, out=out, g=g)
+
+    def rhs(self) -> torch.Tensor:
+        return self.op.rhs()
+
+    def recover(self, beta_own: torch.Tensor) -> torch.Tensor:
+        v_full = all_gather_rows(beta_own, self.op.M, self.group)
+        g = self.op.eng.apply_C(v_full, s_range=self.s_range)
+        all_reduce_(g, self.group)
+        return self.op.eng.recover(g)
+
+
+class _TorchOps:
+    """Vector kernels for the distributed GMRES: the C-ABI block kernels on
+    CUDA, plain torch on CPU (gloo tests)."""
+
+    def __init__(self, engine=None):
+        self.eng = engine
+
+    def dot(self, V, w, k, h):                 # h[r][i] = <V_i^r, w^r>
+        if self.eng is not None and w.is_cuda:
+            return self.eng.block_dot(V, w, k, h)
+        h[:, :k] = torch.einsum("krn,rn->rk", V[:k].conj(), w)
+        return h
+
+    def axpy(self, V, h, k, w):                # w -= sum_i h_i V_i
+        if self.eng is not None and w.is_cuda:
+            return self.eng.block_axpy(V, h, k, w)
+        w -= torch.einsum("rk,krn->rn", h[:, :k], V[:k])
+        return w
+
+    def norm2(self, w, out):
+        if self.eng is not None and w.is_cuda:
+            return self.eng.norm2(w, out)
+        out.copy_((w.real ** 2 + w.imag ** 2).sum(dim=1))
+        return out
+
+
+def gmres_dist(apply, rhs_own: torch.Tensor, tol: float = 1e-10, maxit: int = 150,
+               group=None, engine=None):
+    """Unrestarted GMRES over target-sharded vectors, CGS2
+    Arnoldi, zero initial guess, per-RHS stopping.  ``apply(v_own) -> y_own``
+    must do its own communication.  Returns (x_own, iterations, histories)."""
+    nrhs = rhs_own.shape[0]
+    shape = rhs_own.shape
+    n = rhs_own[0].numel()
+    dev = rhs_own.device
+    ops = _TorchOps(engine)
+    V = torch.zeros((maxit + 1, nrhs, n), dtype=torch.complex128, device=dev)
+    b = rhs_own.reshape(nrhs, n)
+    nb = torch.empty(nrhs, dtype=torch.float64, device=dev)
+    ops.norm2(b, nb)
+    all_reduce_(nb, group)
+    bnorm = np.sqrt(nb.cpu().numpy())
+    active = bnorm > 0
+    V[0] = b / torch.as_tensor(np.where(active, bnorm, 1.0), device=dev)[:, None]
+    H = np.zeros((nrhs, maxit + 1, maxit), dtype=complex)
+    cs = np.zeros((nrhs, maxit), dtype=complex)
+    sn = np.zeros((nrhs, maxit), dtype=complex)
+    g = np.zeros((nrhs, maxit + 1), dtype=complex)
+    g[:, 0] = bnorm
+    hist = [[1.0 if a else 0.0] for a in active]
+    iters = [0] * nrhs
+    h1 = torch.zeros((nrhs, maxit + 1), dtype=torch.complex128, device=dev)
+    h2 = torch.zeros_like(h1)
+    w2 = torch.empty(nrhs, dtype=torch.float64, device=dev)
+    k = 0
+    for k in range(maxit):
+        if not active.any():
+            break
+        w = apply(V[k].reshape(shape)).reshape(nrhs, n).clone()
+        amask = torch.as_tensor(active, device=dev)
+        w[~amask] = 0
+        ops.dot(V, w, k + 1, h1)
+        hk = h1[:, :k + 1].contiguous()
+        all_reduce_(hk, group)
+        ops.axpy(V, hk, k + 1, w)
+        ops.dot(V, w, k + 1, h2)
+        hk2 = h2[:, :k + 1].contiguous()
+        all_reduce_(hk2, group)
+        ops.axpy(V, hk2, k + 1, w)
+        ops.norm2(w, w2)
+        all_reduce_(w2, group)
+        hcol = (hk + hk2).cpu().numpy()
+        wn = np.sqrt(w2.cpu().numpy())
+        if not np.all(np.isfinite(hcol)) or not np.all(np.isfinite(wn)):
+            raise FloatingPointError("gmres_dist: NaN/Inf in Krylov vector (SPEC.md:553)")
+        scale = np.where(active & (wn > 0), wn, 1.0)
+        V[k + 1] = w / torch.as_tensor(scale, device=dev)[:, None]
+        for r in range(nrhs):
+            if not active[r]:
+                continue
+            col = H[r, :, k]
+            col[:k + 1] = hcol[r]
+            col[k + 1] = wn[r]
+            for i in range(k):
+                t = np.conj(cs[r, i]) * col[i] + np.conj(sn[r, i]) * col[i + 1]
+                col[i + 1] = -sn[r, i] * col[i] + cs[r, i] * col[i + 1]
+                col[i] = t
+            a_, b_ = col[k], col[k + 1]
+            rr = math.hypot(abs(a_), abs(b_))
+            cs[r, k] = a_ / rr if rr else 1.0
+            sn[r, k] = b_ / rr if rr else 0.0
+            col[k] = rr
+            col[k + 1] = 0.0
+            g[r, k + 1] = -sn[r, k] * g[r, k]
+            g[r, k] = np.conj(cs[r, k]) * g[r, k]
+            res = abs(g[r, k + 1]) / bnorm[r]
+            hist[r].append(res)
+            iters[r] = k + 1
+            if res <= tol:
+                active[r] = False
+    x = torch.zeros((nrhs, n), dtype=torch.complex128, device=dev)
+    kmax = max(iters) if iters else 0
+    ny = np.zeros((nrhs, kmax), dtype=complex)
+    for r in range(nrhs):
+        kk = iters[r]
+        if kk:
+            ny[r, :kk] = -np.linalg.solve(np.triu(H[r, :kk, :kk]), g[r, :kk])
+    if kmax:
+        ops.axpy(V, torch.as_tensor(ny, device=dev).contiguous(), kmax, x)   # x = sum_i y_i V_i
+    return x.reshape(shape), iters, hist

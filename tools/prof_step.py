@@ -1,0 +1,25 @@
+"""Minimal Schur-matvec loop for ncu captures (cfg3 by default)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_1412_7466_b200 import grating, solver
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--cfg", type=int, default=3)
+ap.add_argument("--steps", type=int, default=3)
+a = ap.parse_args()
+sysm, centers, p, radius = grating.load_config(a.cfg)
+op = solver.SchurOperator(sysm, centers, p, radius=radius)
+rng = np.random.default_rng(0)
+v = op.smat[None, None, :] * (rng.standard_normal((1, op.M, op.L)) + 1j * rng.standard_normal((1, op.M, op.L)))
+v = torch.as_tensor(v).cuda()
+y = torch.empty_like(v)
+for _ in range(a.steps):
+    op(v, out=y)
+torch.cuda.synchronize()
+print("ok", float(y.abs().sum()))
