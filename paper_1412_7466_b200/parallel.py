@@ -42,10 +42,14 @@ def all_gather_rows(v_own: torch.Tensor, M: int, group=None) -> torch.Tensor:
         dist.all_gather_into_tensor(buf, vr, group=group)
         full = buf.permute(1, 0, 2, 3, 4).reshape(v_own.shape[0], M, v_own.shape[2], 2)
         return torch.view_as_complex(full.contiguous())
-    parts = [torch.empty((v_own.shape[0], s, v_own.shape[2], 2), dtype=vr.dtype,
-                         device=vr.device) for s in sizes]
-    dist.all_gather(parts, vr, group=group)
-    return torch.view_as_complex(torch.cat(parts, dim=1).contiguous())
+    # uneven shards: pad every rank's rows to the largest shard, gather, trim
+    mx = max(sizes)
+    pad = torch.zeros((v_own.shape[0], mx, v_own.shape[2], 2), dtype=vr.dtype, device=vr.device)
+    pad[:, :vr.shape[1]] = vr
+    parts = [torch.empty_like(pad) for _ in sizes]
+    dist.all_gather(parts, pad, group=group)
+    full = torch.cat([p[:, :s] for p, s in zip(parts, sizes)], dim=1)
+    return torch.view_as_complex(full.contiguous())
 
 
 def all_reduce_(t: torch.Tensor, group=None) -> torch.Tensor:

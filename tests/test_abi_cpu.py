@@ -1,0 +1,88 @@
+"""CPU-side checks of the product boundary (no GPU): the C-ABI library loads,
+exports every symbol include/periscat_b200.h declares, and the ctypes
+signatures cover them; the product fails loudly without a device; the
+Bessel/Hankel device code (compiled for the host) matches scipy."""
+import ctypes
+import os
+import re
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "periscat_b200.h")
+CSRC = os.path.join(ROOT, "paper_1412_7466_b200", "csrc")
+
+
+def _declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(ps_\w+)\s*\(", txt, re.M)))
+
+
+def test_header_declares_api():
+    names = _declared()
+    for must in ("ps_create", "ps_apply_T", "ps_apply_schur", "ps_gmres", "ps_set_pinv"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1412_7466_b200 import _lib
+    lib = _lib.load()
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert set(_declared()) == set(_lib.SIGNATURES)
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    exported = set(re.findall(r"\bT (ps_\w+)", out))
+    assert set(_declared()) <= exported
+
+
+def test_library_is_sm100a():
+    from paper_1412_7466_b200 import _lib
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1412_7466_b200 import engine
+    with pytest.raises(RuntimeError):
+        engine.Engine(0)
+
+
+def test_host_compiled_hankel_symbols_match_scipy(tmp_path):
+    """bessel.cuh / symbols.cuh compiled for the host: |H_nu| relative error."""
+    import scipy.special as sps
+    src = tmp_path / "h.cpp"
+    src.write_text(r'''
+#include "symbols.cuh"
+extern "C" void sym(const double* z, const double* c, const double* s, int n, double* out) {
+  for (int i = 0; i < n; ++i) {
+    double* o = out + (size_t)i * 2 * 101;
+    ps::hankel_symbols<50>(z[i], c[i], s[i], ps::miller_start_j01(z[i]),
+        [&](int nu, double re, double im) { o[2 * (nu + 50)] = re; o[2 * (nu + 50) + 1] = im; });
+  }
+}''')
+    so = tmp_path / "h.so"
+    subprocess.run(["g++", "-O2", "-shared", "-fPIC", "-I", CSRC, str(src), "-o", str(so)],
+                   check=True)
+    lib = ctypes.CDLL(str(so))
+    rng = np.random.default_rng(0)
+    z = np.concatenate([np.geomspace(0.05, 60, 300), rng.uniform(0.1, 30, 300)])
+    phi = rng.uniform(-np.pi, np.pi, z.size)
+    out = np.zeros((z.size, 101, 2))
+    P = ctypes.POINTER(ctypes.c_double)
+    c, s = np.cos(phi), np.sin(phi)
+    lib.sym(z.ctypes.data_as(P), c.ctypes.data_as(P), s.ctypes.data_as(P), z.size,
+            out.ctypes.data_as(P))
+    got = out[..., 0] + 1j * out[..., 1]
+    nu = np.arange(-50, 51)
+    ref = sps.hankel1(nu[None, :], z[:, None]) * np.exp(1j * nu[None, :] * phi[:, None])
+    ok = np.isfinite(ref) & (np.abs(ref) < 1e300)
+    err = np.where(ok, np.abs(got - ref) / np.where(ok, np.abs(ref), 1), 0)
+    assert err.max() < 1e-12
