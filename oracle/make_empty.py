@@ -43,9 +43,19 @@ def config_for(omega: float, theta_ref: float) -> ProblemConfig:
                          interface_bottom=InterfaceSpec(-0.5))
 
 
+# cfg5: omega = 10, 16 angles theta_B = linspace(-pi/3, pi/3, 16), theta_ref = theta_B - pi/2
+CFG5_THETA_B = [(-math.pi / 3) + i * (2 * math.pi / 3) / 15 for i in range(16)]
+
+
+def phys(name: str):
+    if name.startswith("w10_a"):
+        return 10.0, CFG5_THETA_B[int(name[5:])] - 0.5 * math.pi
+    return PHYS[name]
+
+
 def make(name: str, omega=None, theta=None) -> str:
     if omega is None:
-        omega, theta = PHYS[name]
+        omega, theta = phys(name)
     conf = config_for(omega, theta)
     t0 = time.perf_counter()
     sysm = assemble_empty_system(conf)

@@ -282,6 +282,9 @@ int ps_apply_T(ps_ctx* h, const void* beta, void* out, void* stream) {
   if (int rc = set_device(c)) return rc;
   auto st = reinterpret_cast<cudaStream_t>(stream);
   const int np = 2 * c->copies + 3;
+  if (c->nrhs > 1)
+    return ps::m2l_apply_mrhs(c, reinterpret_cast<const double2*>(beta),
+                              reinterpret_cast<double2*>(out), 0, nullptr, 0, st);
   const size_t in_stride = (size_t)c->M * c->L, out_stride = (size_t)(c->t_end - c->t_begin) * c->L;
   for (int r = 0; r < c->nrhs; ++r) {
     int rc = ps::m2l_apply(c, reinterpret_cast<const double2*>(beta) + r * in_stride,

@@ -494,12 +494,19 @@ struct Work {
   double2 *g, *h, *x, *bsub, *u, *gpart, *bpart;
 };
 
-int work(Ctx* c, int r, Work* w) {
+size_t work_stride(const Ctx* c) {
   const size_t nrc = c->nrow_c, nsv = c->nsv > 0 ? c->nsv : 1;
   const size_t nout = c->ncol_b + 2 * c->nrb;
   const size_t mtl = (size_t)(c->t_end - c->t_begin) * c->L;
   const size_t nch = c->have_layers ? (size_t)b_chunks(c) : 0;
-  const size_t per = nrc + nsv + nout + 2 * mtl + 512 * nrc + nch * mtl + 8;
+  return nrc + nsv + nout + 2 * mtl + 512 * nrc + nch * mtl + 8;
+}
+
+int work(Ctx* c, int r, Work* w) {
+  const size_t nrc = c->nrow_c, nsv = c->nsv > 0 ? c->nsv : 1;
+  const size_t nout = c->ncol_b + 2 * c->nrb;
+  const size_t mtl = (size_t)(c->t_end - c->t_begin) * c->L;
+  const size_t per = work_stride(c);
   const size_t need = per * c->nrhs;
   if (c->work_elems < need) {
     if (c->d_work) cudaFree(c->d_work);
@@ -565,10 +572,37 @@ static int s_apply(Ctx* c, const double2* v_own, const double2* u, double2* y, c
   return PS_OK;
 }
 
+// multi-RHS: coupling per RHS into the workspace slots, then ONE K1m launch
+static int schur_mrhs(Ctx* c, const double2* v, double2* y, bool coupled, cudaStream_t st) {
+  const size_t in_stride = (size_t)c->M * c->L;
+  const size_t out_stride = (size_t)(c->t_end - c->t_begin) * c->L;
+  Work w0;
+  if (int rc = work(c, 0, &w0)) return rc;
+  const long long bstride = (long long)work_stride(c);
+  const int mode = c->s_diag ? 1 : 2;
+  if (int rc = m2l_apply_mrhs(c, v, y, mode, coupled ? w0.bsub : nullptr, bstride, st)) return rc;
+  if (!c->s_diag) {
+    for (int r = 0; r < c->nrhs; ++r) {
+      const double2* v_own = v + r * in_stride + (size_t)c->t_begin * c->L;
+      if (int rc = s_apply(c, v_own, y + r * out_stride, y + r * out_stride, st)) return rc;
+    }
+  }
+  return PS_OK;
+}
+
 int apply_schur_g(Ctx* c, const double2* v, const double2* g, double2* y, cudaStream_t st) {
   const size_t in_stride = (size_t)c->M * c->L;
   const size_t out_stride = (size_t)(c->t_end - c->t_begin) * c->L;
   const bool coupled = c->have_layers && c->rhs[0].d_Uh && g;
+  if (c->nrhs > 1) {
+    if (coupled)
+      for (int r = 0; r < c->nrhs; ++r) {
+        Work w;
+        if (int rc = work(c, r, &w)) return rc;
+        if (int rc = b_pinv(c, r, g + (size_t)r * c->nrow_c, &w, st)) return rc;
+      }
+    return schur_mrhs(c, v, y, coupled, st);
+  }
   for (int r = 0; r < c->nrhs; ++r) {
     Work w;
     if (int rc = work(c, r, &w)) return rc;
@@ -601,6 +635,14 @@ int apply_schur(Ctx* c, const double2* v, double2* y, cudaStream_t st) {
     if (int rc = work(c, r, &w)) return rc;
     if (int rc = dispatch_c(c, v + r * in_stride, bpow_of(c, r), w.gpart, w.g, 0, c->M, st))
       return rc;
+  }
+  if (nrhs > 1) {
+    for (int r = 0; r < nrhs; ++r) {
+      Work w;
+      if (int rc = work(c, r, &w)) return rc;
+      if (int rc = b_pinv(c, r, w.g, &w, st)) return rc;
+    }
+    return schur_mrhs(c, v, y, true, st);
   }
   for (int r = 0; r < nrhs; ++r) {
     Work w;

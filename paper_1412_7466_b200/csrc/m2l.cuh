@@ -14,4 +14,8 @@ int m2l_max_order();
 // out: [nt][L] for the owned targets; see m2l.cu for the epilogue modes.
 int m2l_apply(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
               const double2* v_own, const double2* bsub, cudaStream_t st);
+// All ctx->nrhs right-hand sides at once (m2l_mrhs.cu).  beta [nrhs][M][L],
+// out [nrhs][nt][L]; bsub (mode 1/2) for RHS r at bsub + r * b_stride.
+int m2l_apply_mrhs(Ctx* ctx, const double2* beta, double2* out, int mode, const double2* bsub,
+                   long long b_stride, cudaStream_t st);
 }  // namespace ps

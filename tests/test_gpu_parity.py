@@ -145,3 +145,103 @@ def test_solve_full_cfg1(O):
     assert abs(sol.flux[0]["error"] - ref.flux["error"]) <= 1e-9
     assert sol.flux[0]["error"] <= 1e-9
     assert abs(sol.iterations[0] - ref.iterations) <= 1
+
+
+# ---------------------------------------------------------------- multi-RHS (K1m)
+def test_apply_T_16rhs_cfg2(O):
+    """cfg5-style batch of 16 RHS (different Bloch phases) through K1m."""
+    from paper_1412_7466_b200 import multiscat
+    pb = O.load_problem(2)
+    rng = np.random.default_rng(16)
+    beta = pb.smat[None, None, :] * _cplx(rng, (16, pb.M, pb.L))
+    bl = np.exp(1j * rng.uniform(-np.pi, np.pi, 16))
+    ref = O.apply_T(beta, pb.centers, pb.es.k2, pb.p, bl)
+    got = multiscat.apply_T(beta, pb.centers, pb.es.k2, pb.p, bl)
+    for r in range(16):
+        assert rel(got[r], ref[r]) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("nrhs,p,M", [(2, 25, 17), (5, 7, 33), (19, 3, 9)])
+def test_apply_T_mrhs_shapes(O, nrhs, p, M):
+    """Odd RHS counts, more than one RHS group, ragged target tiles."""
+    from paper_1412_7466_b200 import multiscat
+    rng = np.random.default_rng(nrhs * 1000 + p)
+    centers = np.column_stack([rng.uniform(-0.45, 0.45, M), rng.uniform(-0.4, 0.4, M)])
+    beta = _cplx(rng, (nrhs, M, 2 * p + 1))
+    bl = np.exp(1j * rng.uniform(-np.pi, np.pi, nrhs))
+    ref = O.apply_T(beta, centers, 11.0, p, bl)
+    got = multiscat.apply_T(beta, centers, 11.0, p, bl)
+    for r in range(nrhs):
+        assert rel(got[r], ref[r]) <= MATVEC_TOL
+
+
+ANGLES = ["w10", "w10_a00", "w10_a15"]
+
+
+def test_schur_multi_rhs_matches_oracle(O):
+    """Three incidence angles (own Bloch phase, SVD factors, f) in one batch."""
+    from paper_1412_7466_b200 import grating, solver
+    pb = O.load_problem(1)
+    systems = [grating.load_fixture(n) for n in ANGLES]
+    op = solver.SchurOperator(systems, pb.centers, pb.p, smat=pb.smat)
+    rng = np.random.default_rng(33)
+    v = pb.smat[None, None, :] * _cplx(rng, (3, pb.M, pb.L))
+    got = op(_dev(v)).cpu().numpy()
+    rhs = op.rhs().cpu().numpy()
+    for r, name in enumerate(ANGLES):
+        pr = O.Problem(O.load_empty(name), pb.centers, pb.p, pb.radius, pb.smat)
+        assert rel(got[r], O.apply_schur_operator(pr, v[r]).reshape(pb.M, pb.L)) <= MATVEC_TOL
+        assert rel(rhs[r], O.schur_rhs(pr).reshape(pb.M, pb.L)) <= MATVEC_TOL
+
+
+def test_solve_full_multi_rhs(O):
+    """Batched device GMRES: per-RHS convergence and Bragg coefficients."""
+    from paper_1412_7466_b200 import grating, solver
+    pb = O.load_problem(1)
+    systems = [grating.load_fixture(n) for n in ANGLES]
+    sol = solver.solve_full(systems, pb.centers, pb.p, smat=pb.smat)
+    for r, name in enumerate(ANGLES):
+        pr = O.Problem(O.load_empty(name), pb.centers, pb.p, pb.radius, pb.smat)
+        ref = O.solve_full(pr)
+        assert rel(sol.c[r], ref.c) <= 1e-9
+        assert rel(sol.d[r], ref.d) <= 1e-9
+        assert abs(sol.flux[r]["error"] - ref.flux["error"]) <= 1e-9
+        assert abs(sol.iterations[r] - ref.iterations) <= 1
+
+
+# ---------------------------------------------------------------- golden full solves
+def _golden(cfg):
+    import os
+    from oracle.periscat_oracle import GOLDEN
+    path = os.path.join(GOLDEN, f"golden_cfg{cfg}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"golden_cfg{cfg}.npz not generated")
+    return np.load(path)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_matvec_vs_golden(O, cfg):
+    """apply_T and the Schur operator against the committed oracle goldens."""
+    z = _golden(cfg)
+    pb, op = _operator(O, cfg)
+    v = torch.as_tensor(z["v"][None]).cuda()
+    tids = z["targets"]
+    aT = op.apply_T(v).cpu().numpy()[0][tids]
+    sch = op(v).cpu().numpy()[0][tids]
+    assert rel(aT, z["apply_T"]) <= MATVEC_TOL
+    assert rel(sch, z["schur"]) <= MATVEC_TOL
+    assert rel(op.rhs().cpu().numpy()[0][tids], z["rhs"]) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_solve_full_vs_golden(O, cfg):
+    """Full device solve vs the oracle's solve (c, d <= 1e-9 rel, |dflux| <= 1e-9)."""
+    from paper_1412_7466_b200 import grating, solver
+    z = _golden(cfg)
+    pb = O.load_problem(cfg)
+    sol = solver.solve_full(grating.load_fixture(O.CONFIGS[cfg]["empty"]), pb.centers, pb.p,
+                            smat=pb.smat)
+    assert rel(sol.c[0], z["c"]) <= 1e-9
+    assert rel(sol.d[0], z["d"]) <= 1e-9
+    assert abs(sol.flux[0]["error"] - float(z["flux_error"])) <= 1e-9
+    assert abs(sol.iterations[0] - int(z["iterations"])) <= 1
