@@ -119,48 +119,57 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """nvidia-smi in loop mode (-lms 100) for the duration of the timed region."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
-                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self.proc = None
+        self.out = ""
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                self.out = ""
 
     def summary(self):
-        if not self.rows:
+        rows = [[x.strip() for x in ln.split(",")] for ln in self.out.strip().splitlines() if ln]
+        rows = [r for r in rows if len(r) >= 7]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(r[0]) for r in rows) if v is not None]
+        mx = [v for v in (num(r[1]) for r in rows) if v is not None]
+        pw = [v for v in (num(r[2]) for r in rows) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if r[3 + i].lower().startswith("active")})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "power_w_max": max(pw) if pw else None, "samples": len(rows)}
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -310,6 +319,14 @@ def run_ours(args):
                 "note": "wall clock incl. operator setup (SVD factors uploaded, S, geometry); "
                         "empty-grating assembly+SVD from fixture excluded"}
 
+    # cfg5 (M=1e4, p=20, 16 incidence angles): the multi-RHS K1 alone, own
+    # target shard, translations/s over the whole job, K1m roofline
+    cfg5 = None
+    if not args.no_cfg5:
+        sus = ctypes.c_double()
+        _lib.check(None, lib.ps_dfma_sustained(local, 3.0, ctypes.byref(sus)))
+        cfg5 = cfg5_apply_T(dev, local, rank, world, sus.value, args)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, cores, sample, _ = cpu_oracle_rate(3, 1)
@@ -334,7 +351,8 @@ def run_ours(args):
                         "d2h_bytes_per_step": int(yh.numel() * 16)},
                 "gpu_launches": int(stats["launches"]),
                 "clocks": clk.summary(),
-                "full_solve_m1000": full}
+                "full_solve_m1000": full,
+                "cfg5_apply_T_16rhs": cfg5}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -342,13 +360,68 @@ def run_ours(args):
     return 0
 
 
+def cfg5_apply_T(dev, local, rank, world, peak, args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1412_7466_b200.engine import Engine
+    centers = np.load(os.path.join(ROOT, "tests", "golden", "centers_cfg5.npy"))
+    M, p, R = centers.shape[0], 20, 16
+    L = 2 * p + 1
+    th = np.linspace(-math.pi / 3, math.pi / 3, R) - math.pi / 2
+    eng = Engine(local)
+    eng.set_geometry(centers, p, 12.0, 1.0, 1)
+    eng.set_bloch(np.exp(1j * 10.0 * np.cos(th)))
+    t0, t1 = (M * rank) // world, (M * (rank + 1)) // world
+    eng.set_target_range(t0, t1)
+    rng = np.random.default_rng(5)
+    v = torch.as_tensor(rng.standard_normal((R, M, L)) + 1j * rng.standard_normal((R, M, L))).to(dev)
+    out = eng.empty_own()
+    eng.apply_T(v, out)                       # warm-up (also sizes the workspaces)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    eng.stats_reset()
+    eng.profile(True)
+    steps = max(1, min(args.steps, 3))
+    st = torch.cuda.current_stream()
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            eng.apply_T(v, out)
+        e1.record(st)
+        e1.synchronize()
+    eng.profile(False)
+    stats = eng.stats()
+    t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    tr = M * (3 * M - 1) * R
+    k1_ms = stats["k1_ms"] / max(stats["k1_count"], 1)
+    flops = (t1 - t0) * (3 * M - 1) * R * 8.0 * L * L
+    ach = flops / (k1_ms * 1e-3) / 1e12
+    eng.close()
+    return {"workload": f"cfg5: apply_T (K1m), M={M}, p={p}, {R} RHS (incidence angles), "
+                        "target-sharded", "ms_per_step": ms, "steps": steps,
+            "value": tr / (ms * 1e-3), "unit": UNIT,
+            "roofline": {"bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                         "frac": ach / peak, "kernel": "m2l_mrhs_kernel (K1m)",
+                         "peak_source": "ps_dfma_sustained: DFMA-chain kernel back to back "
+                                        "for 3 s on this GPU (sustained clock)"},
+            "gpu_launches": int(stats["launches"]), "clocks": clk.summary()}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline leg")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the cfg5 16-RHS apply_T block")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

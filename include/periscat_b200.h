@@ -149,6 +149,9 @@ int ps_stats_reset(ps_ctx* ctx);
 /* ---- roofline denominator ---------------------------------------------- */
 /* DFMA-chain FP64 throughput of the device (TFLOP/s, 2 flops per FMA). */
 int ps_dfma_peak(int device, double* tflops, double* ms);
+/* Same kernel launched back to back for ~seconds (sustained clock under the
+ * power cap): the denominator for kernels timed inside a long step. */
+int ps_dfma_sustained(int device, double seconds, double* tflops);
 
 #ifdef __cplusplus
 }

@@ -42,6 +42,7 @@ SIGNATURES = {
     "ps_norm2": (_I, [_P, _I, _I, _P, _P, _P]),
     "ps_gmres": (_I, [_P, _P, _P, _D, _I, _IP, _DP, _P]),
     "ps_dfma_peak": (_I, [_I, _DP, _DP]),
+    "ps_dfma_sustained": (_I, [_I, _D, _DP]),
     "ps_profile": (_I, [_P, _I]),
     "ps_stats": (_I, [_P, ctypes.POINTER(ctypes.c_longlong), _DP, ctypes.POINTER(ctypes.c_longlong)]),
     "ps_stats_reset": (_I, [_P]),

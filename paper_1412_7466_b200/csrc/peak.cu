@@ -24,6 +24,47 @@ __global__ void __launch_bounds__(256) dfma_chains(double* out, int iters, doubl
 
 }  // namespace
 
+// Back-to-back DFMA launches for ~seconds: the clock the FP64 pipe holds
+// under a sustained load (power cap) -- the denominator for long kernels.
+extern "C" int ps_dfma_sustained(int device, double seconds, double* tflops) {
+  if (cudaSetDevice(device) != cudaSuccess) return PS_ERR_CUDA;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double)) != cudaSuccess) return PS_ERR_CUDA;
+  const int blocks = sms * 8, threads = 256, iters = 1 << 14;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  dfma_chains<<<blocks, threads>>>(d, iters, 0.9999999, 1e-7);
+  cudaEventRecord(e0);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float one = 0;
+  {
+    cudaEventRecord(e0);
+    dfma_chains<<<blocks, threads>>>(d, iters, 0.9999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&one, e0, e1);
+  }
+  int reps = (int)(seconds * 1e3 / (one > 0 ? one : 1.0f));
+  if (reps < 1) reps = 1;
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) dfma_chains<<<blocks, threads>>>(d, iters, 0.9999999, 1e-7);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float t = 0;
+  cudaEventElapsedTime(&t, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (cudaGetLastError() != cudaSuccess) return PS_ERR_CUDA;
+  const double flops = 2.0 * 16.0 * (double)iters * blocks * threads * reps;
+  *tflops = flops / (t * 1e-3) / 1e12;
+  return PS_OK;
+}
+
 extern "C" int ps_dfma_peak(int device, double* tflops, double* ms) {
   if (cudaSetDevice(device) != cudaSuccess) return PS_ERR_CUDA;
   int sms = 0;
