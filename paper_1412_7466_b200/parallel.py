@@ -32,7 +32,7 @@ def shard_sizes(M: int, world: int) -> list[int]:
 
 def all_gather_rows(v_own: torch.Tensor, M: int, group=None) -> torch.Tensor:
     """[nrhs][M_own][L] on every rank -> [nrhs][M][L] (rows in rank order)."""
-    world = dist.get_world_size(group)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return v_own
     sizes = shard_sizes(M, world)
