@@ -42,7 +42,8 @@ constexpr int kThreads = (kS + kPW) * 32;
 constexpr int kPairs = kTT * kS;       // symbol rows per batch
 constexpr int kPairsPerWarp = kPairs / kPW;
 static_assert(kTT * kNB == 32, "one consumer warp covers a full target tile");
-static_assert(kPairs % kPW == 0 && kPairsPerWarp <= 32, "at most one pair per producer lane");
+static_assert(kPairs % kPW == 0 && 2 * kPairsPerWarp == 32,
+              "two producer lanes per symbol row (t_+nu / t_-nu halves)");
 
 template <int P>
 struct Shape {
@@ -82,8 +83,10 @@ __device__ __forceinline__ void produce(const Args& a, long long w, double2* sym
   const int tile = (int)(w / a.nbatch);
   const int sb = (int)(w % a.nbatch) * kS;
   const int pw = pi >> 5, lane = pi & 31;
-  if (lane < kPairsPerWarp) {
-    const int pair = pw * kPairsPerWarp + lane;
+  {
+    // lanes 2q, 2q+1 build row q: t_{0..2p} and t_{-1..-2p}
+    const int pair = pw * kPairsPerWarp + (lane >> 1);
+    const bool mirror = lane & 1;
     const int s = pair / kTT, t = pair % kTT;
     const int mloc = tile * kTT + t;
     const int g = sb + s;
@@ -104,14 +107,14 @@ __device__ __forceinline__ void produce(const Args& a, long long w, double2* sym
     const double z = a.k2 * rho;
     // warp-uniform Miller start: no divergence, uniform constant-bank index
     int N = live ? miller_start_j01(z) : 2;
-    constexpr unsigned kMask = kPairsPerWarp == 32 ? 0xffffffffu : ((1u << kPairsPerWarp) - 1u);
-    N = __reduce_max_sync(kMask, N);
+    N = __reduce_max_sync(0xffffffffu, N);
     const double inv = live ? 1.0 / rho : 0.0;  // dead pairs (self term, padding): c = s = 0
     double2* base = col + (S::FP + 2 * P) * kTT;
-    hankel_symbols<2 * P>(z, dx * inv, dy * inv, N, [&](int nu, double re, double im) {
-      if (nu == 0 && !live) re = im = 0.0;
-      base[nu * kTT] = make_double2(re, im);
-    });
+    hankel_symbols_half<2 * P>(z, dx * inv, dy * inv, N, mirror,
+                               [&](int nu, double re, double im) {
+                                 if (nu == 0 && !live) re = im = 0.0;
+                                 base[nu * kTT] = make_double2(re, im);
+                               });
   }
   // bloch-weighted beta of the batch's source images
   for (int idx = pi; idx < kS * S::L; idx += kPW * 32) {

@@ -104,6 +104,24 @@ __device__ __forceinline__ void produce_m(const ArgsM& a, long long w, double2* 
   });
 }
 
+// Pull the bloch-weighted beta rows of batch w into L2 ahead of the consumers
+// (the cfg5 copy is 315 MB, beyond the 126 MB L2).  All 128 producer lanes
+// take one (rhs, image) row each.
+template <int P>
+__device__ __forceinline__ void prefetch_bw(const ArgsM& a, long long w, int pl) {
+  using S = ShapeM<P>;
+  const int sb = (int)(w % a.nbatch) * kSB;
+  const int nr = min(kRG, a.nrhs - a.rg0);
+  for (int row = pl; row < nr * kSB; row += kPW * 32) {
+    const int r = a.rg0 + row / kSB;
+    const int g = sb + row % kSB;
+    if (g >= a.nimg) continue;
+    const char* p = reinterpret_cast<const char*>(a.bw + ((size_t)r * a.nimg + g) * S::L);
+    for (int off = 0; off < S::L * 16; off += 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p + off));
+  }
+}
+
 template <int P>
 __device__ __forceinline__ void consume_m(const double2* __restrict__ sym,
                                           const double2* __restrict__ b0,
@@ -174,10 +192,14 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mrhs_kernel(ArgsM a) {
   if (producer) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
     const int pw = warp - kCW;
+    prefetch_bw<P>(a, w0, pw * 32 + lane);
     produce_m<P>(a, w0, sym0, pw, lane);
     __syncthreads();
+    const int pl = pw * 32 + lane;
+    if (w0 + 1 < w1) prefetch_bw<P>(a, w0 + 1, pl);
     for (long long w = w0; w < w1; ++w) {
       const int cur = (int)((w - w0) & 1);
+      if (w + 2 < w1) prefetch_bw<P>(a, w + 2, pl);
       if (w + 1 < w1) produce_m<P>(a, w + 1, cur ? sym0 : sym1, pw, lane);
       __syncthreads();
     }

@@ -58,4 +58,40 @@ PS_HD void hankel_symbols(double z, double c, double s, int N, Out out) {
   if (NU & 1) step(true);
 }
 
+// Half of a symbol row for two cooperating lanes.  mirror = false emits
+// t_nu (nu = 0..NU); mirror = true emits t_{-nu} (nu = 1..NU) by running the
+// same recurrence on G_nu = (-1)^nu H_nu with the conjugate phase:
+//   G_0 = H_0, G_1 = -H_1, G_{nu+1} = -(2 nu / z) G_nu - G_{nu-1},
+//   t_{-nu} = G_nu e^{-i nu phi}
+// -- no extra operation per order, so both lanes of a pair run full-width.
+template <int NU, typename Out>
+PS_HD void hankel_symbols_half(double z, double c, double s, int N, bool mirror, Out out) {
+  double j0, j1, y0, y1;
+  bessel_jy01(z, N, &j0, &j1, &y0, &y1);
+  const double q = mirror ? -1.0 : 1.0;
+  if (!mirror) out(0, j0, y0);
+  double hmr = j0, hmi = y0;
+  double hr = q * j1, hi = q * y1;
+  const double sq = q * s;
+  double pr = c, pi = sq;
+  const double tz = q * (2.0 / z);
+#pragma unroll
+  for (int nu = 1; nu <= NU; ++nu) {
+    const double ar = fma(hr, pr, -hi * pi);
+    const double ai = fma(hr, pi, hi * pr);
+    out(mirror ? -nu : nu, ar, ai);
+    const double cf = (double)nu * tz;
+    const double nr = fma(cf, hr, -hmr);
+    const double ni = fma(cf, hi, -hmi);
+    hmr = hr;
+    hmi = hi;
+    hr = nr;
+    hi = ni;
+    const double qr = fma(pr, c, -pi * sq);
+    const double qi = fma(pr, sq, pi * c);
+    pr = qr;
+    pi = qi;
+  }
+}
+
 }  // namespace ps

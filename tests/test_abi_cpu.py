@@ -61,11 +61,17 @@ def test_host_compiled_hankel_symbols_match_scipy(tmp_path):
     src = tmp_path / "h.cpp"
     src.write_text(r'''
 #include "symbols.cuh"
-extern "C" void sym(const double* z, const double* c, const double* s, int n, double* out) {
+extern "C" void sym(const double* z, const double* c, const double* s, int n, double* out,
+                    int half) {
   for (int i = 0; i < n; ++i) {
     double* o = out + (size_t)i * 2 * 101;
-    ps::hankel_symbols<50>(z[i], c[i], s[i], ps::miller_start_j01(z[i]),
-        [&](int nu, double re, double im) { o[2 * (nu + 50)] = re; o[2 * (nu + 50) + 1] = im; });
+    auto f = [&](int nu, double re, double im) { o[2 * (nu + 50)] = re; o[2 * (nu + 50) + 1] = im; };
+    if (half) {
+      ps::hankel_symbols_half<50>(z[i], c[i], s[i], ps::miller_start_j01(z[i]), false, f);
+      ps::hankel_symbols_half<50>(z[i], c[i], s[i], ps::miller_start_j01(z[i]), true, f);
+    } else {
+      ps::hankel_symbols<50>(z[i], c[i], s[i], ps::miller_start_j01(z[i]), f);
+    }
   }
 }''')
     so = tmp_path / "h.so"
@@ -75,14 +81,15 @@ extern "C" void sym(const double* z, const double* c, const double* s, int n, do
     rng = np.random.default_rng(0)
     z = np.concatenate([np.geomspace(0.05, 60, 300), rng.uniform(0.1, 30, 300)])
     phi = rng.uniform(-np.pi, np.pi, z.size)
-    out = np.zeros((z.size, 101, 2))
     P = ctypes.POINTER(ctypes.c_double)
     c, s = np.cos(phi), np.sin(phi)
-    lib.sym(z.ctypes.data_as(P), c.ctypes.data_as(P), s.ctypes.data_as(P), z.size,
-            out.ctypes.data_as(P))
-    got = out[..., 0] + 1j * out[..., 1]
     nu = np.arange(-50, 51)
     ref = sps.hankel1(nu[None, :], z[:, None]) * np.exp(1j * nu[None, :] * phi[:, None])
     ok = np.isfinite(ref) & (np.abs(ref) < 1e300)
-    err = np.where(ok, np.abs(got - ref) / np.where(ok, np.abs(ref), 1), 0)
-    assert err.max() < 1e-12
+    for half in (0, 1):       # one-lane row and the two-lane (t_+nu / t_-nu) split of K1
+        out = np.zeros((z.size, 101, 2))
+        lib.sym(z.ctypes.data_as(P), c.ctypes.data_as(P), s.ctypes.data_as(P), z.size,
+                out.ctypes.data_as(P), half)
+        got = out[..., 0] + 1j * out[..., 1]
+        err = np.where(ok, np.abs(got - ref) / np.where(ok, np.abs(ref), 1), 0)
+        assert err.max() < 1e-12
