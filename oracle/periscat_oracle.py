@@ -243,7 +243,10 @@ _EMPTY_CACHE: dict = {}
 def load_empty(name: str) -> EmptySystem:
     if name in _EMPTY_CACHE:
         return _EMPTY_CACHE[name]
-    z = np.load(os.path.join(GOLDEN, f"empty_{name}.npz"))
+    path = os.path.join(GOLDEN, f"empty_{name}.npz")
+    if not os.path.exists(path):
+        path = os.path.join(GOLDEN, "cfg5", f"empty_{name}.npz")
+    z = np.load(path)
     cols = {str(n): slice(int(a), int(b)) for n, (a, b) in zip(z["col_names"], z["cols"])}
     rows = {str(n): slice(int(a), int(b)) for n, (a, b) in zip(z["row_names"], z["rows"])}
     sc = z["scalars"]
