@@ -60,9 +60,55 @@ struct CArgs {
   double period, k2;
 };
 
+// One (node, source image) pair of K3: symbols t_{+-nu}, nu = 0..P+1, built
+// by the reference recurrence (symbols.cuh) and folded straight into
+//   pv += sum_n b_n w_n,  pp += sum_nu b_{nu+1} w_nu,  pm += sum_nu b_{nu-1} w_nu
+// with every beta index a compile-time offset (fully unrolled) so the loads
+// are hoisted out of the recurrence.
+template <int P>
+__device__ __forceinline__ void c_pair(double z, double c, double s, int N,
+                                       const double2* __restrict__ bj, double2& pv, double2& pp,
+                                       double2& pm) {
+  auto B = [&](int n) -> double2 {
+    return (n >= -P && n <= P) ? __ldg(bj + n + P) : make_double2(0.0, 0.0);
+  };
+  double j0, j1, y0, y1;
+  bessel_jy01(z, N, &j0, &j1, &y0, &y1);
+  {
+    const double2 w = make_double2(j0, y0);
+    pv = cfma(B(0), w, pv);
+    pp = cfma(B(1), w, pp);
+    pm = cfma(B(-1), w, pm);
+  }
+  double hmr = j0, hmi = y0, hr = j1, hi = y1, pr = c, pi = s;
+  const double tz = 2.0 / z;
+#pragma unroll
+  for (int nu = 1; nu <= P + 1; ++nu) {
+    const double2 tp = make_double2(fma(hr, pr, -hi * pi), fma(hr, pi, hi * pr));
+    const double sg = (nu & 1) ? -1.0 : 1.0;
+    const double2 tm = make_double2(sg * fma(hr, pr, hi * pi), sg * fma(hi, pr, -hr * pi));
+    if (nu <= P) {
+      pv = cfma(B(nu), tp, pv);
+      pv = cfma(B(-nu), tm, pv);
+    }
+    pp = cfma(B(nu + 1), tp, pp);
+    pp = cfma(B(1 - nu), tm, pp);
+    pm = cfma(B(nu - 1), tp, pm);
+    pm = cfma(B(-nu - 1), tm, pm);
+    const double cf = (double)nu * tz;
+    const double nr = fma(cf, hr, -hmr), ni = fma(cf, hi, -hmi);
+    hmr = hr;
+    hmi = hi;
+    hr = nr;
+    hi = ni;
+    const double qr = fma(pr, c, -pi * s), qi = fma(pr, s, pi * c);
+    pr = qr;
+    pi = qi;
+  }
+}
+
 template <int P>
 __global__ void __launch_bounds__(kCT) c_kernel(CArgs a) {
-  constexpr int NU = P + 1;
   constexpr int L = 2 * P + 1;
   __shared__ double2 red[3 * kCT];
   const int row = blockIdx.x;              // target node index over g1, g2, wall
@@ -115,13 +161,7 @@ __global__ void __launch_bounds__(kCT) c_kernel(CArgs a) {
     const double2* bj = a.beta + (size_t)j * L;
     double2 pv = make_double2(0, 0), pp = make_double2(0, 0), pm = make_double2(0, 0);
     const double zz = a.k2 * rho;
-    hankel_symbols<NU>(zz, dx * inv, dy * inv, miller_start_j01(zz),
-                       [&](int nu, double re, double im) {
-                         const double2 w = make_double2(re, im);
-                         if (nu >= -P && nu <= P) pv = cfma(__ldg(bj + nu + P), w, pv);
-                         if (nu + 1 >= -P && nu + 1 <= P) pp = cfma(__ldg(bj + nu + 1 + P), w, pp);
-                         if (nu - 1 >= -P && nu - 1 <= P) pm = cfma(__ldg(bj + nu - 1 + P), w, pm);
-                       });
+    c_pair<P>(zz, dx * inv, dy * inv, miller_start_j01(zz), bj, pv, pp, pm);
     val = cfma(wgt, pv, val);
     sp = cfma(wgt, pp, sp);
     sm = cfma(wgt, pm, sm);
@@ -215,7 +255,8 @@ __global__ void f_minus(const double2* __restrict__ f, const double2* __restrict
 // (c_d = (i/4) bloch^l w mu), translated to x_m with the M2L symbols
 // t_nu of (x_m - y_l):  a[n'] += c_s t_{-n'} + beta_1 t_{1-n'} + beta_-1 t_{-1-n'}.
 // Chunk c = 0 additionally adds the L2L of the a2 J-expansion (B_pm).
-constexpr int kBT = 64;    // threads (= sources per chunk) for K5
+constexpr int kBT = 128;   // threads for K5: two lanes per source (t_+nu / t_-nu halves)
+constexpr int kBS = 64;    // sources per chunk
 
 struct BArgs {
   const double* centers;   // [M][2]
@@ -234,19 +275,19 @@ struct BShape {
   static constexpr int NSP = 2 * NU + 1;           // odd: conflict-free row stride
   static constexpr int L = 2 * P + 1;
   static constexpr int NQMAX = 36 + P;             // sized for Q <= 36 (ProblemConfig default)
-  static constexpr size_t SMEM_SYM = (size_t)kBT * NSP * sizeof(double2);
+  static constexpr size_t SMEM_SYM = (size_t)kBS * NSP * sizeof(double2);
   static constexpr size_t SMEM_JL = (size_t)(2 * NQMAX + 1) * sizeof(double2);
-  static constexpr size_t SMEM = (SMEM_SYM > SMEM_JL ? SMEM_SYM : SMEM_JL) + 3 * kBT * sizeof(double2);
+  static constexpr size_t SMEM = (SMEM_SYM > SMEM_JL ? SMEM_SYM : SMEM_JL) + 3 * kBS * sizeof(double2);
 };
 
 template <int P>
 __global__ void __launch_bounds__(kBT) b_kernel(BArgs a) {
   using S = BShape<P>;
   constexpr int NU = S::NU, NSP = S::NSP, L = S::L;
-  static_assert(L <= kBT, "one output order per thread");
+  static_assert(L <= kBT / 2, "one output order per thread of each half-CTA");
   extern __shared__ double2 bsm[];
-  double2* sym = bsm;                                   // [kBT][NSP]
-  double2* coef = bsm + (S::SMEM_SYM > S::SMEM_JL ? kBT * NSP : 2 * S::NQMAX + 1);   // [kBT][3]
+  double2* sym = bsm;                                   // [kBS][NSP]
+  double2* coef = bsm + (S::SMEM_SYM > S::SMEM_JL ? kBS * NSP : 2 * S::NQMAX + 1);   // [kBS][3]
   const int mloc = blockIdx.x;
   const int m = a.t_begin + mloc;
   const int chunk = blockIdx.y;
@@ -254,10 +295,12 @@ __global__ void __launch_bounds__(kBT) b_kernel(BArgs a) {
   const int nl = 2 * a.copies + 1;
   const int nsrc = (a.n1 + a.n2) * nl;
   const double hk = 0.5 * a.k2;
-  const int it = chunk * kBT + threadIdx.x;
-  const int nlive = min(kBT, nsrc - chunk * kBT);
+  const int src = threadIdx.x >> 1;          // lanes 2q, 2q+1 share source q
+  const bool mirror = threadIdx.x & 1;
+  const int it = chunk * kBS + src;
+  const int nlive = min(kBS, nsrc - chunk * kBS);
   {
-    double2* row = sym + (size_t)threadIdx.x * NSP;
+    double2* row = sym + (size_t)src * NSP;
     if (it < nsrc) {
       const int node = it / nl;
       const int l = it % nl - a.copies;
@@ -270,27 +313,34 @@ __global__ void __launch_bounds__(kBT) b_kernel(BArgs a) {
       const double2 iw = make_double2(-0.25 * w * wl.y, 0.25 * w * wl.x);   // (i/4) bloch^l w
       const double2 cd = cmul(iw, a.x[mu_col]);
       const double nx = q[2], ny = q[3];
-      coef[3 * threadIdx.x + 0] = cmul(iw, a.x[sg_col]);
-      coef[3 * threadIdx.x + 1] = cmul(cd, make_double2(hk * nx, -hk * ny));
-      coef[3 * threadIdx.x + 2] = cmul(cd, make_double2(-hk * nx, -hk * ny));
+      if (!mirror) {
+        coef[3 * src + 0] = cmul(iw, a.x[sg_col]);
+        coef[3 * src + 1] = cmul(cd, make_double2(hk * nx, -hk * ny));
+        coef[3 * src + 2] = cmul(cd, make_double2(-hk * nx, -hk * ny));
+      }
       const double dx = xm - q[0] - (double)l * a.period;
       const double dy = ym - q[1];
       const double rho = hypot(dx, dy);
       const double inv = 1.0 / rho;
       double2* r0 = row + NU;
       const double zz = a.k2 * rho;
-      hankel_symbols<NU>(zz, dx * inv, dy * inv, miller_start_j01(zz),
-                         [&](int nu, double re, double im) { r0[nu] = make_double2(re, im); });
+      hankel_symbols_half<NU>(zz, dx * inv, dy * inv, miller_start_j01(zz), mirror,
+                              [&](int nu, double re, double im) { r0[nu] = make_double2(re, im); });
     }
   }
   __syncthreads();
+  // accumulation: half h of the CTA sums sources [h*kBS/2, (h+1)*kBS/2) for
+  // output order n' = (threadIdx.x % (kBT/2)) - P, then the halves combine
   double2 out = make_double2(0, 0);
-  if (threadIdx.x < L) {
-    const int nprime = threadIdx.x - P;
+  const int half = threadIdx.x / (kBT / 2), op = threadIdx.x % (kBT / 2);
+  if (op < L) {
+    const int nprime = op - P;
     // six independent chains: (monopole, dipole+, dipole-) x (even, odd source)
     double2 c0 = make_double2(0, 0), c1 = c0, c2 = c0, c3 = c0, c4 = c0, c5 = c0;
-    int y = 0;
-    for (; y + 1 < nlive; y += 2) {
+    const int y0 = half * (kBS / 2);
+    const int y1 = min(nlive, y0 + kBS / 2);
+    int y = y0;
+    for (; y + 1 < y1; y += 2) {
       const double2* r = sym + (size_t)y * NSP + NU;
       const double2* r2 = r + NSP;
       c0 = cfma(coef[3 * y + 0], r[-nprime], c0);
@@ -300,7 +350,7 @@ __global__ void __launch_bounds__(kBT) b_kernel(BArgs a) {
       c4 = cfma(coef[3 * y + 4], r2[1 - nprime], c4);
       c5 = cfma(coef[3 * y + 5], r2[-1 - nprime], c5);
     }
-    if (y < nlive) {
+    if (y < y1) {
       const double2* r = sym + (size_t)y * NSP + NU;
       c0 = cfma(coef[3 * y + 0], r[-nprime], c0);
       c1 = cfma(coef[3 * y + 1], r[1 - nprime], c1);
@@ -308,6 +358,14 @@ __global__ void __launch_bounds__(kBT) b_kernel(BArgs a) {
     }
     out = make_double2(((c0.x + c3.x) + (c1.x + c4.x)) + (c2.x + c5.x),
                        ((c0.y + c3.y) + (c1.y + c4.y)) + (c2.y + c5.y));
+  }
+  __syncthreads();                       // symbol rows no longer needed
+  double2* comb = sym;                   // [kBT/2] partials of half 1
+  if (half == 1 && op < L) comb[op] = out;
+  __syncthreads();
+  if (half == 0 && op < L) {
+    out.x += comb[op].x;
+    out.y += comb[op].y;
   }
   if (chunk == 0) {
     // B_pm: L2L of the a2 expansion about x2:
@@ -377,8 +435,15 @@ __global__ void dense_s_epilogue(const double2* __restrict__ S, const double* __
 }
 
 int c_splits(const Ctx* c, int s0, int s1) {
+  // one full wave at 8 CTAs/SM, but at least ~2 pairs per thread and at most
+  // ~64 pairs per thread
+  const int rows = c->n1 + c->n2 + c->nw;
   const long long npair = (long long)(s1 - s0) * (2 * c->copies + 1);
-  long long ns = (npair + 4 * kCT - 1) / (4 * kCT);   // ~4 pairs per thread
+  long long ns = (8LL * c->sm_count + rows - 1) / rows;
+  const long long lo = (npair + 64LL * kCT - 1) / (64LL * kCT);
+  const long long hi = (npair + 2LL * kCT - 1) / (2LL * kCT);
+  if (ns < lo) ns = lo;
+  if (ns > hi) ns = hi;
   if (ns < 1) ns = 1;
   if (ns > 512) ns = 512;
   return (int)ns;
@@ -386,7 +451,7 @@ int c_splits(const Ctx* c, int s0, int s1) {
 
 int b_chunks(const Ctx* c) {
   const int nsrc = (c->n1 + c->n2) * (2 * c->copies + 1);
-  return (nsrc + kBT - 1) / kBT;
+  return (nsrc + kBS - 1) / kBS;
 }
 
 template <int P>
