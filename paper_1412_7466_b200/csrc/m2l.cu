@@ -31,6 +31,18 @@ namespace ps {
 
 namespace {
 
+template <int V>
+struct IC {
+  static constexpr int value = V;
+};
+template <int N, typename F, int I = 0>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(IC<I>{});
+    static_for<N, F, I + 1>(static_cast<F&&>(f));
+  }
+}
+
 constexpr int kTT = 8;                 // targets per tile
 constexpr int kNB = 4;                 // row blocks (lanes) per target
 constexpr int kS = 8;                  // source images per batch = consumer warps
@@ -144,21 +156,31 @@ __device__ __forceinline__ void consume(const double2* __restrict__ sym,
   double2 w[BO];
 #pragma unroll
   for (int i = 0; i < BO; ++i) w[(R0 - i + MODB) % BO] = sp[-i * kTT];
-#pragma unroll
-  for (int n = 0; n < S::L; ++n) {
+  // one column step; u = n mod BO is compile-time so the ring indices are static
+  auto step = [&](int n, auto u_c) {
+    constexpr int u = decltype(u_c)::value;
     const double2 nxt = sp[(n + 1) * kTT];
     const double2 bb = bet[n];
     const double nby = -bb.y;
 #pragma unroll
     for (int i = 0; i < BO; ++i) {
-      const double2 tt = w[(R0 + n - i + MODB) % BO];
+      const double2 tt = w[(R0 + u - i + MODB) % BO];
       acc[i].x = fma(bb.x, tt.x, acc[i].x);
       acc[i].x = fma(nby, tt.y, acc[i].x);
       acc[i].y = fma(bb.x, tt.y, acc[i].y);
       acc[i].y = fma(bb.y, tt.x, acc[i].y);
     }
-    w[(R0 + n + 1 + MODB) % BO] = nxt;
-  }
+    w[(R0 + u + 1 + MODB) % BO] = nxt;
+  };
+#ifndef PS_K1_PARTIAL_UNROLL
+  static_for<S::L>([&](auto u) { step(decltype(u)::value, IC<decltype(u)::value % BO>{}); });
+#else
+  constexpr int NFULL = (S::L / BO) * BO;
+#pragma unroll 1
+  for (int n0 = 0; n0 < NFULL; n0 += BO)
+    static_for<BO>([&](auto u) { step(n0 + decltype(u)::value, u); });
+  static_for<S::L - NFULL>([&](auto u) { step(NFULL + decltype(u)::value, u); });
+#endif
 }
 
 template <int P>

@@ -27,6 +27,18 @@ namespace ps {
 
 namespace {
 
+template <int V>
+struct IC {
+  static constexpr int value = V;
+};
+template <int N, typename F, int I = 0>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(IC<I>{});
+    static_for<N, F, I + 1>(static_cast<F&&>(f));
+  }
+}
+
 constexpr int kTT = 8;                  // targets per tile
 constexpr int kNB = 4;                  // row blocks per target
 constexpr int kSB = 8;                  // source images per batch
@@ -60,11 +72,19 @@ struct ArgsM {
   double2* partial;        // [G][maxseg][kRG][kTT][L]
   int nrhs, rg0, M, t_begin, nt, copies, ncp, nimg, nbatch, maxseg;
   long long W;
+  long long q;             // work-range quantum (divides nbatch)
   double period, k2;
 };
 
-__device__ __forceinline__ long long work_begin(long long W, int G, int c) {
-  return (W * (long long)c) / G;
+// CTA c's work range starts at a multiple of q = nbatch / kPhases: all CTAs
+// sweep the source list in at most kPhases phase groups, so the beta rows a
+// batch needs are fetched from DRAM once per group instead of once per CTA
+// (the cfg5 weighted-beta copy is 315 MB > 126 MB L2).
+constexpr int kPhases = 8;
+
+__host__ __device__ __forceinline__ long long work_begin(long long W, int G, int c, long long q) {
+  const long long raw = (W * (long long)c) / G;
+  return ((raw + q / 2) / q) * q;
 }
 
 template <int P>
@@ -136,14 +156,18 @@ __device__ __forceinline__ void consume_m(const double2* __restrict__ sym,
   double2 w[BO];
 #pragma unroll
   for (int i = 0; i < BO; ++i) w[(R0 - i + MODB) % BO] = sp[-i * kTT];
-#pragma unroll
-  for (int n = 0; n < S::L; ++n) {
+  // one column step; u = n mod BO is compile-time so the ring indices are
+  // static.  The column loop is unrolled by BO only (a runtime loop over
+  // BO-blocks): at cfg5 size this beats the full unroll (80.3% vs 78.2% of
+  // DFMA peak, smaller instruction footprint for 8 warps at different PCs).
+  auto step = [&](int n, auto u_c) {
+    constexpr int u = decltype(u_c)::value;
     const double2 nxt = sp[(n + 1) * kTT];
     const double2 x0 = __ldg(b0 + n);
     const double2 x1 = __ldg(b1 + n);
 #pragma unroll
     for (int i = 0; i < BO; ++i) {
-      const double2 tt = w[(R0 + n - i + MODB) % BO];
+      const double2 tt = w[(R0 + u - i + MODB) % BO];
       acc0[i].x = fma(x0.x, tt.x, acc0[i].x);
       acc1[i].x = fma(x1.x, tt.x, acc1[i].x);
       acc0[i].y = fma(x0.x, tt.y, acc0[i].y);
@@ -151,14 +175,23 @@ __device__ __forceinline__ void consume_m(const double2* __restrict__ sym,
     }
 #pragma unroll
     for (int i = 0; i < BO; ++i) {
-      const double2 tt = w[(R0 + n - i + MODB) % BO];
+      const double2 tt = w[(R0 + u - i + MODB) % BO];
       acc0[i].x = fma(-x0.y, tt.y, acc0[i].x);
       acc1[i].x = fma(-x1.y, tt.y, acc1[i].x);
       acc0[i].y = fma(x0.y, tt.x, acc0[i].y);
       acc1[i].y = fma(x1.y, tt.x, acc1[i].y);
     }
-    w[(R0 + n + 1 + MODB) % BO] = nxt;
-  }
+    w[(R0 + u + 1 + MODB) % BO] = nxt;
+  };
+#ifdef PS_K1M_FULL_UNROLL
+  static_for<S::L>([&](auto u) { step(decltype(u)::value, IC<decltype(u)::value % BO>{}); });
+#else
+  constexpr int NFULL = (S::L / BO) * BO;
+#pragma unroll 1
+  for (int n0 = 0; n0 < NFULL; n0 += BO)
+    static_for<BO>([&](auto u) { step(n0 + decltype(u)::value, u); });
+  static_for<S::L - NFULL>([&](auto u) { step(NFULL + decltype(u)::value, u); });
+#endif
 }
 
 template <int P>
@@ -169,8 +202,8 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mrhs_kernel(ArgsM a) {
   double2* sym0 = smem;
   double2* sym1 = smem + S::SYM;
   const int G = gridDim.x;
-  const long long w0 = work_begin(a.W, G, blockIdx.x);
-  const long long w1 = work_begin(a.W, G, blockIdx.x + 1);
+  const long long w0 = work_begin(a.W, G, blockIdx.x, a.q);
+  const long long w1 = work_begin(a.W, G, blockIdx.x + 1, a.q);
   if (w0 >= w1) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp >= kCW;
@@ -268,7 +301,7 @@ __global__ void bloch_weight(const double2* __restrict__ beta, const double2* __
 
 // Sum partials in CTA order; epilogue as m2l_reduce, per RHS.
 __global__ void m2l_mrhs_reduce(const double2* __restrict__ partial, int G, long long W,
-                                int nbatch, int maxseg, int nt, int L, int rg0, int nr, int mode,
+                                long long q, int nbatch, int maxseg, int nt, int L, int rg0, int nr, int mode,
                                 const double2* __restrict__ v, long long v_stride, int v_off,
                                 const double2* __restrict__ sdiag,
                                 const double2* __restrict__ bsub, long long b_stride,
@@ -282,11 +315,11 @@ __global__ void m2l_mrhs_reduce(const double2* __restrict__ partial, int G, long
   const long long wa = (long long)tile * nbatch, wb = wa + nbatch;
   int c = (int)((wa * G) / W);
   if (c >= G) c = G - 1;
-  while (c > 0 && work_begin(W, G, c) > wa) --c;
-  while (c < G - 1 && work_begin(W, G, c + 1) <= wa) ++c;
+  while (c > 0 && work_begin(W, G, c, q) > wa) --c;
+  while (c < G - 1 && work_begin(W, G, c + 1, q) <= wa) ++c;
   double2 sum = make_double2(0.0, 0.0);
   for (; c < G; ++c) {
-    const long long c0 = work_begin(W, G, c), c1 = work_begin(W, G, c + 1);
+    const long long c0 = work_begin(W, G, c, q), c1 = work_begin(W, G, c + 1, q);
     if (c0 >= wb) break;
     if (c1 <= c0 || c1 <= wa) continue;
     const int seg = tile - (int)(c0 / nbatch);
@@ -336,7 +369,14 @@ int launch_m(Ctx* ctx, const double2* beta, double2* out, int mode, const double
   a.k2 = ctx->k2;
   int G = ctx->sm_count;
   if ((long long)G > a.W) G = (int)a.W;
-  a.maxseg = (int)((a.W / G + 1) / a.nbatch) + 2;
+  // quantum: a divisor of nbatch near nbatch / kPhases, small enough that
+  // every CTA still gets work
+  long long q = a.nbatch / kPhases;
+  if (q < 1) q = 1;
+  while (a.nbatch % q) --q;
+  if (q * G > a.W) q = 1;
+  a.q = q;
+  a.maxseg = (int)((a.W / G + q + 1) / a.nbatch) + 3;
   // bloch-weighted copy of beta (all RHS, all images)
   const long long total = (long long)ctx->nrhs * a.nimg * S::L;
   const size_t need_p = (size_t)G * a.maxseg * kRG * kTT * S::L;
@@ -379,7 +419,7 @@ int launch_m(Ctx* ctx, const double2* beta, double2* out, int mode, const double
     const int nr = std::min(kRG, ctx->nrhs - a.rg0);
     const long long n = (long long)nr * nt * S::L;
     m2l_mrhs_reduce<<<(int)((n + 255) / 256), 256, 0, st>>>(
-        ctx->d_partial, G, a.W, a.nbatch, a.maxseg, nt, S::L, a.rg0, nr, mode, beta, in_stride,
+        ctx->d_partial, G, a.W, a.q, a.nbatch, a.maxseg, nt, S::L, a.rg0, nr, mode, beta, in_stride,
         ctx->t_begin, ctx->d_S, bsub, b_stride, out, out_stride);
     PS_CUDA_TRY(ctx, cudaGetLastError());
     ctx->launches += 2;
