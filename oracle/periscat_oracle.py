@@ -343,17 +343,35 @@ def apply_C(es: EmptySystem, beta, centers) -> np.ndarray:
 # ----------------------------------------------------------------------------
 # solver
 # ----------------------------------------------------------------------------
+def rotate_smatrix(S: np.ndarray, phi: float) -> np.ndarray:
+    """(S^(m))_{ln} = e^{i phi (l - n)} s_{ln}."""
+    p = (S.shape[0] - 1) // 2
+    idx = np.arange(-p, p + 1)
+    return S * np.exp(1j * phi * (idx[:, None] - idx[None, :]))
+
+
 @dataclass
 class Problem:
     es: EmptySystem
     centers: np.ndarray
     p: int
     radius: float
-    smat: np.ndarray = field(default=None)      # (L,) diagonal disk S
+    smat: np.ndarray = field(default=None)      # (L,) diagonal disk S or (L, L) dense
+    rot: np.ndarray = field(default=None)       # (M,) rotations for a dense S
 
     def __post_init__(self):
         if self.smat is None:
             self.smat = disk_smatrix(self.radius, self.es.k2, self.es.kp, self.p)
+
+    def apply_S(self, u: np.ndarray) -> np.ndarray:
+        """Block-diagonal S applied to u (M, L) (PA:667-679)."""
+        if self.smat.ndim == 1:
+            return self.smat[None, :] * u
+        out = np.empty_like(u)
+        for m in range(u.shape[0]):
+            Sm = self.smat if self.rot is None else rotate_smatrix(self.smat, self.rot[m])
+            out[m] = Sm @ u[m]
+        return out
 
     @property
     def M(self):
@@ -373,13 +391,13 @@ def apply_schur_operator(pb: Problem, v, with_coupling: bool = True) -> np.ndarr
     if with_coupling:
         x = es.apply_pinv(apply_C(es, v, pb.centers))
         u = u - apply_B_phys(es, x, pb.centers, pb.p)
-    return (v - pb.smat[None, :] * u).reshape(-1)
+    return (v - pb.apply_S(u)).reshape(-1)
 
 
 def schur_rhs(pb: Problem) -> np.ndarray:
     """-S B A^+ f = +S B_phys A^+ f."""
     x = pb.es.apply_pinv(pb.es.f)
-    return (pb.smat[None, :] * apply_B_phys(pb.es, x, pb.centers, pb.p)).reshape(-1)
+    return pb.apply_S(apply_B_phys(pb.es, x, pb.centers, pb.p)).reshape(-1)
 
 
 def gmres(op, rhs, tol: float = 1e-10, maxit: int = 150):

@@ -240,7 +240,10 @@ __global__ void init_state(GState s, int nrhs, int maxit, const double* __restri
   g[0] = make_double2(bn, 0.0);
   s.res[r] = bn > 0.0 ? 1.0 : 0.0;
   s.active[r] = bn > 0.0 ? 1 : 0;
-  if (r == 0) *s.nonfinite = 0;
+  if (!isfinite(bn)) {
+    s.active[r] = 0;
+    s.nonfinite[1 + r] = 1;      // per-RHS flag, checked by the host after init
+  }
 }
 
 __global__ void set_flags(int* active, const int* flags, int nrhs) {
@@ -375,7 +378,7 @@ int gmres(Ctx* c, const double2* rhs, double2* x, double tol, int maxit, int* it
   const size_t szHc = (size_t)nrhs * (maxit + 1);
   const size_t szPart = (size_t)nrhs * (maxit + 1) * nc;
   const size_t n2 = (size_t)nrhs * n;
-  const size_t total2 = szV + n2 + szH + 2 * szCS + szG + 2 * szHc + szPart + 8 * nrhs + 64;
+  const size_t total2 = szV + n2 + szH + 2 * szCS + szG + 2 * szHc + szPart + 8 * nrhs + 128;
   void* base;
   if (int rc = scratch(c, total2 * sizeof(double2), &base)) return rc;
   double2* p = (double2*)base;
@@ -396,7 +399,8 @@ int gmres(Ctx* c, const double2* rhs, double2* x, double tol, int maxit, int* it
   s.active = (int*)(dsmall + 3 * nrhs);
   int* kk_dev = s.active + nrhs;
   int* flags_dev = kk_dev + nrhs;
-  s.nonfinite = flags_dev + nrhs;
+  s.nonfinite = flags_dev + nrhs;          // [1 + nrhs]
+  PS_CUDA_TRY(c, cudaMemsetAsync(s.nonfinite, 0, (1 + nrhs) * sizeof(int), st));
 
   // init: V_0 = b / ||b||
   if (int rc = norm_impl(c, nrhs, n, rhs, nrm2, part, st)) return rc;
@@ -407,9 +411,16 @@ int gmres(Ctx* c, const double2* rhs, double2* x, double tol, int maxit, int* it
   PS_CUDA_TRY(c, cudaGetLastError());
 
   std::vector<double> res(nrhs), bn(nrhs);
-  std::vector<int> active(nrhs), kk(nrhs, 0);
+  std::vector<int> active(nrhs), kk(nrhs, 0), badrhs(nrhs + 1, 0);
   PS_CUDA_TRY(c, cudaMemcpyAsync(bn.data(), s.bnorm, nrhs * sizeof(double), cudaMemcpyDeviceToHost, st));
+  PS_CUDA_TRY(c, cudaMemcpyAsync(badrhs.data(), s.nonfinite, (nrhs + 1) * sizeof(int),
+                                 cudaMemcpyDeviceToHost, st));
   PS_CUDA_TRY(c, cudaStreamSynchronize(st));
+  for (int r = 0; r < nrhs; ++r)
+    if (badrhs[1 + r]) {
+      c->err = "ps_gmres: NaN/Inf in the right-hand side " + std::to_string(r) + " (SPEC.md:553)";
+      return PS_ERR_NUMERICAL;
+    }
   for (int r = 0; r < nrhs; ++r) {
     active[r] = bn[r] > 0.0;
     iters[r] = 0;

@@ -162,6 +162,7 @@ __device__ __forceinline__ void consume(const double2* __restrict__ sym,
     const double2 nxt = sp[(n + 1) * kTT];
     const double2 bb = bet[n];
     const double nby = -bb.y;
+#ifdef PS_K1_ONEPASS
 #pragma unroll
     for (int i = 0; i < BO; ++i) {
       const double2 tt = w[(R0 + u - i + MODB) % BO];
@@ -170,6 +171,22 @@ __device__ __forceinline__ void consume(const double2* __restrict__ sym,
       acc[i].y = fma(bb.x, tt.y, acc[i].y);
       acc[i].y = fma(bb.y, tt.x, acc[i].y);
     }
+#else
+    // two passes: the 2*BO FMAs of a pass are independent, so each
+    // accumulator's second FMA issues a full pass after its first
+#pragma unroll
+    for (int i = 0; i < BO; ++i) {
+      const double2 tt = w[(R0 + u - i + MODB) % BO];
+      acc[i].x = fma(bb.x, tt.x, acc[i].x);
+      acc[i].y = fma(bb.x, tt.y, acc[i].y);
+    }
+#pragma unroll
+    for (int i = 0; i < BO; ++i) {
+      const double2 tt = w[(R0 + u - i + MODB) % BO];
+      acc[i].x = fma(nby, tt.y, acc[i].x);
+      acc[i].y = fma(bb.y, tt.x, acc[i].y);
+    }
+#endif
     w[(R0 + u + 1 + MODB) % BO] = nxt;
   };
 #ifndef PS_K1_PARTIAL_UNROLL

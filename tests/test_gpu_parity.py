@@ -245,3 +245,60 @@ def test_solve_full_vs_golden(O, cfg):
     assert rel(sol.d[0], z["d"]) <= 1e-9
     assert abs(sol.flux[0]["error"] - float(z["flux_error"])) <= 1e-9
     assert abs(sol.iterations[0] - int(z["iterations"])) <= 1
+
+
+# ---------------------------------------------------------------- dense S (a4)
+@pytest.mark.parametrize("nrhs", [1, 3])
+def test_dense_rotated_smatrix(O, nrhs):
+    """Non-diagonal S with per-inclusion rotation phases: the
+    dense epilogue (1 RHS) and the K1m + dense epilogue path (3 RHS)."""
+    from paper_1412_7466_b200 import grating, solver
+    pb = O.load_problem(1)
+    rng = np.random.default_rng(77)
+    L = pb.L
+    S = np.diag(pb.smat) + 1e-3 * np.outer(pb.smat, np.ones(L)) * _cplx(rng, (L, L))
+    rot = rng.uniform(0, 2 * np.pi, pb.M)
+    names = ANGLES[:nrhs]
+    op = solver.SchurOperator([grating.load_fixture(n) for n in names], pb.centers, pb.p,
+                              smat=S, rot=rot)
+    v = _cplx(rng, (nrhs, pb.M, L))
+    got = op(_dev(v)).cpu().numpy()
+    rhs = op.rhs().cpu().numpy()
+    for r, n in enumerate(names):
+        pr = O.Problem(O.load_empty(n), pb.centers, pb.p, pb.radius, S, rot)
+        assert rel(got[r], O.apply_schur_operator(pr, v[r]).reshape(pb.M, L)) <= MATVEC_TOL
+        assert rel(rhs[r], O.schur_rhs(pr).reshape(pb.M, L)) <= MATVEC_TOL
+
+
+# ---------------------------------------------------------------- GMRES contract (a9)
+def test_gmres_nonconvergence_is_reported(O):
+    """hitting maxit is reported through the history, not raised."""
+    from paper_1412_7466_b200 import solver
+    pb, op = _operator(O, 2)
+    x, its, hist = solver.gmres(op, op.rhs(), 1e-14, 3)
+    assert its == [3] and hist[0][-1] > 1e-14
+    assert all(b <= a * (1 + 1e-12) for a, b in zip(hist[0], hist[0][1:]))
+
+
+def test_gmres_nan_raises(O):
+    """NaN/Inf in a Krylov vector -> numerical error."""
+    from paper_1412_7466_b200 import NumericalError, solver
+    pb, op = _operator(O, 1)
+    rhs = op.rhs().clone()
+    rhs[0, 3, 5] = float("nan")
+    with pytest.raises(NumericalError):
+        solver.gmres(op, rhs, 1e-10, 20)
+
+
+def test_gmres_identity_one_iteration(O):
+    """operator = identity (single inclusion, no images, no
+    coupling -> T = 0) converges in one iteration to x = rhs."""
+    from paper_1412_7466_b200 import grating, solver
+    pb = O.load_problem(1)
+    sysm = grating.load_fixture("w10")
+    sysm.config.near_field_copies = 0
+    op = solver.SchurOperator(sysm, pb.centers[:1], pb.p, smat=pb.smat, coupled=False)
+    b = torch.as_tensor(np.random.default_rng(2).standard_normal((1, 1, pb.L)) + 0j).cuda()
+    x, its, hist = solver.gmres(op, b, 1e-12, 10)
+    assert its == [1]
+    assert rel(x.cpu().numpy(), b.cpu().numpy()) < 1e-14
