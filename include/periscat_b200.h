@@ -89,6 +89,17 @@ int ps_set_pinv(ps_ctx* ctx, int irhs, int nrow, int ncol, const double* U_host,
                 const double* s_host, const double* Vh_host, const double* col_scale_host,
                 double eps, const double* f_host, int col_c, int col_d);
 
+/* Assemble the coupling blocks C (multiscat.multipole_to_targets_block,
+ * SPEC.md:494-502) and B_phys (source_to_local_block) as
+ * device matrices -- per RHS, Bloch weights folded in, C for the owned
+ * source range and B for the owned targets -- if they fit in max_gb; every
+ * later Schur matvec then streams them instead of regenerating the Graf
+ * symbols.  Otherwise (or after any geometry / phase / range change) the
+ * matrix-free kernels are used.  Call after ps_set_pinv. */
+int ps_precompute_coupling(ps_ctx* ctx, double max_gb);
+/* 1 if the pre-assembled coupling blocks are in use, 0 if matrix-free. */
+int ps_coupling_mode(const ps_ctx* ctx);
+
 /* ---- hot path (device pointers) ---------------------------------------- */
 
 /* a = T beta: all-pairs Graf M2L over the 2P+1 phased copies, self term

@@ -44,6 +44,8 @@ SIGNATURES = {
     "ps_dfma_peak": (_I, [_I, _DP, _DP]),
     "ps_dfma_sustained": (_I, [_I, _D, _DP]),
     "ps_profile": (_I, [_P, _I]),
+    "ps_precompute_coupling": (_I, [_P, _D]),
+    "ps_coupling_mode": (_I, [_P]),
     "ps_stats": (_I, [_P, ctypes.POINTER(ctypes.c_longlong), _DP, ctypes.POINTER(ctypes.c_longlong)]),
     "ps_stats_reset": (_I, [_P]),
 }

@@ -84,6 +84,7 @@ void ps_destroy(ps_ctx* h) {
     for (void* p : rp)
       if (p) cudaFree(p);
   }
+  ps::release_dense_coupling(c);
   ps::gmres_release(c);
   delete c;
 }
@@ -96,6 +97,7 @@ int ps_set_geometry(ps_ctx* h, int M, int p, int copies, double period, double k
                     const double* centers) {
   if (!h) return PS_ERR_ARG;
   Ctx* c = C(h);
+  ps::release_dense_coupling(c);   // geometry / phases changed
   if (M < 0 || p < 0 || copies < 0 || !(period > 0) || !(k2 > 0) || (M > 0 && !centers)) {
     c->err = "ps_set_geometry: bad argument";
     return PS_ERR_ARG;
@@ -137,6 +139,7 @@ int ps_set_geometry(ps_ctx* h, int M, int p, int copies, double period, double k
 int ps_set_target_range(ps_ctx* h, int t_begin, int t_end) {
   if (!h) return PS_ERR_ARG;
   Ctx* c = C(h);
+  ps::release_dense_coupling(c);   // geometry / phases changed
   if (t_begin < 0 || t_end < t_begin || t_end > c->M) {
     c->err = "ps_set_target_range: bad range";
     return PS_ERR_ARG;
@@ -149,6 +152,7 @@ int ps_set_target_range(ps_ctx* h, int t_begin, int t_end) {
 int ps_set_rhs_bloch(ps_ctx* h, int nrhs, const double* bloch) {
   if (!h) return PS_ERR_ARG;
   Ctx* c = C(h);
+  ps::release_dense_coupling(c);   // geometry / phases changed
   if (nrhs < 1 || !bloch) {
     c->err = "ps_set_rhs_bloch: bad argument";
     return PS_ERR_ARG;
@@ -191,6 +195,7 @@ int ps_set_layers(ps_ctx* h, int n1, const double* g1, int n2, const double* g2,
                   const double* w2, const double* x2, int Q, int nrb) {
   if (!h) return PS_ERR_ARG;
   Ctx* c = C(h);
+  ps::release_dense_coupling(c);   // geometry / phases changed
   if (n1 <= 0 || n2 <= 0 || nw <= 0 || Q < 0 || nrb <= 0 || !g1 || !g2 || !w2 || !x2) {
     c->err = "ps_set_layers: bad argument";
     return PS_ERR_ARG;
@@ -415,6 +420,19 @@ int ps_norm2(ps_ctx* h, int nrhs, int n, const void* w, double* nrm2, void* stre
   return ps::norm2(c, nrhs, n, reinterpret_cast<const double2*>(w), nrm2,
                    reinterpret_cast<cudaStream_t>(stream));
 }
+
+int ps_precompute_coupling(ps_ctx* h, double max_gb) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (c->p < 0 || !c->have_layers || !c->rhs[0].d_Uh) {
+    c->err = "ps_precompute_coupling: geometry / layers / pinv not set";
+    return PS_ERR_STATE;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::precompute_coupling(c, max_gb * 1e9);
+}
+
+int ps_coupling_mode(const ps_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->dense : -1; }
 
 int ps_profile(ps_ctx* h, int enable) {
   if (!h) return PS_ERR_ARG;

@@ -612,6 +612,11 @@ int apply_C(Ctx* c, const double2* beta, double2* g, int s0, int s1, cudaStream_
   for (int r = 0; r < c->nrhs; ++r) {
     Work w;
     if (int rc = work(c, r, &w)) return rc;
+    if (c->dense && s0 == c->dcs0 && s1 == c->dcs1) {
+      if (int rc = dense_apply_C(c, r, beta + r * in_stride, w.gpart, g + (size_t)r * c->nrow_c, st))
+        return rc;
+      continue;
+    }
     if (int rc = dispatch_c(c, beta + r * in_stride, bpow_of(c, r), w.gpart,
                             g + (size_t)r * c->nrow_c, s0, s1, st))
       return rc;
@@ -622,6 +627,7 @@ int apply_C(Ctx* c, const double2* beta, double2* g, int s0, int s1, cudaStream_
 // B_phys A^+ g for RHS r into w.bsub
 static int b_pinv(Ctx* c, int r, const double2* g, Work* w, cudaStream_t st) {
   if (int rc = pinv(c, r, g, w->x, c->ncol_b, st)) return rc;
+  if (c->dense) return dense_apply_B(c, r, w->x, w->bsub, st);
   return dispatch_b(c, w->x, bpow_of(c, r), w->bpart, w->bsub, st);
 }
 
@@ -698,8 +704,12 @@ int apply_schur(Ctx* c, const double2* v, double2* y, cudaStream_t st) {
   for (int r = 0; r < nrhs; ++r) {
     Work w;
     if (int rc = work(c, r, &w)) return rc;
-    if (int rc = dispatch_c(c, v + r * in_stride, bpow_of(c, r), w.gpart, w.g, 0, c->M, st))
+    if (c->dense && c->dcs0 == 0 && c->dcs1 == c->M) {
+      if (int rc = dense_apply_C(c, r, v + r * in_stride, w.gpart, w.g, st)) return rc;
+    } else if (int rc = dispatch_c(c, v + r * in_stride, bpow_of(c, r), w.gpart, w.g, 0, c->M,
+                                   st)) {
       return rc;
+    }
   }
   if (nrhs > 1) {
     for (int r = 0; r < nrhs; ++r) {

@@ -23,6 +23,9 @@ struct RhsData {          // per right-hand side (incidence angle)
   double2* d_Vb = nullptr;    // [ncol_b + 2*nrb][nsv] = conj(Vh)^T rows (B cols, c, d)
   double* d_cscale = nullptr; // [ncol_b + 2*nrb]
   double2* d_f = nullptr;     // [nrow_c] rhs f restricted to C rows
+  // pre-assembled coupling blocks (coupling_dense.cu), Bloch weights folded in
+  double2* d_CT = nullptr;    // [(dcs1-dcs0) L][nrow_c]
+  double2* d_B = nullptr;     // [Mt L][ncol_b]
 };
 
 struct Ctx {
@@ -53,6 +56,8 @@ struct Ctx {
   int ncol_b = 0;           // 2*n1 + 2*n2 + (2Q+1)
   int nrb = 0;              // Rayleigh-Bloch orders per direction (c, d)
   int nsv = 0;              // number of singular values
+  int dense = 0;            // 1: apply C and B from the pre-assembled matrices
+  int dcs0 = 0, dcs1 = 0;   // source range the stored C^T covers
 
   // right-hand sides
   int nrhs = 1;

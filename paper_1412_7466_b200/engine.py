@@ -133,6 +133,11 @@ class Engine:
                                          system.cols["c"].start, system.cols["d"].start))
         self.coupled = True
 
+    def precompute_coupling(self, max_gb: float = 40.0) -> bool:
+        """Pre-assemble C and B on the device if they fit max_gb (see header)."""
+        self._check(self.lib.ps_precompute_coupling(self.ctx, float(max_gb)))
+        return self.lib.ps_coupling_mode(self.ctx) == 1
+
     # ---------------------------------------------------------------- apply
     def _dev(self, x, shape):
         if not isinstance(x, torch.Tensor) or x.device != self.device or x.dtype != torch.complex128 \

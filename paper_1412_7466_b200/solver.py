@@ -21,7 +21,7 @@ from .scatmat import disk_scattering_matrix
 class SchurOperator:
     def __init__(self, systems, centers, p: int, smat=None, radius: float | None = None,
                  rot=None, device=None, target_range=None, coupled: bool = True,
-                 engine: Engine | None = None):
+                 engine: Engine | None = None, dense_gb: float = 40.0):
         if not isinstance(systems, (list, tuple)):
             systems = [systems]
         self.systems = list(systems)
@@ -49,6 +49,8 @@ class SchurOperator:
                 eng.set_pinv(r, s)
         if target_range is not None:
             eng.set_target_range(*target_range)
+        # pre-assembled B / C blocks when they fit (else matrix-free K3/K5)
+        self.dense = bool(coupled and dense_gb > 0 and eng.precompute_coupling(dense_gb))
         self.M, self.p, self.L, self.nrhs = eng.M, p, eng.L, eng.nrhs
         self.device = eng.device
 

@@ -54,7 +54,7 @@ def test_sharded_driver_nccl_world1():
         pb = O.load_problem(2)
         z = np.load(os.path.join(O.GOLDEN, "golden_cfg2.npz"))
         op = solver.SchurOperator(grating.load_fixture("w10"), pb.centers, pb.p, smat=pb.smat,
-                                  target_range=parallel.shard_range(pb.M, 0, 1))
+                                  target_range=parallel.shard_range(pb.M, 0, 1), dense_gb=0.0)
         sh = parallel.ShardedSchur(op)
         x, its, hist = parallel.gmres_dist(sh, sh.rhs(), 1e-10, 150, engine=op.eng)
         xe = sh.recover(x.contiguous())

@@ -89,17 +89,21 @@ def test_domain_error_coincident():
         multiscat.apply_T(np.ones((2, 3), complex), c, 5.0, 1)
 
 
-def _operator(O, cfg, coupled=True):
+def _operator(O, cfg, coupled=True, dense_gb=40.0):
     from paper_1412_7466_b200 import grating, solver
     pb = O.load_problem(cfg)
     sysm = grating.load_fixture(O.CONFIGS[cfg]["empty"])
-    op = solver.SchurOperator(sysm, pb.centers, pb.p, smat=pb.smat, coupled=coupled)
+    op = solver.SchurOperator(sysm, pb.centers, pb.p, smat=pb.smat, coupled=coupled,
+                              dense_gb=dense_gb)
     return pb, op
 
 
+@pytest.mark.parametrize("dense_gb", [40.0, 0.0])
 @pytest.mark.parametrize("cfg", [1, 2])
-def test_apply_C_matches_oracle(O, cfg):
-    pb, op = _operator(O, cfg)
+def test_apply_C_matches_oracle(O, cfg, dense_gb):
+    """Pre-assembled C (dense_gb > 0) and matrix-free K3 (dense_gb = 0)."""
+    pb, op = _operator(O, cfg, dense_gb=dense_gb)
+    assert op.dense == (dense_gb > 0)
     rng = np.random.default_rng(20 + cfg)
     beta = _cplx(rng, (pb.M, pb.L))
     ref = O.apply_C(pb.es, beta, pb.centers)[:576]
@@ -107,9 +111,10 @@ def test_apply_C_matches_oracle(O, cfg):
     assert rel(got, ref) <= MATVEC_TOL
 
 
+@pytest.mark.parametrize("dense_gb", [40.0, 0.0])
 @pytest.mark.parametrize("cfg", [1, 2])
-def test_schur_matches_oracle(O, cfg):
-    pb, op = _operator(O, cfg)
+def test_schur_matches_oracle(O, cfg, dense_gb):
+    pb, op = _operator(O, cfg, dense_gb=dense_gb)
     rng = np.random.default_rng(30 + cfg)
     for v in (_cplx(rng, (pb.M, pb.L)), pb.smat[None, :] * _cplx(rng, (pb.M, pb.L))):
         ref = O.apply_schur_operator(pb, v).reshape(pb.M, pb.L)
@@ -117,9 +122,10 @@ def test_schur_matches_oracle(O, cfg):
         assert rel(got, ref) <= MATVEC_TOL
 
 
+@pytest.mark.parametrize("dense_gb", [40.0, 0.0])
 @pytest.mark.parametrize("cfg", [1, 2])
-def test_schur_rhs_matches_oracle(O, cfg):
-    pb, op = _operator(O, cfg)
+def test_schur_rhs_matches_oracle(O, cfg, dense_gb):
+    pb, op = _operator(O, cfg, dense_gb=dense_gb)
     ref = O.schur_rhs(pb).reshape(pb.M, pb.L)
     got = op.rhs().cpu().numpy()[0]
     assert rel(got, ref) <= MATVEC_TOL
@@ -178,12 +184,13 @@ def test_apply_T_mrhs_shapes(O, nrhs, p, M):
 ANGLES = ["w10", "w10_a00", "w10_a15"]
 
 
-def test_schur_multi_rhs_matches_oracle(O):
+@pytest.mark.parametrize("dense_gb", [40.0, 0.0])
+def test_schur_multi_rhs_matches_oracle(O, dense_gb):
     """Three incidence angles (own Bloch phase, SVD factors, f) in one batch."""
     from paper_1412_7466_b200 import grating, solver
     pb = O.load_problem(1)
     systems = [grating.load_fixture(n) for n in ANGLES]
-    op = solver.SchurOperator(systems, pb.centers, pb.p, smat=pb.smat)
+    op = solver.SchurOperator(systems, pb.centers, pb.p, smat=pb.smat, dense_gb=dense_gb)
     rng = np.random.default_rng(33)
     v = pb.smat[None, None, :] * _cplx(rng, (3, pb.M, pb.L))
     got = op(_dev(v)).cpu().numpy()
@@ -219,11 +226,12 @@ def _golden(cfg):
     return np.load(path)
 
 
+@pytest.mark.parametrize("dense_gb", [40.0, 0.0])
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4])
-def test_matvec_vs_golden(O, cfg):
+def test_matvec_vs_golden(O, cfg, dense_gb):
     """apply_T and the Schur operator against the committed oracle goldens."""
     z = _golden(cfg)
-    pb, op = _operator(O, cfg)
+    pb, op = _operator(O, cfg, dense_gb=dense_gb)
     v = torch.as_tensor(z["v"][None]).cuda()
     tids = z["targets"]
     aT = op.apply_T(v).cpu().numpy()[0][tids]
