@@ -46,6 +46,7 @@ def _config_block(cfg_id, M, p, nrhs, world):
                         "theta_ref=-7pi/10, P=1 near-field copies",
             "M": M, "p": p, "nrhs": nrhs, "translations_per_step": M * (3 * M - 1) * nrhs,
             "parallelism": f"target-sharded x{world}",
+            "coupling": "pre-assembled C^T / B_phys (device GEMVs)",
             "l2": "flushed (256 MiB write) before every timed step"}
 
 
@@ -177,7 +178,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1412_7466_b200 import _lib, grating, solver
+    from paper_1412_7466_b200 import _lib, grating, parallel, solver
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -203,30 +204,17 @@ def run_ours(args):
     v_full = torch.as_tensor(v_host).to(dev).contiguous()
     v_own = v_full[:, t0:t1].contiguous()
     y = eng.empty_own()
-    g = torch.empty((1, eng.nrow_c), dtype=torch.complex128, device=dev)
-    gather = [torch.empty_like(v_own) for _ in range(world)] if world > 1 else None
-    s_rng = (t0, t1)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    # one Schur matvec: N=1 -> the operator on the resident full vector;
+    # N>1 -> parallel.ShardedSchur (NCCL all-gather of beta, C partial over own
+    # sources + all-reduce, own-target T/B/S) -- the path gmres_dist drives
+    sharded = parallel.ShardedSchur(op) if world > 1 else None
 
     def step():
         if world == 1:
             op(v_full, out=y)
-            return
-        # all-gather the coefficient vector, C partial over own sources, reduce
-        sizes_equal = all((M * (r + 1)) // world - (M * r) // world == t1 - t0 for r in range(world))
-        if sizes_equal:
-            buf = torch.empty((world,) + tuple(v_own.shape), dtype=v_own.dtype, device=dev)
-            dist.all_gather_into_tensor(buf, v_own)
-            vf = buf.permute(1, 0, 2, 3).reshape(1, M, L)
         else:
-            parts = [torch.empty((1, (M * (r + 1)) // world - (M * r) // world, L),
-                                 dtype=v_own.dtype, device=dev) for r in range(world)]
-            dist.all_gather(parts, v_own)
-            vf = torch.cat(parts, dim=1)
-        vf = vf.contiguous()
-        eng.apply_C(vf, s_range=s_rng, out=g)
-        dist.all_reduce(g)
-        op(vf, out=y, g=g)
+            sharded(v_own, out=y)
 
     for _ in range(args.warmup):
         step()
@@ -276,7 +264,7 @@ def run_ours(args):
 
     # e2e through the public API with pinned host buffers (N=1: full call;
     # N>1: every rank's call, max over ranks)
-    vh = torch.as_tensor(v_host).pin_memory()
+    vh = torch.as_tensor(v_host if world == 1 else v_host[:, t0:t1]).contiguous().pin_memory()
     yh = torch.empty((1, t1 - t0, L), dtype=torch.complex128).pin_memory()
 
     def e2e_step():
@@ -284,9 +272,7 @@ def run_ours(args):
         if world == 1:
             op(vd, out=y)
         else:
-            eng.apply_C(vd, s_range=s_rng, out=g)
-            dist.all_reduce(g)
-            op(vd, out=y, g=g)
+            sharded(vd, out=y)
         yh.copy_(y, non_blocking=True)
 
     for _ in range(max(args.warmup, 1)):
@@ -347,7 +333,7 @@ def run_ours(args):
                                             "(MEASURED_PEAKS.json has no FP64 entry)"},
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT,
-                        "h2d_bytes_per_step": int(v_host.nbytes),
+                        "h2d_bytes_per_step": int(vh.numel() * 16),
                         "d2h_bytes_per_step": int(yh.numel() * 16)},
                 "gpu_launches": int(stats["launches"]),
                 "clocks": clk.summary(),
