@@ -97,6 +97,10 @@ int ps_set_pinv(ps_ctx* ctx, int irhs, int nrow, int ncol, const double* U_host,
  * symbols.  Otherwise (or after any geometry / phase / range change) the
  * matrix-free kernels are used.  Call after ps_set_pinv. */
 int ps_precompute_coupling(ps_ctx* ctx, double max_gb);
+/* Single-RHS M2L kernel choice: 0 auto (symmetric K1s -- each Graf symbol
+ * row serves the pair and its reverse -- when this context owns every
+ * target, else tiled K1), 1 force tiled K1, 2 force K1s (full range only). */
+int ps_set_k1_variant(ps_ctx* ctx, int variant);
 /* 1 if the pre-assembled coupling blocks are in use, 0 if matrix-free. */
 int ps_coupling_mode(const ps_ctx* ctx);
 

@@ -292,7 +292,7 @@ int ps_apply_T(ps_ctx* h, const void* beta, void* out, void* stream) {
                               reinterpret_cast<double2*>(out), 0, nullptr, 0, st);
   const size_t in_stride = (size_t)c->M * c->L, out_stride = (size_t)(c->t_end - c->t_begin) * c->L;
   for (int r = 0; r < c->nrhs; ++r) {
-    int rc = ps::m2l_apply(c, reinterpret_cast<const double2*>(beta) + r * in_stride,
+    int rc = ps::m2l_apply_1(c, reinterpret_cast<const double2*>(beta) + r * in_stride,
                            c->d_blochpow + (size_t)r * np + 1,
                            reinterpret_cast<double2*>(out) + r * out_stride, 0, nullptr, nullptr,
                            st);
@@ -430,6 +430,17 @@ int ps_precompute_coupling(ps_ctx* h, double max_gb) {
   }
   if (int rc = set_device(c)) return rc;
   return ps::precompute_coupling(c, max_gb * 1e9);
+}
+
+int ps_set_k1_variant(ps_ctx* h, int variant) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (variant < 0 || variant > 2) {
+    c->err = "ps_set_k1_variant: 0 auto, 1 tiled, 2 symmetric";
+    return PS_ERR_ARG;
+  }
+  c->k1_variant = variant;
+  return PS_OK;
 }
 
 int ps_coupling_mode(const ps_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->dense : -1; }

@@ -685,10 +685,10 @@ int apply_schur_g(Ctx* c, const double2* v, const double2* g, double2* y, cudaSt
     const double2* vr = v + r * in_stride;
     const double2* v_own = vr + (size_t)c->t_begin * c->L;
     if (c->s_diag) {
-      if (int rc = m2l_apply(c, vr, bpow_of(c, r) + 1, y + r * out_stride, 1, v_own, bsub, st))
+      if (int rc = m2l_apply_1(c, vr, bpow_of(c, r) + 1, y + r * out_stride, 1, v_own, bsub, st))
         return rc;
     } else {
-      if (int rc = m2l_apply(c, vr, bpow_of(c, r) + 1, w.u, 2, v_own, bsub, st)) return rc;
+      if (int rc = m2l_apply_1(c, vr, bpow_of(c, r) + 1, w.u, 2, v_own, bsub, st)) return rc;
       if (int rc = s_apply(c, v_own, w.u, y + r * out_stride, st)) return rc;
     }
   }
@@ -726,10 +726,10 @@ int apply_schur(Ctx* c, const double2* v, double2* y, cudaStream_t st) {
     const double2* vr = v + r * in_stride;
     const double2* v_own = vr + (size_t)c->t_begin * c->L;
     if (c->s_diag) {
-      if (int rc = m2l_apply(c, vr, bpow_of(c, r) + 1, y + r * out_stride, 1, v_own, w.bsub, st))
+      if (int rc = m2l_apply_1(c, vr, bpow_of(c, r) + 1, y + r * out_stride, 1, v_own, w.bsub, st))
         return rc;
     } else {
-      if (int rc = m2l_apply(c, vr, bpow_of(c, r) + 1, w.u, 2, v_own, w.bsub, st)) return rc;
+      if (int rc = m2l_apply_1(c, vr, bpow_of(c, r) + 1, w.u, 2, v_own, w.bsub, st)) return rc;
       if (int rc = s_apply(c, v_own, w.u, y + r * out_stride, st)) return rc;
     }
   }

@@ -386,6 +386,14 @@ int launch_p(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
 
 int m2l_max_order() { return PS_M2L_MAX_P; }
 
+int m2l_apply_1(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
+                const double2* v_own, const double2* bsub, cudaStream_t st) {
+  const bool full = ctx->t_begin == 0 && ctx->t_end == ctx->M;
+  const bool sym = ctx->k1_variant == 2 || (ctx->k1_variant == 0 && full && ctx->M >= 64);
+  if (sym && full) return m2l_apply_sym(ctx, beta, bpow, out, mode, v_own, bsub, st);
+  return m2l_apply(ctx, beta, bpow, out, mode, v_own, bsub, st);
+}
+
 int m2l_apply(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
               const double2* v_own, const double2* bsub, cudaStream_t st) {
   switch (ctx->p) {

@@ -16,6 +16,13 @@ int m2l_apply(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, 
               const double2* v_own, const double2* bsub, cudaStream_t st);
 // All ctx->nrhs right-hand sides at once (m2l_mrhs.cu).  beta [nrhs][M][L],
 // out [nrhs][nt][L]; bsub (mode 1/2) for RHS r at bsub + r * b_stride.
+// One RHS, full target range: symmetric variant (m2l_sym.cu), same contract
+// as m2l_apply.
+int m2l_apply_sym(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
+                  const double2* v_own, const double2* bsub, cudaStream_t st);
+// dispatch: K1s when ctx owns every target and k1_variant allows it, else K1
+int m2l_apply_1(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
+                const double2* v_own, const double2* bsub, cudaStream_t st);
 int m2l_apply_mrhs(Ctx* ctx, const double2* beta, double2* out, int mode, const double2* bsub,
                    long long b_stride, cudaStream_t st);
 }  // namespace ps

@@ -1,0 +1,457 @@
+// K1s: symmetric all-pairs M2L for one RHS when the rank owns every target
+// (multiscat.apply_T).  The symbol row of the pair
+// (m, j, l), t_nu = H_nu(k rho) e^{i nu phi} of x_m - x_j - l d e_x, also
+// serves the reverse pair (j, m, -l): its displacement is the negative, so
+// t'_nu = (-1)^nu t_nu.  With
+//   a_j[m'] += sum_n beta'[n] t'_{n-m'} = (-1)^m' sum_n ((-1)^n beta'[n]) t_{n-m'}
+// the reverse apply is the forward Toeplitz sweep over the SAME shared-memory
+// row with sign-flipped coefficients and a sign on the output row.  Each
+// symbol row therefore feeds two L x L applies and the producer FP64 work per
+// translation halves (the single-RHS K1 spends ~14% of the pipe on symbols).
+//
+// Work: unordered target-tile pairs (A <= B) of 8 inclusions, row-major
+// (A, A), (A, A+1), ...; a block is 2P+1 batches (one per copy l) of the 64
+// rows (m in A, j in B).  Consumer warp w owns target A*8+w (forward) and
+// B*8+w (reverse); its lane (b, s) covers row block b against source slot s
+// of the batch, so per batch each warp sweeps 8 sources forward and, for
+// A < B, 8 sources in reverse, and the source sums are 3-level shuffle trees
+// (no shared-memory reduction, no consumer barrier).  Forward accumulators
+// live for a whole block row; reverse parts are flushed per block.  Diagonal
+// blocks (A = B) run forward only.  k1s_reduce sums the parts in a fixed
+// order (deterministic) and applies the Schur epilogue.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "ctx.cuh"
+#include "m2l.cuh"
+#include "symbols.cuh"
+
+namespace ps {
+
+namespace {
+
+template <int V>
+struct IC {
+  static constexpr int value = V;
+};
+template <int N, typename F, int I = 0>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(IC<I>{});
+    static_for<N, F, I + 1>(static_cast<F&&>(f));
+  }
+}
+
+constexpr int kTT = 8;                 // inclusions per tile
+constexpr int kNB = 4;                 // row blocks per target
+constexpr int kCW = 8;                 // consumer warps (= tile width)
+constexpr int kPW = 4;                 // producer warps
+constexpr int kThreads = (kCW + kPW) * 32;
+#ifndef PS_K1S_CREGS
+#define PS_K1S_CREGS 216
+#endif
+constexpr int kConsumerRegs = PS_K1S_CREGS;
+constexpr int kProducerRegs = 504 - 2 * PS_K1S_CREGS;   // 3 warps x 168 per sub-partition
+static_assert(kProducerRegs >= 24 && kProducerRegs % 8 == 0, "setmaxnreg range");
+static_assert(2 * kTT * kTT == kPW * 32, "64 rows: two producer lanes per row");
+
+template <int P>
+struct ShapeS {
+  static constexpr int L = 2 * P + 1;
+  static constexpr int NS = 4 * P + 1;
+  static constexpr int BO = (L + kNB - 1) / kNB;
+  static constexpr int ROWS = BO * kNB;
+  static constexpr int FP = ROWS - L;
+  static constexpr int NSP = FP + NS + 1;
+  static constexpr int SJ = kTT * NSP + 1;        // odd: both access patterns conflict-free
+  static constexpr int SYM = kTT * SJ;            // double2 per buffer
+  static constexpr size_t SMEM = 2 * (size_t)SYM * sizeof(double2);
+};
+
+struct ArgsS {
+  const double* centers;   // [M][2]
+  const double2* bw;       // [M * ncp][L] bloch-weighted beta per source image
+  double2* apart;          // [G][maxseg][kTT][L]  forward parts, one per (CTA, block row)
+  double2* bpart;          // [NB][kTT][L]         reverse parts, one per cross block
+  int M, T, NB, copies, ncp, maxseg;
+  double period, k2;
+};
+
+__device__ __forceinline__ long long tri_off(int a, int T) {   // blocks with first tile < a
+  return (long long)a * T - (long long)a * (a - 1) / 2;
+}
+
+__device__ __forceinline__ void block_ab(long long k, int T, int& A, int& B) {
+  int a = 0;
+  // small T: linear scan from a floating estimate
+  double disc = (2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * (double)k;
+  a = (int)(((2.0 * T + 1.0) - sqrt(disc > 0 ? disc : 0)) * 0.5);
+  if (a < 0) a = 0;
+  if (a > T - 1) a = T - 1;
+  while (a > 0 && tri_off(a, T) > k) --a;
+  while (a < T - 1 && tri_off(a + 1, T) <= k) ++a;
+  A = a;
+  B = a + (int)(k - tri_off(a, T));
+}
+
+template <int P>
+__device__ __forceinline__ void produce_s(const ArgsS& a, int A, int B, int li, double2* sym,
+                                          int pw, int lane) {
+  using S = ShapeS<P>;
+  const int row = pw * 16 + (lane >> 1);       // 64 rows over 4 warps x 16 lane pairs
+  const bool mirror = lane & 1;
+  const int mt = row & 7, jt = row >> 3;       // target slot in A, source slot in B
+  const int m = A * kTT + mt, j = B * kTT + jt;
+  const int l = li - a.copies;
+  bool live = (m < a.M) && (j < a.M) && !(l == 0 && m == j);
+  double dx = 1.0, dy = 0.0;
+  if (live) {
+    const double2 cm = reinterpret_cast<const double2*>(a.centers)[m];
+    const double2 cj = reinterpret_cast<const double2*>(a.centers)[j];
+    dx = cm.x - cj.x - (double)l * a.period;
+    dy = cm.y - cj.y;
+  }
+  const double rho = live ? hypot(dx, dy) : 1.0;
+  const double z = a.k2 * rho;
+  int N = live ? miller_start_j01(z) : 2;
+  N = __reduce_max_sync(0xffffffffu, N);
+  const double inv = live ? 1.0 / rho : 0.0;
+  // row (m, j) at  j * SJ + slot * 8 + m
+  double2* base = sym + (size_t)jt * S::SJ + (S::FP + 2 * P) * kTT + mt;
+  hankel_symbols_half<2 * P>(z, dx * inv, dy * inv, N, mirror, [&](int nu, double re, double im) {
+    if (nu == 0 && !live) re = im = 0.0;
+    base[nu * kTT] = make_double2(re, im);
+  });
+}
+
+// one Toeplitz sweep: rows at sp0 + slot*kTT (slot of nu = n - r), coefficients
+// from global (sign-flipped on odd n for the reverse apply)
+template <int P, bool REV>
+__device__ __forceinline__ void consume_s(const double2* __restrict__ rowbase,
+                                          const double2* __restrict__ bsrc,
+                                          double2 (&acc)[ShapeS<P>::BO], int b) {
+  using S = ShapeS<P>;
+  constexpr int BO = S::BO;
+  constexpr int R0 = S::FP + 2 * P;
+  constexpr int MODB = 64 * BO;
+  const double2* sp = rowbase + (size_t)(R0 - b * BO) * kTT;
+  double2 w[BO];
+#pragma unroll
+  for (int i = 0; i < BO; ++i) w[(R0 - i + MODB) % BO] = sp[-i * kTT];
+  auto step = [&](auto n_c) {
+    constexpr int n = decltype(n_c)::value;
+    constexpr int u = n % BO;
+    const double2 nxt = sp[(n + 1) * kTT];
+    double2 bb = __ldg(bsrc + n);
+    if (REV && ((n - P) & 1)) bb = make_double2(-bb.x, -bb.y);   // (-1)^{order n}
+#pragma unroll
+    for (int i = 0; i < BO; ++i) {
+      const double2 tt = w[(R0 + u - i + MODB) % BO];
+      acc[i].x = fma(bb.x, tt.x, acc[i].x);
+      acc[i].y = fma(bb.x, tt.y, acc[i].y);
+    }
+#pragma unroll
+    for (int i = 0; i < BO; ++i) {
+      const double2 tt = w[(R0 + u - i + MODB) % BO];
+      acc[i].x = fma(-bb.y, tt.y, acc[i].x);
+      acc[i].y = fma(bb.y, tt.x, acc[i].y);
+    }
+    w[(R0 + u + 1 + MODB) % BO] = nxt;
+  };
+  static_for<S::L>(step);
+}
+
+// Sum one accumulator set over the 8 source lanes s (lane = b*8 + s) with a
+// fixed xor tree, then lane s = 0 writes the rows of its block b.
+// sign_rows: multiply row m' by (-1)^{m'} (reverse parts).
+template <int P>
+__device__ __forceinline__ void flush_s(double2 (&acc)[ShapeS<P>::BO], double2* dst, int b, int s,
+                                       bool sign_rows) {
+  using S = ShapeS<P>;
+  constexpr int BO = S::BO;
+#pragma unroll
+  for (int i = 0; i < BO; ++i) {
+#pragma unroll
+    for (int o = 1; o < kTT; o <<= 1) {
+      acc[i].x += __shfl_xor_sync(0xffffffffu, acc[i].x, o);
+      acc[i].y += __shfl_xor_sync(0xffffffffu, acc[i].y, o);
+    }
+  }
+  if (s == 0) {
+#pragma unroll
+    for (int i = 0; i < BO; ++i) {
+      const int r = b * BO + i;
+      if (r < S::L) {
+        double2 v = acc[i];
+        if (sign_rows && ((r - P) & 1)) v = make_double2(-v.x, -v.y);
+        dst[r] = v;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < BO; ++i) acc[i] = make_double2(0.0, 0.0);
+}
+
+template <int P>
+__global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
+  using S = ShapeS<P>;
+  constexpr int BO = S::BO, L = S::L;
+  extern __shared__ double2 smem[];
+  double2* sym0 = smem;
+  double2* sym1 = smem + S::SYM;
+  const long long k0 = ((long long)a.NB * blockIdx.x) / gridDim.x;
+  const long long k1 = ((long long)a.NB * (blockIdx.x + 1)) / gridDim.x;
+  if (k0 >= k1) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp >= kCW;
+  const int nbat = (int)(k1 - k0) * a.ncp;      // batches of this CTA
+
+  // zero the pad slots (front FP slots, tail slot) of both buffers once
+  for (int idx = threadIdx.x; idx < 2 * kTT * kTT * (S::FP + 1); idx += kThreads) {
+    const int buf = idx / (kTT * kTT * (S::FP + 1));
+    const int r = idx % (kTT * kTT * (S::FP + 1));
+    const int jt = r / (kTT * (S::FP + 1));
+    const int r2 = r % (kTT * (S::FP + 1));
+    const int q = r2 / kTT, mt = r2 % kTT;
+    const int slot = q < S::FP ? q : S::FP + S::NS;
+    (buf ? sym1 : sym0)[(size_t)jt * S::SJ + (size_t)slot * kTT + mt] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+
+  if (producer) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
+    const int pw = warp - kCW;
+    int A, B;
+    block_ab(k0, a.T, A, B);
+    int li = 0;
+    produce_s<P>(a, A, B, li, sym0, pw, lane);
+    __syncthreads();
+    for (int it = 0; it < nbat; ++it) {
+      // advance to the batch it + 1
+      if (++li == a.ncp) {
+        li = 0;
+        if (++B == a.T) {
+          ++A;
+          B = A;
+        }
+      }
+      if (it + 1 < nbat) produce_s<P>(a, A, B, li, (it & 1) ? sym0 : sym1, pw, lane);
+      __syncthreads();
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
+  __syncthreads();
+
+  // warp w owns target A*8+w (forward, accA) and B*8+w (reverse, accB);
+  // lane (b, s) covers rows [b*BO, b*BO+BO) and source slot s of the batch
+  const int b = lane / kTT, s = lane % kTT;
+  double2 accA[BO], accB[BO];
+#pragma unroll
+  for (int i = 0; i < BO; ++i) accA[i] = accB[i] = make_double2(0.0, 0.0);
+  int A, B;
+  block_ab(k0, a.T, A, B);
+  const int A0 = A;
+  long long blk = k0;
+  int li = 0;
+  for (int it = 0; it < nbat; ++it) {
+    double2* symc = (it & 1) ? sym1 : sym0;
+    const int l = li - a.copies;
+    // forward: target m = A*8 + w, source image (j = B*8 + s, l): row (m=w, j=s)
+    {
+      const int j = min(B * kTT + s, a.M - 1);            // dead rows are zero
+      consume_s<P, false>(symc + (size_t)s * S::SJ + warp,
+                          a.bw + ((size_t)j * a.ncp + li) * L, accA, b);
+    }
+    // reverse: target j = B*8 + w, source image (m = A*8 + s, -l): row (m=s, j=w)
+    if (A != B) {
+      const int m = min(A * kTT + s, a.M - 1);
+      consume_s<P, true>(symc + (size_t)warp * S::SJ + s,
+                         a.bw + ((size_t)m * a.ncp + (a.copies - l)) * L, accB, b);
+    }
+    if (li == a.ncp - 1) {                     // block complete
+      if (A != B) flush_s<P>(accB, a.bpart + ((size_t)blk * kTT + warp) * L, b, s, true);
+      ++blk;
+      li = 0;
+      const int Aold = A;
+      if (++B == a.T) {
+        ++A;
+        B = A;
+      }
+      if (A != Aold || it + 1 == nbat)         // block row finished (or CTA done)
+        flush_s<P>(accA,
+                   a.apart + (((size_t)blockIdx.x * a.maxseg + (Aold - A0)) * kTT + warp) * L, b,
+                   s, false);
+    } else {
+      ++li;
+    }
+    __syncthreads();
+  }
+}
+
+// bw[g][n] = bloch^{l(g)} beta[j(g)][n]
+__global__ void bloch_weight_1(const double2* __restrict__ beta, const double2* __restrict__ bpow,
+                               int M, int L, int ncp, double2* __restrict__ bw) {
+  const long long total = (long long)M * ncp * L;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int n = (int)(i % L);
+    const long long g = i / L;
+    const int j = (int)(g / ncp), li = (int)(g % ncp);
+    const double2 bv = beta[(long long)j * L + n];
+    const double2 wv = bpow[1 + li];
+    bw[i] = make_double2(fma(bv.x, wv.x, -bv.y * wv.y), fma(bv.x, wv.y, bv.y * wv.x));
+  }
+}
+
+// out[m][r] for tile X = m / 8, fixed order: reverse parts of the cross
+// blocks (A, X), A < X, then the forward parts of the CTAs covering block row X.
+__global__ void k1s_reduce(const double2* __restrict__ apart, const double2* __restrict__ bpart,
+                           int T, int NB, int G, int maxseg, int M, int L, int mode,
+                           const double2* __restrict__ v_own, const double2* __restrict__ sdiag,
+                           const double2* __restrict__ bsub, double2* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= M * L) return;
+  const int m = idx / L, r = idx % L;
+  const int X = m / kTT, w = m % kTT;
+  auto off = [&](int a) -> long long { return (long long)a * T - (long long)a * (a - 1) / 2; };
+  auto kbeg = [&](int c) -> long long { return ((long long)NB * c) / G; };
+  double2 sum = make_double2(0.0, 0.0);
+  for (int A = 0; A < X; ++A) {
+    const long long k = off(A) + (X - A);
+    const double2 v = bpart[((size_t)k * kTT + w) * L + r];
+    sum.x += v.x;
+    sum.y += v.y;
+  }
+  const long long ra = off(X), rb = off(X + 1);          // block range of row X
+  int c = (int)((ra * G) / NB);
+  if (c >= G) c = G - 1;
+  while (c > 0 && kbeg(c) > ra) --c;
+  while (c < G - 1 && kbeg(c + 1) <= ra) ++c;
+  for (; c < G; ++c) {
+    const long long c0 = kbeg(c), c1 = kbeg(c + 1);
+    if (c0 >= rb) break;
+    if (c1 <= c0 || c1 <= ra) continue;
+    // first block row of CTA c
+    int a0 = (int)(((2.0 * T + 1.0) - sqrt((2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * (double)c0)) * 0.5);
+    if (a0 < 0) a0 = 0;
+    if (a0 > T - 1) a0 = T - 1;
+    while (a0 > 0 && off(a0) > c0) --a0;
+    while (a0 < T - 1 && off(a0 + 1) <= c0) ++a0;
+    const double2 v = apart[(((size_t)c * maxseg + (X - a0)) * kTT + w) * L + r];
+    sum.x += v.x;
+    sum.y += v.y;
+  }
+  if (mode == 0) {
+    out[idx] = sum;
+    return;
+  }
+  if (bsub) {
+    sum.x -= bsub[idx].x;
+    sum.y -= bsub[idx].y;
+  }
+  if (mode == 2) {
+    out[idx] = sum;
+    return;
+  }
+  const double2 sd = sdiag[r];
+  const double2 vv = v_own[idx];
+  out[idx] = make_double2(vv.x - fma(sd.x, sum.x, -sd.y * sum.y), vv.y - fma(sd.x, sum.y, sd.y * sum.x));
+}
+
+// number of block rows a CTA's range touches (host, exact)
+int max_rows_per_cta(int T, int NB, int G) {
+  auto off = [&](long long a) { return a * T - a * (a - 1) / 2; };
+  auto row_of = [&](long long k) {
+    long long a = 0;
+    while (a < T - 1 && off(a + 1) <= k) ++a;
+    return a;
+  };
+  int mx = 1;
+  for (int c = 0; c < G; ++c) {
+    const long long k0 = ((long long)NB * c) / G, k1 = ((long long)NB * (c + 1)) / G;
+    if (k1 <= k0) continue;
+    mx = std::max(mx, (int)(row_of(k1 - 1) - row_of(k0) + 1));
+  }
+  return mx;
+}
+
+template <int P>
+int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
+             const double2* v_own, const double2* bsub, cudaStream_t st) {
+  using S = ShapeS<P>;
+  ArgsS a;
+  a.centers = ctx->d_centers;
+  a.M = ctx->M;
+  a.T = (ctx->M + kTT - 1) / kTT;
+  a.NB = a.T * (a.T + 1) / 2;
+  a.copies = ctx->copies;
+  a.ncp = 2 * ctx->copies + 1;
+  a.period = ctx->period;
+  a.k2 = ctx->k2;
+  int G = ctx->sm_count;
+  if (G > a.NB) G = a.NB;
+  a.maxseg = max_rows_per_cta(a.T, a.NB, G);
+  const size_t na = (size_t)G * a.maxseg * kTT * S::L;
+  const size_t nbp = (size_t)a.NB * kTT * S::L;
+  const size_t npart = na + nbp;
+  const size_t nbw = (size_t)ctx->M * a.ncp * S::L;
+  if (ctx->partial_elems < npart + nbw) {
+    if (ctx->d_partial) cudaFree(ctx->d_partial);
+    ctx->d_partial = nullptr;
+    ctx->partial_elems = 0;
+    PS_CUDA_TRY(ctx, cudaMalloc(&ctx->d_partial, (npart + nbw) * sizeof(double2)));
+    ctx->partial_elems = npart + nbw;
+  }
+  a.apart = ctx->d_partial;
+  a.bpart = ctx->d_partial + na;
+  double2* bw = ctx->d_partial + npart;
+  a.bw = bw;
+  bloch_weight_1<<<2 * ctx->sm_count, 256, 0, st>>>(beta, bpow - 1, ctx->M, S::L, a.ncp, bw);
+  PS_CUDA_TRY(ctx, cudaGetLastError());
+  static bool attr_done = false;
+  if (!attr_done) {
+    PS_CUDA_TRY(ctx, cudaFuncSetAttribute(m2l_sym_kernel<P>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+    attr_done = true;
+  }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->profile) {
+    PS_CUDA_TRY(ctx, cudaEventCreate(&e0));
+    PS_CUDA_TRY(ctx, cudaEventCreate(&e1));
+    PS_CUDA_TRY(ctx, cudaEventRecord(e0, st));
+  }
+  m2l_sym_kernel<P><<<G, kThreads, S::SMEM, st>>>(a);
+  PS_CUDA_TRY(ctx, cudaGetLastError());
+  if (ctx->profile) {
+    PS_CUDA_TRY(ctx, cudaEventRecord(e1, st));
+    ctx->k1_events.push_back({e0, e1});
+  }
+  const int n = ctx->M * S::L;
+  k1s_reduce<<<(n + 255) / 256, 256, 0, st>>>(a.apart, a.bpart, a.T, a.NB, G, a.maxseg, ctx->M,
+                                              S::L, mode, v_own, ctx->d_S, bsub, out);
+  PS_CUDA_TRY(ctx, cudaGetLastError());
+  ctx->launches += 3;
+  return PS_OK;
+}
+
+}  // namespace
+
+int m2l_apply_sym(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
+                  const double2* v_own, const double2* bsub, cudaStream_t st) {
+  switch (ctx->p) {
+#define PS_CASE(P) \
+  case P:          \
+    return launch_s<P>(ctx, beta, bpow, out, mode, v_own, bsub, st);
+    PS_M2L_ORDERS(PS_CASE)
+#undef PS_CASE
+    default:
+      ctx->err = "apply_T (symmetric): multipole order p=" + std::to_string(ctx->p) +
+                 " not compiled";
+      return PS_ERR_UNSUPPORTED;
+  }
+}
+
+}  // namespace ps

@@ -133,6 +133,10 @@ class Engine:
                                          system.cols["c"].start, system.cols["d"].start))
         self.coupled = True
 
+    def set_k1_variant(self, variant: int):
+        """0 auto, 1 tiled K1, 2 symmetric K1s (see include/periscat_b200.h)."""
+        self._check(self.lib.ps_set_k1_variant(self.ctx, int(variant)))
+
     def precompute_coupling(self, max_gb: float = 40.0) -> bool:
         """Pre-assemble C and B on the device if they fit max_gb (see header)."""
         self._check(self.lib.ps_precompute_coupling(self.ctx, float(max_gb)))
