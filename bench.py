@@ -192,6 +192,8 @@ def run_ours(args):
     peak = ctypes.c_double()
     pms = ctypes.c_double()
     _lib.check(None, lib.ps_dfma_peak(local, ctypes.byref(peak), ctypes.byref(pms)))
+    tpeak = ctypes.c_double()
+    _lib.check(None, lib.ps_dmma_peak(local, ctypes.byref(tpeak)))
 
     sysm, centers, p, radius = grating.load_config(CFG)
     M, L = centers.shape[0], 2 * p + 1
@@ -326,11 +328,16 @@ def run_ours(args):
                 "config": _config_block(CFG, M, p, 1, world),
                 "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value,
                              "unit": "TFLOP/s", "frac": achieved / peak.value,
-                             "traffic": traffic, "kernel": "m2l_kernel (K1)",
+                             "traffic": traffic,
+                             "kernel": "m2l_sym_kernel (K1s, symmetric single-RHS M2L)" if world == 1
+                                       else "m2l_kernel (K1, tiled; target shard)",
                              "k1_avg_ms": k1_avg_ms,
                              "algorithmic": "8(2p+1)^2 flops per translation",
-                             "peak_source": "ps_dfma_peak DFMA-chain microbenchmark on this GPU "
-                                            "(MEASURED_PEAKS.json has no FP64 entry)"},
+                             "peak_source": "ps_dfma_peak: best DFMA-chain microbenchmark on this "
+                                            "GPU (MEASURED_PEAKS.json has no FP64 entry); K1 "
+                                            "issues DFMA on the FP64 vector pipe",
+                             "fp64_tensor_peak": tpeak.value,
+                             "frac_of_fp64_tensor_peak": achieved / tpeak.value},
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT,
                         "h2d_bytes_per_step": int(vh.numel() * 16),

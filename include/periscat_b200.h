@@ -167,6 +167,8 @@ int ps_dfma_peak(int device, double* tflops, double* ms);
 /* Same kernel launched back to back for ~seconds (sustained clock under the
  * power cap): the denominator for kernels timed inside a long step. */
 int ps_dfma_sustained(int device, double seconds, double* tflops);
+/* FP64 tensor-core (mma.sync m8n8k4 f64) throughput of the device, TFLOP/s. */
+int ps_dmma_peak(int device, double* tflops);
 
 #ifdef __cplusplus
 }

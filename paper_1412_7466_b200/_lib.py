@@ -43,6 +43,7 @@ SIGNATURES = {
     "ps_gmres": (_I, [_P, _P, _P, _D, _I, _IP, _DP, _P]),
     "ps_dfma_peak": (_I, [_I, _DP, _DP]),
     "ps_dfma_sustained": (_I, [_I, _D, _DP]),
+    "ps_dmma_peak": (_I, [_I, _DP]),
     "ps_profile": (_I, [_P, _I]),
     "ps_precompute_coupling": (_I, [_P, _D]),
     "ps_coupling_mode": (_I, [_P]),
