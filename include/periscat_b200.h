@@ -101,6 +101,9 @@ int ps_precompute_coupling(ps_ctx* ctx, double max_gb);
  * row serves the pair and its reverse -- when this context owns every
  * target, else tiled K1), 1 force tiled K1, 2 force K1s (full range only). */
 int ps_set_k1_variant(ps_ctx* ctx, int variant);
+/* Multi-RHS M2L kernel choice: 0 auto (FP64 tensor cores, mma.sync f64, for
+ * >= 12 RHS; DFMA K1m below), 1 force DFMA K1m, 2 force DMMA K1d. */
+int ps_set_mrhs_variant(ps_ctx* ctx, int variant);
 /* 1 if the pre-assembled coupling blocks are in use, 0 if matrix-free. */
 int ps_coupling_mode(const ps_ctx* ctx);
 

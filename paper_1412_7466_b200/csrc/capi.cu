@@ -443,6 +443,17 @@ int ps_set_k1_variant(ps_ctx* h, int variant) {
   return PS_OK;
 }
 
+int ps_set_mrhs_variant(ps_ctx* h, int variant) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (variant < 0 || variant > 2) {
+    c->err = "ps_set_mrhs_variant: 0 auto, 1 DFMA, 2 DMMA";
+    return PS_ERR_ARG;
+  }
+  c->mrhs_variant = variant;
+  return PS_OK;
+}
+
 int ps_coupling_mode(const ps_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->dense : -1; }
 
 int ps_profile(ps_ctx* h, int enable) {

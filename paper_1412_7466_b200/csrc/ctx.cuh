@@ -57,6 +57,7 @@ struct Ctx {
   int nrb = 0;              // Rayleigh-Bloch orders per direction (c, d)
   int nsv = 0;              // number of singular values
   int k1_variant = 0;       // 0 auto (K1s when all targets owned), 1 tiled K1, 2 symmetric K1s
+  int mrhs_variant = 0;     // 0 auto (K1d DMMA for >= 12 RHS), 1 DFMA K1m, 2 DMMA K1d
   int dense = 0;            // 1: apply C and B from the pre-assembled matrices
   int dcs0 = 0, dcs1 = 0;   // source range the stored C^T covers
 

@@ -23,6 +23,12 @@ int m2l_apply_sym(Ctx* ctx, const double2* beta, const double2* bpow, double2* o
 // dispatch: K1s when ctx owns every target and k1_variant allows it, else K1
 int m2l_apply_1(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
                 const double2* v_own, const double2* bsub, cudaStream_t st);
+// >= 12 RHS on the FP64 tensor cores (m2l_mma.cu), same contract as m2l_apply_mrhs.
+int m2l_apply_mma(Ctx* ctx, const double2* beta, double2* out, int mode, const double2* bsub,
+                  long long b_stride, cudaStream_t st);
+int m2l_apply_mrhs_dfma(Ctx* ctx, const double2* beta, double2* out, int mode,
+                        const double2* bsub, long long b_stride, cudaStream_t st);
+// dispatch for nrhs > 1: K1d (DMMA) when nrhs >= 12 (or forced), else K1m (DFMA)
 int m2l_apply_mrhs(Ctx* ctx, const double2* beta, double2* out, int mode, const double2* bsub,
                    long long b_stride, cudaStream_t st);
 }  // namespace ps

@@ -431,6 +431,13 @@ int launch_m(Ctx* ctx, const double2* beta, double2* out, int mode, const double
 
 int m2l_apply_mrhs(Ctx* ctx, const double2* beta, double2* out, int mode, const double2* bsub,
                    long long b_stride, cudaStream_t st) {
+  const bool mma = ctx->mrhs_variant == 2 || (ctx->mrhs_variant == 0 && ctx->nrhs >= 12);
+  if (mma) return m2l_apply_mma(ctx, beta, out, mode, bsub, b_stride, st);
+  return m2l_apply_mrhs_dfma(ctx, beta, out, mode, bsub, b_stride, st);
+}
+
+int m2l_apply_mrhs_dfma(Ctx* ctx, const double2* beta, double2* out, int mode,
+                        const double2* bsub, long long b_stride, cudaStream_t st) {
   switch (ctx->p) {
 #define PS_CASE(P) \
   case P:          \

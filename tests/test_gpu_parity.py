@@ -310,3 +310,23 @@ def test_gmres_identity_one_iteration(O):
     x, its, hist = solver.gmres(op, b, 1e-12, 10)
     assert its == [1]
     assert rel(x.cpu().numpy(), b.cpu().numpy()) < 1e-14
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("nrhs,p,M", [(16, 20, 40), (13, 25, 21), (4, 6, 30)])
+def test_mrhs_variants(O, variant, nrhs, p, M):
+    """Both multi-RHS kernels (1: DFMA K1m, 2: FP64-tensor-core K1d) vs the oracle."""
+    from paper_1412_7466_b200.engine import Engine
+    rng = np.random.default_rng(nrhs * 31 + p + variant)
+    centers = np.column_stack([rng.uniform(-0.45, 0.45, M), rng.uniform(-0.4, 0.4, M)])
+    L = 2 * p + 1
+    beta = _cplx(rng, (nrhs, M, L))
+    bl = np.exp(1j * rng.uniform(-np.pi, np.pi, nrhs))
+    eng = Engine(0)
+    eng.set_geometry(centers, p, 12.0, 1.0, 1)
+    eng.set_bloch(bl)
+    eng.set_mrhs_variant(variant)
+    got = eng.apply_T(_dev(beta)).cpu().numpy()
+    ref = O.apply_T(beta, centers, 12.0, p, bl)
+    for r in range(nrhs):
+        assert rel(got[r], ref[r]) <= MATVEC_TOL
