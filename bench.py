@@ -313,7 +313,7 @@ def run_ours(args):
     if not args.no_cfg5:
         sus = ctypes.c_double()
         _lib.check(None, lib.ps_dfma_sustained(local, 3.0, ctypes.byref(sus)))
-        cfg5 = cfg5_apply_T(dev, local, rank, world, sus.value, args)
+        cfg5 = cfg5_apply_T(dev, local, rank, world, sus.value, tpeak.value, args)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -353,7 +353,7 @@ def run_ours(args):
     return 0
 
 
-def cfg5_apply_T(dev, local, rank, world, peak, args):
+def cfg5_apply_T(dev, local, rank, world, dfma_peak, tensor_peak, args):
     import torch
     import torch.distributed as dist
 
@@ -397,13 +397,15 @@ def cfg5_apply_T(dev, local, rank, world, peak, args):
     flops = (t1 - t0) * (3 * M - 1) * R * 8.0 * L * L
     ach = flops / (k1_ms * 1e-3) / 1e12
     eng.close()
-    return {"workload": f"cfg5: apply_T (K1m), M={M}, p={p}, {R} RHS (incidence angles), "
+    return {"workload": f"cfg5: apply_T, M={M}, p={p}, {R} RHS (incidence angles), "
                         "target-sharded", "ms_per_step": ms, "steps": steps,
             "value": tr / (ms * 1e-3), "unit": UNIT,
-            "roofline": {"bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                         "frac": ach / peak, "kernel": "m2l_mrhs_kernel (K1m)",
-                         "peak_source": "ps_dfma_sustained: DFMA-chain kernel back to back "
-                                        "for 3 s on this GPU (sustained clock)"},
+            "roofline": {"bound": "fp64", "achieved": ach, "peak": tensor_peak,
+                         "unit": "TFLOP/s", "frac": ach / tensor_peak,
+                         "kernel": "m2l_mma_kernel (K1d: mma.sync m8n8k4 f64 FP64 tensor cores)",
+                         "peak_source": "ps_dmma_peak: mma.sync f64 chains on this GPU",
+                         "dfma_sustained_peak": dfma_peak,
+                         "frac_of_dfma_peak": ach / dfma_peak},
             "gpu_launches": int(stats["launches"]), "clocks": clk.summary()}
 
 

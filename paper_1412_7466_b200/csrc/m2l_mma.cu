@@ -109,6 +109,22 @@ __device__ __forceinline__ void produce_d(const ArgsD& a, long long w, double2* 
   });
 }
 
+// L2 prefetch of the weighted-beta rows of batch w (all producer lanes)
+template <int P>
+__device__ __forceinline__ void prefetch_bw_d(const ArgsD& a, long long w, int pl) {
+  using S = ShapeD<P>;
+  const int sb = (int)(w % a.nbatch) * kSB;
+  const int nr = min(kRG, a.nrhs - a.rg0);
+  for (int row = pl; row < nr * kSB; row += kPW * 32) {
+    const int r = a.rg0 + row / kSB;
+    const int g = sb + row % kSB;
+    if (g >= a.nimg) continue;
+    const char* p = reinterpret_cast<const char*>(a.bw + ((size_t)r * a.nimg + g) * S::L);
+    for (int off = 0; off < S::L * 16; off += 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p + off));
+  }
+}
+
 template <int P>
 __global__ void __launch_bounds__(kThreads, 1) m2l_mma_kernel(ArgsD a) {
   using S = ShapeD<P>;
@@ -131,10 +147,14 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mma_kernel(ArgsD a) {
   if (producer) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
     const int pw = warp - kCW;
+    const int pl = pw * 32 + lane;
+    prefetch_bw_d<P>(a, w0, pl);
+    if (w0 + 1 < w1) prefetch_bw_d<P>(a, w0 + 1, pl);
     produce_d<P>(a, w0, sym0, pw, lane);
     __syncthreads();
     for (long long w = w0; w < w1; ++w) {
       const int cur = (int)((w - w0) & 1);
+      if (w + 2 < w1) prefetch_bw_d<P>(a, w + 2, pl);
       if (w + 1 < w1) produce_d<P>(a, w + 1, cur ? sym0 : sym1, pw, lane);
       __syncthreads();
     }
