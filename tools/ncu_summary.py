@@ -16,6 +16,8 @@ KEYS = [
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe active % (of active cycles)"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed", "FP64 pipe active % (of elapsed)"),
+    ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "FP64 tensor (DMMA) sub-pipe active %"),
+    ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor pipe active % (elapsed)"),
     ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue active %"),
     ("smsp__warps_active.avg.per_cycle_active", "warps active / SMSP"),
     ("smsp__warps_eligible.avg.per_cycle_active", "warps eligible / SMSP"),
