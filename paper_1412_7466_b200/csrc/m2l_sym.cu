@@ -10,13 +10,15 @@
 // translation halves (the single-RHS K1 spends ~14% of the pipe on symbols).
 //
 // Work: unordered target-tile pairs (A <= B) of 8 inclusions, row-major
-// (A, A), (A, A+1), ...; a block is 2P+1 batches (one per copy l) of the 64
+// (A, A), (A, A+1), ...; a block is 2c+1 batches (one per image l) of the 64
 // rows (m in A, j in B).  Consumer warp w owns target A*8+w (forward) and
 // B*8+w (reverse); its lane (b, s) covers row block b against source slot s
 // of the batch, so per batch each warp sweeps 8 sources forward and, for
 // A < B, 8 sources in reverse, and the source sums are 3-level shuffle trees
-// (no shared-memory reduction, no consumer barrier).  Forward accumulators
-// live for a whole block row; reverse parts are flushed per block.  Diagonal
+// (no shared-memory reduction, no consumer barrier).  Complex MACs use the
+// Karatsuba 3-multiplication form (consume_s); one accumulator set is live
+// per sweep and is reduced over the source lanes into two persistent rows
+// per lane (forward: whole block row, reverse: one block).  Diagonal
 // blocks (A = B) run forward only.  k1s_reduce sums the parts in a fixed
 // order (deterministic) and applies the Schur epilogue.
 #include <cuda_runtime.h>
@@ -73,6 +75,7 @@ struct ShapeS {
 struct ArgsS {
   const double* centers;   // [M][2]
   const double2* bw;       // [M * ncp][L] bloch-weighted beta per source image
+  const double* bws;       // [M * ncp][L] re + im of bw (Karatsuba operand)
   double2* apart;          // [G][maxseg][kTT][L]  forward parts, one per (CTA, block row)
   double2* bpart;          // [NB][kTT][L]         reverse parts, one per cross block
   int M, T, NB, copies, ncp, maxseg;
@@ -126,72 +129,119 @@ __device__ __forceinline__ void produce_s(const ArgsS& a, int A, int B, int li, 
   });
 }
 
-// one Toeplitz sweep: rows at sp0 + slot*kTT (slot of nu = n - r), coefficients
-// from global (sign-flipped on odd n for the reverse apply)
+// One Toeplitz sweep with Karatsuba (3-multiplication) complex products:
+// rows at sp0 + slot*kTT (slot of nu = n - r), coefficients from global
+// (sign-flipped on odd order n for the reverse apply).  For b = beta[n] and
+// t = t_{n-r}:
+//   S1 += b.x t.x,  S2 += b.y t.y,  S3 += (b.x + b.y)(t.x + t.y)
+//   Re = S1 - S2,   Im = S3 - S1 - S2
+// so a complex MAC costs 3 DFMA instead of 4; t.x + t.y is formed once per
+// symbol as it enters the register window (1 DADD per step, shared by the
+// BO rows) and b.x + b.y is precomputed per source (bws).
 template <int P, bool REV>
 __device__ __forceinline__ void consume_s(const double2* __restrict__ rowbase,
                                           const double2* __restrict__ bsrc,
-                                          double2 (&acc)[ShapeS<P>::BO], int b) {
+                                          const double* __restrict__ ssrc,
+                                          double (&acc)[3][ShapeS<P>::BO], int b) {
   using S = ShapeS<P>;
   constexpr int BO = S::BO;
   constexpr int R0 = S::FP + 2 * P;
   constexpr int MODB = 64 * BO;
   const double2* sp = rowbase + (size_t)(R0 - b * BO) * kTT;
-  double2 w[BO];
+  double wx[BO], wy[BO], ws[BO];
 #pragma unroll
-  for (int i = 0; i < BO; ++i) w[(R0 - i + MODB) % BO] = sp[-i * kTT];
+  for (int i = 0; i < BO; ++i) {
+    const double2 t = sp[-i * kTT];
+    const int q = (R0 - i + MODB) % BO;
+    wx[q] = t.x;
+    wy[q] = t.y;
+    ws[q] = t.x + t.y;
+  }
   auto step = [&](auto n_c) {
     constexpr int n = decltype(n_c)::value;
     constexpr int u = n % BO;
     const double2 nxt = sp[(n + 1) * kTT];
     double2 bb = __ldg(bsrc + n);
-    if (REV && ((n - P) & 1)) bb = make_double2(-bb.x, -bb.y);   // (-1)^{order n}
-#pragma unroll
-    for (int i = 0; i < BO; ++i) {
-      const double2 tt = w[(R0 + u - i + MODB) % BO];
-      acc[i].x = fma(bb.x, tt.x, acc[i].x);
-      acc[i].y = fma(bb.x, tt.y, acc[i].y);
+    double bs = __ldg(ssrc + n);
+    if (REV && ((n - P) & 1)) {                                  // (-1)^{order n}
+      bb = make_double2(-bb.x, -bb.y);
+      bs = -bs;
     }
 #pragma unroll
-    for (int i = 0; i < BO; ++i) {
-      const double2 tt = w[(R0 + u - i + MODB) % BO];
-      acc[i].x = fma(-bb.y, tt.y, acc[i].x);
-      acc[i].y = fma(bb.y, tt.x, acc[i].y);
-    }
-    w[(R0 + u + 1 + MODB) % BO] = nxt;
+    for (int i = 0; i < BO; ++i) acc[0][i] = fma(bb.x, wx[(R0 + u - i + MODB) % BO], acc[0][i]);
+#pragma unroll
+    for (int i = 0; i < BO; ++i) acc[1][i] = fma(bb.y, wy[(R0 + u - i + MODB) % BO], acc[1][i]);
+#pragma unroll
+    for (int i = 0; i < BO; ++i) acc[2][i] = fma(bs, ws[(R0 + u - i + MODB) % BO], acc[2][i]);
+    constexpr int q = (R0 + u + 1 + MODB) % BO;
+    wx[q] = nxt.x;
+    wy[q] = nxt.y;
+    ws[q] = nxt.x + nxt.y;
   };
   static_for<S::L>(step);
 }
 
-// Sum one accumulator set over the 8 source lanes s (lane = b*8 + s) with a
-// fixed xor tree, then lane s = 0 writes the rows of its block b.
+// Reduce the Karatsuba partial sums of one sweep over the 8 source lanes s
+// (lane = b*8 + s) by recursive halving (xor 4, 2, 1: each level ships half
+// of the values, fixed order -> deterministic) and add them into the lane's
+// two persistent complex rows r0 = 8*s2 + 4*s1 + 2*s0, r0 + 1 of block b.
+// The accumulators are cleared for the next sweep.
+template <int BO>
+__device__ __forceinline__ void reduce_keep(double (&acc)[3][BO], double2 (&keep)[2], int s) {
+  static_assert(BO <= 16, "two rows per lane");
+  auto V = [&](int idx) -> double {           // idx = 3*row + component (row < 16)
+    const int r = idx / 3, c = idx % 3;
+    return r < BO ? acc[c][r] : 0.0;
+  };
+  const bool h4 = s & 4, h2 = s & 2, h1 = s & 1;
+  double v1[24];
+#pragma unroll
+  for (int k = 0; k < 24; ++k) {
+    const double lo = V(k), hi = V(24 + k);
+    const double send = h4 ? lo : hi;
+    v1[k] = (h4 ? hi : lo) + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  double v2[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    const double send = h2 ? v1[k] : v1[12 + k];
+    v2[k] = (h2 ? v1[12 + k] : v1[k]) + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  double v3[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const double send = h1 ? v2[k] : v2[6 + k];
+    v3[k] = (h1 ? v2[6 + k] : v2[k]) + __shfl_xor_sync(0xffffffffu, send, 1);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double s1 = v3[3 * k], s2 = v3[3 * k + 1], s3 = v3[3 * k + 2];
+    keep[k].x += s1 - s2;
+    keep[k].y += s3 - s1 - s2;
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int i = 0; i < BO; ++i) acc[c][i] = 0.0;
+}
+
+// write the lane's two persistent rows of block b, then clear them.
 // sign_rows: multiply row m' by (-1)^{m'} (reverse parts).
 template <int P>
-__device__ __forceinline__ void flush_s(double2 (&acc)[ShapeS<P>::BO], double2* dst, int b, int s,
-                                       bool sign_rows) {
+__device__ __forceinline__ void write_keep(double2 (&keep)[2], double2* dst, int b, int s,
+                                          bool sign_rows) {
   using S = ShapeS<P>;
-  constexpr int BO = S::BO;
+  const int r0 = 8 * ((s >> 2) & 1) + 4 * ((s >> 1) & 1) + 2 * (s & 1);
 #pragma unroll
-  for (int i = 0; i < BO; ++i) {
-#pragma unroll
-    for (int o = 1; o < kTT; o <<= 1) {
-      acc[i].x += __shfl_xor_sync(0xffffffffu, acc[i].x, o);
-      acc[i].y += __shfl_xor_sync(0xffffffffu, acc[i].y, o);
+  for (int k = 0; k < 2; ++k) {
+    const int i = r0 + k, r = b * S::BO + i;
+    if (i < S::BO && r < S::L) {
+      double2 v = keep[k];
+      if (sign_rows && ((r - P) & 1)) v = make_double2(-v.x, -v.y);
+      dst[r] = v;
     }
+    keep[k] = make_double2(0.0, 0.0);
   }
-  if (s == 0) {
-#pragma unroll
-    for (int i = 0; i < BO; ++i) {
-      const int r = b * BO + i;
-      if (r < S::L) {
-        double2 v = acc[i];
-        if (sign_rows && ((r - P) & 1)) v = make_double2(-v.x, -v.y);
-        dst[r] = v;
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < BO; ++i) acc[i] = make_double2(0.0, 0.0);
 }
 
 template <int P>
@@ -245,12 +295,18 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
   __syncthreads();
 
-  // warp w owns target A*8+w (forward, accA) and B*8+w (reverse, accB);
-  // lane (b, s) covers rows [b*BO, b*BO+BO) and source slot s of the batch
+  // warp w owns target A*8+w (forward, keepA) and B*8+w (reverse, keepB);
+  // lane (b, s) covers rows [b*BO, b*BO+BO) and source slot s of the batch.
+  // One Karatsuba accumulator set is live per sweep; after each sweep it is
+  // reduced over s into the lane's two persistent rows.
   const int b = lane / kTT, s = lane % kTT;
-  double2 accA[BO], accB[BO];
+  double acc[3][BO];
 #pragma unroll
-  for (int i = 0; i < BO; ++i) accA[i] = accB[i] = make_double2(0.0, 0.0);
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int i = 0; i < BO; ++i) acc[c][i] = 0.0;
+  double2 keepA[2], keepB[2];
+  keepA[0] = keepA[1] = keepB[0] = keepB[1] = make_double2(0.0, 0.0);
   int A, B;
   block_ab(k0, a.T, A, B);
   const int A0 = A;
@@ -262,17 +318,19 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
     // forward: target m = A*8 + w, source image (j = B*8 + s, l): row (m=w, j=s)
     {
       const int j = min(B * kTT + s, a.M - 1);            // dead rows are zero
-      consume_s<P, false>(symc + (size_t)s * S::SJ + warp,
-                          a.bw + ((size_t)j * a.ncp + li) * L, accA, b);
+      const size_t g = ((size_t)j * a.ncp + li) * L;
+      consume_s<P, false>(symc + (size_t)s * S::SJ + warp, a.bw + g, a.bws + g, acc, b);
+      reduce_keep<BO>(acc, keepA, s);
     }
     // reverse: target j = B*8 + w, source image (m = A*8 + s, -l): row (m=s, j=w)
     if (A != B) {
       const int m = min(A * kTT + s, a.M - 1);
-      consume_s<P, true>(symc + (size_t)warp * S::SJ + s,
-                         a.bw + ((size_t)m * a.ncp + (a.copies - l)) * L, accB, b);
+      const size_t g = ((size_t)m * a.ncp + (a.copies - l)) * L;
+      consume_s<P, true>(symc + (size_t)warp * S::SJ + s, a.bw + g, a.bws + g, acc, b);
+      reduce_keep<BO>(acc, keepB, s);
     }
     if (li == a.ncp - 1) {                     // block complete
-      if (A != B) flush_s<P>(accB, a.bpart + ((size_t)blk * kTT + warp) * L, b, s, true);
+      if (A != B) write_keep<P>(keepB, a.bpart + ((size_t)blk * kTT + warp) * L, b, s, true);
       ++blk;
       li = 0;
       const int Aold = A;
@@ -281,9 +339,9 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
         B = A;
       }
       if (A != Aold || it + 1 == nbat)         // block row finished (or CTA done)
-        flush_s<P>(accA,
-                   a.apart + (((size_t)blockIdx.x * a.maxseg + (Aold - A0)) * kTT + warp) * L, b,
-                   s, false);
+        write_keep<P>(keepA,
+                      a.apart + (((size_t)blockIdx.x * a.maxseg + (Aold - A0)) * kTT + warp) * L,
+                      b, s, false);
     } else {
       ++li;
     }
@@ -293,7 +351,8 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
 
 // bw[g][n] = bloch^{l(g)} beta[j(g)][n]
 __global__ void bloch_weight_1(const double2* __restrict__ beta, const double2* __restrict__ bpow,
-                               int M, int L, int ncp, double2* __restrict__ bw) {
+                               int M, int L, int ncp, double2* __restrict__ bw,
+                               double* __restrict__ bws) {
   const long long total = (long long)M * ncp * L;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -302,7 +361,9 @@ __global__ void bloch_weight_1(const double2* __restrict__ beta, const double2* 
     const int j = (int)(g / ncp), li = (int)(g % ncp);
     const double2 bv = beta[(long long)j * L + n];
     const double2 wv = bpow[1 + li];
-    bw[i] = make_double2(fma(bv.x, wv.x, -bv.y * wv.y), fma(bv.x, wv.y, bv.y * wv.x));
+    const double2 v = make_double2(fma(bv.x, wv.x, -bv.y * wv.y), fma(bv.x, wv.y, bv.y * wv.x));
+    bw[i] = v;
+    bws[i] = v.x + v.y;
   }
 }
 
@@ -398,18 +459,20 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   const size_t nbp = (size_t)a.NB * kTT * S::L;
   const size_t npart = na + nbp;
   const size_t nbw = (size_t)ctx->M * a.ncp * S::L;
-  if (ctx->partial_elems < npart + nbw) {
+  if (ctx->partial_elems < npart + nbw + nbw) {
     if (ctx->d_partial) cudaFree(ctx->d_partial);
     ctx->d_partial = nullptr;
     ctx->partial_elems = 0;
-    PS_CUDA_TRY(ctx, cudaMalloc(&ctx->d_partial, (npart + nbw) * sizeof(double2)));
-    ctx->partial_elems = npart + nbw;
+    PS_CUDA_TRY(ctx, cudaMalloc(&ctx->d_partial, (npart + nbw + nbw) * sizeof(double2)));
+    ctx->partial_elems = npart + nbw + nbw;
   }
   a.apart = ctx->d_partial;
   a.bpart = ctx->d_partial + na;
   double2* bw = ctx->d_partial + npart;
   a.bw = bw;
-  bloch_weight_1<<<2 * ctx->sm_count, 256, 0, st>>>(beta, bpow - 1, ctx->M, S::L, a.ncp, bw);
+  a.bws = reinterpret_cast<double*>(bw + nbw);
+  bloch_weight_1<<<2 * ctx->sm_count, 256, 0, st>>>(beta, bpow - 1, ctx->M, S::L, a.ncp, bw,
+                                                    const_cast<double*>(a.bws));
   PS_CUDA_TRY(ctx, cudaGetLastError());
   static bool attr_done = false;
   if (!attr_done) {

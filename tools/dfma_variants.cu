@@ -29,6 +29,40 @@ __global__ void chains2(double* out, int iters, double b) {
   for (int i = 0; i < NC; ++i) s += x[i];
   if (s == 12345.678) out[0] = s;
 }
+
+// mixed: warps with (warp & 1) == 0 run DFMA chains, odd warps run DMMA
+// chains (mma.sync m8n8k4 f64): do the two FP64 paths share one pipe?
+// mode 0: all DFMA, 1: all DMMA, 2: half/half
+__global__ void mixed(double* out, int iters, int mode) {
+  const int w = threadIdx.x >> 5;
+  const bool use_mma = mode == 1 || (mode == 2 && (w & 1));
+  double s = 0;
+  if (use_mma) {
+    double a = 1.0 + threadIdx.x * 1e-9, b = 0.999999;
+    double c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = i * 1e-3;
+    for (int it = 0; it < iters / 8; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                     : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  } else {
+    double x[16], wv[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) { x[i] = threadIdx.x * 1e-3 + i; wv[i] = 0.999 + i * 1e-6; }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = fma(wv[i], 1e-7, x[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += x[i];
+  }
+  if (s == 12345.678) out[0] = s;
+}
 template <typename K>
 void run(const char* name, K k, int blocks, int threads, double fl_per_iter_thread, int iters) {
   double* d; cudaMalloc(&d, 8);
@@ -43,9 +77,37 @@ void run(const char* name, K k, int blocks, int threads, double fl_per_iter_thre
   printf("%-28s blocks=%4d thr=%4d  %.2f TFLOP/s\n", name, blocks, threads, fl / (best * 1e-3) / 1e12);
   cudaFree(d);
 }
-int main() {
+int main(int argc, char** argv) {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int it = 1 << 14;
+  if (argc > 1 && argv[1][0] == 'm') {
+    // per-warp flops per iteration: DFMA warp 32 thr x 16 fma x 2; DMMA warp 8/8 iters x 8 mma x 512
+    for (int thr : {256, 512, 1024}) {
+      for (int mode = 0; mode < 3; ++mode) {
+        double* d; cudaMalloc(&d, 8);
+        cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+        mixed<<<sms, thr>>>(d, 1024, mode);
+        float best = 1e30f;
+        for (int r = 0; r < 3; ++r) {
+          cudaEventRecord(e0); mixed<<<sms, thr>>>(d, it, mode); cudaEventRecord(e1); cudaEventSynchronize(e1);
+          float t; cudaEventElapsedTime(&t, e0, e1); if (t < best) best = t;
+        }
+        const int warps = thr / 32;
+        const int wm = mode == 0 ? 0 : mode == 1 ? warps : warps / 2;
+        const double fl = (double)sms * ((warps - wm) * 32.0 * 16 * 2 * it + wm * (it / 8) * 8.0 * 512);
+        printf("mixed mode=%d thr=%4d  %.2f TFLOP/s\n", mode, thr, fl / (best * 1e-3) / 1e12);
+        cudaFree(d);
+      }
+    }
+    return 0;
+  }
+  if (argc > 1) {   // warps-per-SMSP sweep at one CTA per SM (the K1s shape)
+    for (int thr : {128, 256, 384, 512}) {
+      run("chains2<26>", [](double* d, int i, int b, int t) { chains2<26><<<b, t>>>(d, i, 1e-7); }, sms, thr, 52.0, it);
+      run("chains2<52>", [](double* d, int i, int b, int t) { chains2<52><<<b, t>>>(d, i, 1e-7); }, sms, thr, 104.0, it / 2);
+    }
+    return 0;
+  }
   for (int occ : {2, 4, 8, 16}) {
     run("chains<16>", [](double* d, int i, int b, int t) { chains<16><<<b, t>>>(d, i, 0.9999999, 1e-7); }, sms * occ, 256, 32.0, it);
     run("chains<8>", [](double* d, int i, int b, int t) { chains<8><<<b, t>>>(d, i, 0.9999999, 1e-7); }, sms * occ, 256, 16.0, it);
