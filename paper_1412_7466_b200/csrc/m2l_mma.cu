@@ -9,8 +9,8 @@
 // (the Toeplitz blocks of the 8 targets stacked vertically: 8L rows are
 // exactly L row tiles of 8, so only the K = L dimension is padded).  It runs
 // as mma.sync.m8n8k4.f64 (DMMA, 256 FMA per warp instruction; measured
-// 37.1 TF/s on B200 against 34.2 TF/s for DFMA), four real MMAs per complex
-// tile.  The symbol rows come from the same producer warpgroup as K1/K1m.
+// 37.1 TF/s on B200 against 34.2 TF/s for DFMA), three real MMAs per complex
+// tile (Karatsuba: Ar Br, Ai Bi, (Ar + Ai)(Br + Bi)).  The symbol rows come from the same producer warpgroup as K1/K1m.
 //
 // Warps: 12 consumer warps own (row tile, RHS tile) accumulator units
 // (2L units per CTA group, <= 7 per warp); 4 producer warps (setmaxnreg).
@@ -179,9 +179,11 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mma_kernel(ArgsD a) {
     tA[k] = srow / L;                            // target slot
     mA[k] = srow % L;                            // row m'
   }
-  double cr[UPW][2], ci[UPW][2];
+  // Karatsuba: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi);
+  // Re C = P1 - P2, Im C = P3 - P1 - P2 -> three real MMAs per complex tile
+  double p1[UPW][2], p2[UPW][2], p3[UPW][2];
 #pragma unroll
-  for (int k = 0; k < UPW; ++k) cr[k][0] = cr[k][1] = ci[k][0] = ci[k][1] = 0.0;
+  for (int k = 0; k < UPW; ++k) p1[k][0] = p1[k][1] = p2[k][0] = p2[k][1] = p3[k][0] = p3[k][1] = 0.0;
   int seg = 0;
   const int rb = a.rg0 + fr;                     // B column (RHS) for tile 0; +8 for tile 1
 
@@ -204,15 +206,16 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mma_kernel(ArgsD a) {
           if (ok0) b0 = __ldg(bw0 + n);
           if (ok1) b1 = __ldg(bw1 + n);
         }
+        const double bs0 = b0.x + b0.y, bs1 = b1.x + b1.y;
 #pragma unroll
         for (int k = 0; k < UPW; ++k) {
           if (!uok[k]) continue;
           const double2 av = rowb[(size_t)tA[k] * S::NSP + (n - mA[k])];
           const double2 bb = nt_[k] ? b1 : b0;
-          dmma(cr[k], av.x, bb.x);
-          dmma(cr[k], av.y, -bb.y);
-          dmma(ci[k], av.x, bb.y);
-          dmma(ci[k], av.y, bb.x);
+          const double bs = nt_[k] ? bs1 : bs0;
+          dmma(p1[k], av.x, bb.x);
+          dmma(p2[k], av.y, bb.y);
+          dmma(p3[k], av.x + av.y, bs);
         }
       }
     }
@@ -226,10 +229,11 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mma_kernel(ArgsD a) {
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             const int rl = nt_[k] * 8 + 2 * fc + i;        // RHS within the group
-            dst[((size_t)rl * kTT + t) * L + mp] = make_double2(cr[k][i], ci[k][i]);
+            dst[((size_t)rl * kTT + t) * L + mp] =
+                make_double2(p1[k][i] - p2[k][i], p3[k][i] - p1[k][i] - p2[k][i]);
           }
         }
-        cr[k][0] = cr[k][1] = ci[k][0] = ci[k][1] = 0.0;
+        p1[k][0] = p1[k][1] = p2[k][0] = p2[k][1] = p3[k][0] = p3[k][1] = 0.0;
       }
       ++seg;
     }
