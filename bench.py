@@ -354,6 +354,10 @@ def run_ours(args):
                                        else "m2l_kernel (K1, tiled; target shard)",
                              "k1_avg_ms": k1_avg_ms,
                              "algorithmic": "8(2p+1)^2 flops per translation",
+                             "executed": "Karatsuba complex MACs: 3 real FMA (6 flops) per "
+                                         "complex MAC, i.e. 6(2p+1)^2 FP64 flops issued per "
+                                         "translation plus symbol generation; 'achieved' "
+                                         "counts the 8(2p+1)^2 algorithmic flops",
                              "peak_source": "ps_dfma_peak: best DFMA-chain microbenchmark on this "
                                             "GPU (MEASURED_PEAKS.json has no FP64 entry); K1 "
                                             "issues DFMA on the FP64 vector pipe",
@@ -424,6 +428,7 @@ def cfg5_apply_T(dev, local, rank, world, dfma_peak, tensor_peak, args):
             "roofline": {"bound": "fp64", "achieved": ach, "peak": tensor_peak,
                          "unit": "TFLOP/s", "frac": ach / tensor_peak,
                          "kernel": "m2l_mma_kernel (K1d: mma.sync m8n8k4 f64 FP64 tensor cores)",
+                         "executed": "Karatsuba: 3 real MMAs per complex tile (6L^2 issued vs 8L^2 algorithmic flops per translation)",
                          "peak_source": "ps_dmma_peak: mma.sync f64 chains on this GPU",
                          "dfma_sustained_peak": dfma_peak,
                          "frac_of_dfma_peak": ach / dfma_peak},

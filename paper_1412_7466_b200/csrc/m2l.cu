@@ -8,14 +8,15 @@
 // Work decomposition (one CTA per SM, persistent over a contiguous range of
 // the (target tile x source batch) work list):
 //   * a target tile is kTT = 8 targets, a source batch kS = 8 source images;
-//   * 2 producer warps build the 64 symbol rows t_{-2p..2p} of the next batch
+//   * 4 producer warps build the 64 symbol rows t_{-2p..2p} of the next batch
 //     into shared memory (one pair per lane, bessel.cuh/symbols.cuh) and stage
 //     the batch's bloch-weighted beta vectors;
 //   * 8 consumer warps (one per source image of the current batch) apply the
 //     Toeplitz sums: lane (b, t) owns rows [b*BO, b*BO+BO) of target t and
 //     streams the L columns with a BO-deep sliding window of symbols held in
-//     registers, so every column step is 2 LDS.128 (beta broadcast + one
-//     symbol) against 4*BO DFMA;
+//     registers; complex MACs use the Karatsuba form, so every column step is
+//     3 LDS (beta broadcast, its re+im, one symbol) against 3*BO DFMA;
+//   * setmaxnreg splits the register file 216 (consumers) / 72 (producers);
 //   * the two roles are double-buffered around one __syncthreads per batch;
 //   * at a tile boundary the 8 consumer warps reduce their accumulators
 //     through shared memory and write one partial per (CTA, tile segment);
@@ -56,6 +57,9 @@ constexpr int kPairsPerWarp = kPairs / kPW;
 static_assert(kTT * kNB == 32, "one consumer warp covers a full target tile");
 static_assert(kPairs % kPW == 0 && 2 * kPairsPerWarp == 32,
               "two producer lanes per symbol row (t_+nu / t_-nu halves)");
+static_assert(kPW == 4, "one producer warp per sub-partition (setmaxnreg split)");
+constexpr int kConsumerRegs = 216;
+constexpr int kProducerRegs = 504 - 2 * kConsumerRegs;   // 3 warps x 168 per sub-partition
 
 template <int P>
 struct Shape {
@@ -67,7 +71,8 @@ struct Shape {
   static constexpr int NSP = FP + NS + 1;      // + one tail slot for the prefetch
   static constexpr int SYM = kS * NSP * kTT;   // double2 per symbol buffer
   static constexpr int BET = kS * L;           // double2 per beta buffer
-  static constexpr size_t SMEM = 2 * (size_t)(SYM + BET) * sizeof(double2);
+  static constexpr size_t SMEM =
+      2 * (size_t)(SYM + BET) * sizeof(double2) + 2 * (size_t)BET * sizeof(double);
 };
 
 struct Args {
@@ -90,7 +95,7 @@ __device__ __forceinline__ void consumer_bar() {
 
 template <int P>
 __device__ __forceinline__ void produce(const Args& a, long long w, double2* sym, double2* bet,
-                                        int pi) {
+                                        double* bets, int pi) {
   using S = Shape<P>;
   const int tile = (int)(w / a.nbatch);
   const int sb = (int)(w % a.nbatch) * kS;
@@ -141,63 +146,52 @@ __device__ __forceinline__ void produce(const Args& a, long long w, double2* sym
       v.y = fma(b.x, wgt.y, b.y * wgt.x);
     }
     bet[idx] = v;
+    bets[idx] = v.x + v.y;
   }
 }
 
+// Karatsuba Toeplitz sweep (3 DFMA per complex MAC): for b = beta[n] and
+// t = t_{n-r},  S1 += b.x t.x,  S2 += b.y t.y,  S3 += (b.x + b.y)(t.x + t.y);
+// Re = S1 - S2, Im = S3 - S1 - S2 at the tile flush.  t.x + t.y is formed as
+// the symbol enters the register window; b.x + b.y comes from the producer.
 template <int P>
 __device__ __forceinline__ void consume(const double2* __restrict__ sym,
                                         const double2* __restrict__ bet,
-                                        double2 (&acc)[Shape<P>::BO], int b, int t) {
+                                        const double* __restrict__ bets,
+                                        double (&acc)[3][Shape<P>::BO], int b, int t) {
   using S = Shape<P>;
   constexpr int BO = S::BO;
   constexpr int R0 = S::FP + 2 * P;              // slot of nu = 0 - 0 at step 0
   constexpr int MODB = 64 * BO;                  // keeps ring indices non-negative
   const double2* sp = sym + (size_t)(R0 - b * BO) * kTT + t;
-  double2 w[BO];
+  double wx[BO], wy[BO], ws[BO];
 #pragma unroll
-  for (int i = 0; i < BO; ++i) w[(R0 - i + MODB) % BO] = sp[-i * kTT];
+  for (int i = 0; i < BO; ++i) {
+    const double2 v = sp[-i * kTT];
+    const int q = (R0 - i + MODB) % BO;
+    wx[q] = v.x;
+    wy[q] = v.y;
+    ws[q] = v.x + v.y;
+  }
   // one column step; u = n mod BO is compile-time so the ring indices are static
-  auto step = [&](int n, auto u_c) {
-    constexpr int u = decltype(u_c)::value;
+  auto step = [&](auto n_c) {
+    constexpr int n = decltype(n_c)::value;
+    constexpr int u = n % BO;
     const double2 nxt = sp[(n + 1) * kTT];
     const double2 bb = bet[n];
-    const double nby = -bb.y;
-#ifdef PS_K1_ONEPASS
+    const double bs = bets[n];
 #pragma unroll
-    for (int i = 0; i < BO; ++i) {
-      const double2 tt = w[(R0 + u - i + MODB) % BO];
-      acc[i].x = fma(bb.x, tt.x, acc[i].x);
-      acc[i].x = fma(nby, tt.y, acc[i].x);
-      acc[i].y = fma(bb.x, tt.y, acc[i].y);
-      acc[i].y = fma(bb.y, tt.x, acc[i].y);
-    }
-#else
-    // two passes: the 2*BO FMAs of a pass are independent, so each
-    // accumulator's second FMA issues a full pass after its first
+    for (int i = 0; i < BO; ++i) acc[0][i] = fma(bb.x, wx[(R0 + u - i + MODB) % BO], acc[0][i]);
 #pragma unroll
-    for (int i = 0; i < BO; ++i) {
-      const double2 tt = w[(R0 + u - i + MODB) % BO];
-      acc[i].x = fma(bb.x, tt.x, acc[i].x);
-      acc[i].y = fma(bb.x, tt.y, acc[i].y);
-    }
+    for (int i = 0; i < BO; ++i) acc[1][i] = fma(bb.y, wy[(R0 + u - i + MODB) % BO], acc[1][i]);
 #pragma unroll
-    for (int i = 0; i < BO; ++i) {
-      const double2 tt = w[(R0 + u - i + MODB) % BO];
-      acc[i].x = fma(nby, tt.y, acc[i].x);
-      acc[i].y = fma(bb.y, tt.x, acc[i].y);
-    }
-#endif
-    w[(R0 + u + 1 + MODB) % BO] = nxt;
+    for (int i = 0; i < BO; ++i) acc[2][i] = fma(bs, ws[(R0 + u - i + MODB) % BO], acc[2][i]);
+    constexpr int q = (R0 + u + 1 + MODB) % BO;
+    wx[q] = nxt.x;
+    wy[q] = nxt.y;
+    ws[q] = nxt.x + nxt.y;
   };
-#ifndef PS_K1_PARTIAL_UNROLL
-  static_for<S::L>([&](auto u) { step(decltype(u)::value, IC<decltype(u)::value % BO>{}); });
-#else
-  constexpr int NFULL = (S::L / BO) * BO;
-#pragma unroll 1
-  for (int n0 = 0; n0 < NFULL; n0 += BO)
-    static_for<BO>([&](auto u) { step(n0 + decltype(u)::value, u); });
-  static_for<S::L - NFULL>([&](auto u) { step(NFULL + decltype(u)::value, u); });
-#endif
+  static_for<S::L>(step);
 }
 
 template <int P>
@@ -209,6 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_kernel(Args a) {
   double2* sym1 = smem + S::SYM;
   double2* bet0 = smem + 2 * S::SYM;
   double2* bet1 = bet0 + S::BET;
+  double* bets0 = reinterpret_cast<double*>(bet1 + S::BET);
+  double* bets1 = bets0 + S::BET;
 
   const int G = gridDim.x;
   const long long w0 = work_begin(a.W, G, blockIdx.x);
@@ -230,50 +226,64 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_kernel(Args a) {
     (buf ? sym1 : sym0)[((size_t)s * S::NSP + slot) * kTT + t] = make_double2(0.0, 0.0);
   }
   __syncthreads();
-  if (producer) produce<P>(a, w0, sym0, bet0, pi);
+
+  if (producer) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
+    produce<P>(a, w0, sym0, bet0, bets0, pi);
+    __syncthreads();
+    for (long long w = w0; w < w1; ++w) {
+      const int cur = (int)((w - w0) & 1);
+      if (w + 1 < w1)
+        produce<P>(a, w + 1, cur ? sym0 : sym1, cur ? bet0 : bet1, cur ? bets0 : bets1, pi);
+      __syncthreads();
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
   __syncthreads();
 
-  double2 acc[BO];
+  double acc[3][BO];
 #pragma unroll
-  for (int i = 0; i < BO; ++i) acc[i] = make_double2(0.0, 0.0);
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int i = 0; i < BO; ++i) acc[c][i] = 0.0;
   const int b = lane / kTT, t = lane % kTT;
   int seg = 0;
 
   for (long long w = w0; w < w1; ++w) {
     const int cur = (int)((w - w0) & 1);
     double2* symc = cur ? sym1 : sym0;
-    double2* betc = cur ? bet1 : bet0;
-    if (producer) {
-      if (w + 1 < w1) produce<P>(a, w + 1, cur ? sym0 : sym1, cur ? bet0 : bet1, pi);
-    } else {
-      consume<P>(symc + (size_t)warp * S::NSP * kTT, betc + warp * S::L, acc, b, t);
-      const bool flush = (w + 1 == w1) || ((w + 1) % a.nbatch == 0);
-      if (flush) {
-        // cross-warp reduction through the (now idle) current symbol buffer
-        consumer_bar();
-        double2* red = symc;   // [kS][kTT][ROWS]
+    const double2* betc = cur ? bet1 : bet0;
+    const double* betsc = cur ? bets1 : bets0;
+    consume<P>(symc + (size_t)warp * S::NSP * kTT, betc + warp * S::L, betsc + warp * S::L, acc,
+               b, t);
+    const bool flush = (w + 1 == w1) || ((w + 1) % a.nbatch == 0);
+    if (flush) {
+      // cross-warp reduction through the (now idle) current symbol buffer
+      consumer_bar();
+      double2* red = symc;   // [kS][kTT][ROWS]
 #pragma unroll
-        for (int i = 0; i < BO; ++i)
-          red[((size_t)warp * kTT + t) * S::ROWS + b * BO + i] = acc[i];
-        consumer_bar();
-        const int tile = (int)(w / a.nbatch);
-        double2* dst = a.partial + ((size_t)blockIdx.x * a.maxseg + seg) * kTT * S::L;
-        for (int idx = threadIdx.x; idx < kTT * S::L; idx += kS * 32) {
-          const int tt = idx / S::L, r = idx % S::L;
-          double2 sum = make_double2(0.0, 0.0);
+      for (int i = 0; i < BO; ++i)
+        red[((size_t)warp * kTT + t) * S::ROWS + b * BO + i] =
+            make_double2(acc[0][i] - acc[1][i], acc[2][i] - acc[0][i] - acc[1][i]);
+      consumer_bar();
+      double2* dst = a.partial + ((size_t)blockIdx.x * a.maxseg + seg) * kTT * S::L;
+      for (int idx = threadIdx.x; idx < kTT * S::L; idx += kS * 32) {
+        const int tt = idx / S::L, r = idx % S::L;
+        double2 sum = make_double2(0.0, 0.0);
 #pragma unroll
-          for (int ww = 0; ww < kS; ++ww) {
-            const double2 v = red[((size_t)ww * kTT + tt) * S::ROWS + r];
-            sum.x += v.x;
-            sum.y += v.y;
-          }
-          dst[idx] = sum;
+        for (int ww = 0; ww < kS; ++ww) {
+          const double2 v = red[((size_t)ww * kTT + tt) * S::ROWS + r];
+          sum.x += v.x;
+          sum.y += v.y;
         }
-        (void)tile;
-        ++seg;
-#pragma unroll
-        for (int i = 0; i < BO; ++i) acc[i] = make_double2(0.0, 0.0);
+        dst[idx] = sum;
       }
+      ++seg;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int i = 0; i < BO; ++i) acc[c][i] = 0.0;
     }
     __syncthreads();
   }
@@ -389,7 +399,9 @@ int m2l_max_order() { return PS_M2L_MAX_P; }
 int m2l_apply_1(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
                 const double2* v_own, const double2* bsub, cudaStream_t st) {
   const bool full = ctx->t_begin == 0 && ctx->t_end == ctx->M;
-  const bool sym = ctx->k1_variant == 2 || (ctx->k1_variant == 0 && full && ctx->M >= 64);
+  // crossover measured with tools/probe_variant.py (Karatsuba K1 / K1s): the
+  // symmetric kernel wins from M ~ 500 (4% at M = 1000), the tiled one below
+  const bool sym = ctx->k1_variant == 2 || (ctx->k1_variant == 0 && full && ctx->M >= 512);
   if (sym && full) return m2l_apply_sym(ctx, beta, bpow, out, mode, v_own, bsub, st);
   return m2l_apply(ctx, beta, bpow, out, mode, v_own, bsub, st);
 }

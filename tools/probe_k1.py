@@ -22,7 +22,12 @@ for cfg in (3, 2):
     rng = np.random.default_rng(0)
     v = torch.as_tensor(rng.standard_normal((1, M, L)) + 1j * rng.standard_normal((1, M, L))).cuda()
     out = torch.empty_like(v)
-    for name, fn in (("apply_T", lambda: op.apply_T(v, out)), ("schur", lambda: op(v, out))):
+    def tiled():
+        op.eng.set_k1_variant(1)
+        op.apply_T(v, out)
+        op.eng.set_k1_variant(0)
+    for name, fn in (("apply_T", lambda: op.apply_T(v, out)), ("schur", lambda: op(v, out)),
+                     ("apply_T_tiled", tiled)):
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
