@@ -76,6 +76,8 @@ struct ArgsS {
   const double* centers;   // [M][2]
   const double2* bw;       // [M * ncp][L] bloch-weighted beta per source image
   const double* bws;       // [M * ncp][L] re + im of bw (Karatsuba operand)
+  const double2* bwr;      // (-1)^(n-P) bw: coefficients of the reverse apply
+  const double* bwsr;      // (-1)^(n-P) bws
   double2* apart;          // [G][maxseg][kTT][L]  forward parts, one per (CTA, block row)
   double2* bpart;          // [NB][kTT][L]         reverse parts, one per cross block
   int M, T, NB, copies, ncp, maxseg;
@@ -97,6 +99,16 @@ __device__ __forceinline__ void block_ab(long long k, int T, int& A, int& B) {
   while (a < T - 1 && tri_off(a + 1, T) <= k) ++a;
   A = a;
   B = a + (int)(k - tri_off(a, T));
+}
+
+// Shared-memory layout of a batch: element (row (m, j), slot) at
+//   j * SJ + slot * kTT + (m ^ sw(slot)),   sw(slot) = 4 * ((slot / BO) & 1).
+// The xor swizzle makes the two row blocks b, b+1 read by one quarter-warp
+// land in opposite bank halves, so both consumer access patterns (forward
+// rows (w, s), reverse rows (s, w)) are conflict-free with odd SJ.
+template <int BO>
+__host__ __device__ __forceinline__ int sw_of(int slot) {
+  return 4 * ((slot / BO) & 1);
 }
 
 template <int P>
@@ -121,52 +133,54 @@ __device__ __forceinline__ void produce_s(const ArgsS& a, int A, int B, int li, 
   int N = live ? miller_start_j01(z) : 2;
   N = __reduce_max_sync(0xffffffffu, N);
   const double inv = live ? 1.0 / rho : 0.0;
-  // row (m, j) at  j * SJ + slot * 8 + m
-  double2* base = sym + (size_t)jt * S::SJ + (S::FP + 2 * P) * kTT + mt;
+  double2* base = sym + (size_t)jt * S::SJ;
   hankel_symbols_half<2 * P>(z, dx * inv, dy * inv, N, mirror, [&](int nu, double re, double im) {
     if (nu == 0 && !live) re = im = 0.0;
-    base[nu * kTT] = make_double2(re, im);
+    const int slot = S::FP + 2 * P + nu;
+    base[slot * kTT + (mt ^ sw_of<S::BO>(slot))] = make_double2(re, im);
   });
 }
 
-// One Toeplitz sweep with Karatsuba (3-multiplication) complex products:
-// rows at sp0 + slot*kTT (slot of nu = n - r), coefficients from global
-// (sign-flipped on odd order n for the reverse apply).  For b = beta[n] and
-// t = t_{n-r}:
-//   S1 += b.x t.x,  S2 += b.y t.y,  S3 += (b.x + b.y)(t.x + t.y)
+// One Toeplitz sweep with Karatsuba (3-multiplication) complex products.
+// spe / spo: the lane's symbol row at slot R0 - b*BO for the two swizzle
+// phases (the phase of slot R0 - b*BO + t is the parity of (R0+t)/BO - b, so
+// it is fixed at compile time per step t once b's parity is folded into
+// spe / spo).  For c = coef[n] and t = t_{n-r}:
+//   S1 += c.x t.x,  S2 += c.y t.y,  S3 += (c.x + c.y)(t.x + t.y)
 //   Re = S1 - S2,   Im = S3 - S1 - S2
 // so a complex MAC costs 3 DFMA instead of 4; t.x + t.y is formed once per
 // symbol as it enters the register window (1 DADD per step, shared by the
-// BO rows) and b.x + b.y is precomputed per source (bws).
-template <int P, bool REV>
-__device__ __forceinline__ void consume_s(const double2* __restrict__ rowbase,
+// BO rows) and c.x + c.y is precomputed per source (bws / bwsr).
+template <int P>
+__device__ __forceinline__ void consume_s(const double2* __restrict__ spe,
+                                          const double2* __restrict__ spo,
                                           const double2* __restrict__ bsrc,
                                           const double* __restrict__ ssrc,
-                                          double (&acc)[3][ShapeS<P>::BO], int b) {
+                                          double (&acc)[3][ShapeS<P>::BO]) {
   using S = ShapeS<P>;
   constexpr int BO = S::BO;
   constexpr int R0 = S::FP + 2 * P;
   constexpr int MODB = 64 * BO;
-  const double2* sp = rowbase + (size_t)(R0 - b * BO) * kTT;
+  auto ld = [&](auto t_c) -> double2 {
+    constexpr int t = decltype(t_c)::value;
+    constexpr bool odd = ((R0 + t) / BO) & 1;
+    return (odd ? spo : spe)[t * kTT];
+  };
   double wx[BO], wy[BO], ws[BO];
-#pragma unroll
-  for (int i = 0; i < BO; ++i) {
-    const double2 t = sp[-i * kTT];
-    const int q = (R0 - i + MODB) % BO;
+  static_for<BO>([&](auto i_c) {
+    constexpr int i = decltype(i_c)::value;
+    const double2 t = ld(IC<-i>{});
+    constexpr int q = (R0 - i + MODB) % BO;
     wx[q] = t.x;
     wy[q] = t.y;
     ws[q] = t.x + t.y;
-  }
+  });
   auto step = [&](auto n_c) {
     constexpr int n = decltype(n_c)::value;
     constexpr int u = n % BO;
-    const double2 nxt = sp[(n + 1) * kTT];
-    double2 bb = __ldg(bsrc + n);
-    double bs = __ldg(ssrc + n);
-    if (REV && ((n - P) & 1)) {                                  // (-1)^{order n}
-      bb = make_double2(-bb.x, -bb.y);
-      bs = -bs;
-    }
+    const double2 nxt = ld(IC<n + 1>{});
+    const double2 bb = __ldg(bsrc + n);
+    const double bs = __ldg(ssrc + n);
 #pragma unroll
     for (int i = 0; i < BO; ++i) acc[0][i] = fma(bb.x, wx[(R0 + u - i + MODB) % BO], acc[0][i]);
 #pragma unroll
@@ -181,67 +195,51 @@ __device__ __forceinline__ void consume_s(const double2* __restrict__ rowbase,
   static_for<S::L>(step);
 }
 
-// Reduce the Karatsuba partial sums of one sweep over the 8 source lanes s
-// (lane = b*8 + s) by recursive halving (xor 4, 2, 1: each level ships half
-// of the values, fixed order -> deterministic) and add them into the lane's
-// two persistent complex rows r0 = 8*s2 + 4*s1 + 2*s0, r0 + 1 of block b.
-// The accumulators are cleared for the next sweep.
-template <int BO>
-__device__ __forceinline__ void reduce_keep(double (&acc)[3][BO], double2 (&keep)[2], int s) {
-  static_assert(BO <= 16, "two rows per lane");
+// Flush one persistent accumulator set: reduce the Karatsuba sums over the 4
+// source lanes s' of a row block (lane bits 0-1; xor 2 then xor 1, each
+// level ships half the values -> fixed order, deterministic), then lane s'
+// writes rows r0..r0+3 of block b, r0 = 8*bit1 + 4*bit0, as complex values
+// (sign_rows: times (-1)^{m'}, reverse parts).  mask: the half-warp whose
+// lanes flush together.  The accumulators are cleared.
+template <int P>
+__device__ __forceinline__ void flush_s(double (&acc)[3][ShapeS<P>::BO], double2* dst, int b,
+                                        int sl, bool sign_rows, unsigned mask) {
+  using S = ShapeS<P>;
+  constexpr int BO = S::BO;
+  static_assert(BO <= 16, "four rows per lane");
   auto V = [&](int idx) -> double {           // idx = 3*row + component (row < 16)
     const int r = idx / 3, c = idx % 3;
     return r < BO ? acc[c][r] : 0.0;
   };
-  const bool h4 = s & 4, h2 = s & 2, h1 = s & 1;
+  const bool h2 = sl & 2, h1 = sl & 1;
   double v1[24];
 #pragma unroll
   for (int k = 0; k < 24; ++k) {
     const double lo = V(k), hi = V(24 + k);
-    const double send = h4 ? lo : hi;
-    v1[k] = (h4 ? hi : lo) + __shfl_xor_sync(0xffffffffu, send, 4);
+    const double send = h2 ? lo : hi;
+    v1[k] = (h2 ? hi : lo) + __shfl_xor_sync(mask, send, 2);
   }
   double v2[12];
 #pragma unroll
   for (int k = 0; k < 12; ++k) {
-    const double send = h2 ? v1[k] : v1[12 + k];
-    v2[k] = (h2 ? v1[12 + k] : v1[k]) + __shfl_xor_sync(0xffffffffu, send, 2);
+    const double send = h1 ? v1[k] : v1[12 + k];
+    v2[k] = (h1 ? v1[12 + k] : v1[k]) + __shfl_xor_sync(mask, send, 1);
   }
-  double v3[6];
+  const int r0 = 8 * (h2 ? 1 : 0) + 4 * (h1 ? 1 : 0);
 #pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    const double send = h1 ? v2[k] : v2[6 + k];
-    v3[k] = (h1 ? v2[6 + k] : v2[k]) + __shfl_xor_sync(0xffffffffu, send, 1);
-  }
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const double s1 = v3[3 * k], s2 = v3[3 * k + 1], s3 = v3[3 * k + 2];
-    keep[k].x += s1 - s2;
-    keep[k].y += s3 - s1 - s2;
+  for (int k = 0; k < 4; ++k) {
+    const int i = r0 + k, r = b * BO + i;
+    if (i < BO && r < S::L) {
+      const double s1 = v2[3 * k], s2 = v2[3 * k + 1], s3 = v2[3 * k + 2];
+      double2 v = make_double2(s1 - s2, s3 - s1 - s2);
+      if (sign_rows && ((r - P) & 1)) v = make_double2(-v.x, -v.y);
+      dst[r] = v;
+    }
   }
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
     for (int i = 0; i < BO; ++i) acc[c][i] = 0.0;
-}
-
-// write the lane's two persistent rows of block b, then clear them.
-// sign_rows: multiply row m' by (-1)^{m'} (reverse parts).
-template <int P>
-__device__ __forceinline__ void write_keep(double2 (&keep)[2], double2* dst, int b, int s,
-                                          bool sign_rows) {
-  using S = ShapeS<P>;
-  const int r0 = 8 * ((s >> 2) & 1) + 4 * ((s >> 1) & 1) + 2 * (s & 1);
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int i = r0 + k, r = b * S::BO + i;
-    if (i < S::BO && r < S::L) {
-      double2 v = keep[k];
-      if (sign_rows && ((r - P) & 1)) v = make_double2(-v.x, -v.y);
-      dst[r] = v;
-    }
-    keep[k] = make_double2(0.0, 0.0);
-  }
 }
 
 template <int P>
@@ -266,7 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
     const int r2 = r % (kTT * (S::FP + 1));
     const int q = r2 / kTT, mt = r2 % kTT;
     const int slot = q < S::FP ? q : S::FP + S::NS;
-    (buf ? sym1 : sym0)[(size_t)jt * S::SJ + (size_t)slot * kTT + mt] = make_double2(0.0, 0.0);
+    (buf ? sym1 : sym0)[(size_t)jt * S::SJ + (size_t)slot * kTT + (mt ^ sw_of<S::BO>(slot))] =
+        make_double2(0.0, 0.0);
   }
   __syncthreads();
 
@@ -295,42 +294,46 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
   __syncthreads();
 
-  // warp w owns target A*8+w (forward, keepA) and B*8+w (reverse, keepB);
-  // lane (b, s) covers rows [b*BO, b*BO+BO) and source slot s of the batch.
-  // One Karatsuba accumulator set is live per sweep; after each sweep it is
-  // reduced over s into the lane's two persistent rows.
-  const int b = lane / kTT, s = lane % kTT;
+  // Half-warp roles: lanes 0-15 apply the forward rows of target A*8+w,
+  // lanes 16-31 the reverse rows of target B*8+w; lane (b, s') covers row
+  // block b against source slots s' and s'+4 (two passes per batch).  Each
+  // lane keeps ONE persistent accumulator set (forward: whole block row,
+  // reverse: one block), so nothing is reduced per sweep.
+  const int h = lane >> 4, b = (lane >> 2) & 3, sl = lane & 3;
+  const unsigned hmask = h ? 0xffff0000u : 0x0000ffffu;
   double acc[3][BO];
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
     for (int i = 0; i < BO; ++i) acc[c][i] = 0.0;
-  double2 keepA[2], keepB[2];
-  keepA[0] = keepA[1] = keepB[0] = keepB[1] = make_double2(0.0, 0.0);
+  const double2* cw = h ? a.bwr : a.bw;
+  const double* cs = h ? a.bwsr : a.bws;
+  constexpr int R0 = S::FP + 2 * P;
+  const int sw_e = 4 * (b & 1), sw_o = 4 * ((b & 1) ^ 1);
   int A, B;
   block_ab(k0, a.T, A, B);
   const int A0 = A;
   long long blk = k0;
   int li = 0;
   for (int it = 0; it < nbat; ++it) {
-    double2* symc = (it & 1) ? sym1 : sym0;
-    const int l = li - a.copies;
-    // forward: target m = A*8 + w, source image (j = B*8 + s, l): row (m=w, j=s)
-    {
-      const int j = min(B * kTT + s, a.M - 1);            // dead rows are zero
-      const size_t g = ((size_t)j * a.ncp + li) * L;
-      consume_s<P, false>(symc + (size_t)s * S::SJ + warp, a.bw + g, a.bws + g, acc, b);
-      reduce_keep<BO>(acc, keepA, s);
-    }
-    // reverse: target j = B*8 + w, source image (m = A*8 + s, -l): row (m=s, j=w)
-    if (A != B) {
-      const int m = min(A * kTT + s, a.M - 1);
-      const size_t g = ((size_t)m * a.ncp + (a.copies - l)) * L;
-      consume_s<P, true>(symc + (size_t)warp * S::SJ + s, a.bw + g, a.bws + g, acc, b);
-      reduce_keep<BO>(acc, keepB, s);
+    const double2* symc = (it & 1) ? sym1 : sym0;
+    if (h == 0 || A != B) {
+      // forward: row (m = w, j = s), source j = B*8+s image li
+      // reverse: row (m = s, j = w), source m = A*8+s image 2c - li
+      const int img = h ? 2 * a.copies - li : li;
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        const int s = sl + 4 * pass;
+        const int jj = h ? warp : s, mm = h ? s : warp;
+        const int src = min((h ? A : B) * kTT + s, a.M - 1);   // dead rows are zero
+        const double2* rowp = symc + (size_t)jj * S::SJ + (size_t)(R0 - b * BO) * kTT;
+        const size_t g = ((size_t)src * a.ncp + img) * L;
+        consume_s<P>(rowp + (mm ^ sw_e), rowp + (mm ^ sw_o), cw + g, cs + g, acc);
+      }
     }
     if (li == a.ncp - 1) {                     // block complete
-      if (A != B) write_keep<P>(keepB, a.bpart + ((size_t)blk * kTT + warp) * L, b, s, true);
+      const bool cross = A != B;
+      const long long bdone = blk;
       ++blk;
       li = 0;
       const int Aold = A;
@@ -338,10 +341,12 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
         ++A;
         B = A;
       }
-      if (A != Aold || it + 1 == nbat)         // block row finished (or CTA done)
-        write_keep<P>(keepA,
-                      a.apart + (((size_t)blockIdx.x * a.maxseg + (Aold - A0)) * kTT + warp) * L,
-                      b, s, false);
+      if (h) {
+        if (cross) flush_s<P>(acc, a.bpart + ((size_t)bdone * kTT + warp) * L, b, sl, true, hmask);
+      } else if (A != Aold || it + 1 == nbat) {   // block row finished (or CTA done)
+        flush_s<P>(acc, a.apart + (((size_t)blockIdx.x * a.maxseg + (Aold - A0)) * kTT + warp) * L,
+                   b, sl, false, hmask);
+      }
     } else {
       ++li;
     }
@@ -352,7 +357,8 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
 // bw[g][n] = bloch^{l(g)} beta[j(g)][n]
 __global__ void bloch_weight_1(const double2* __restrict__ beta, const double2* __restrict__ bpow,
                                int M, int L, int ncp, double2* __restrict__ bw,
-                               double* __restrict__ bws) {
+                               double* __restrict__ bws, double2* __restrict__ bwr,
+                               double* __restrict__ bwsr) {
   const long long total = (long long)M * ncp * L;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -364,6 +370,9 @@ __global__ void bloch_weight_1(const double2* __restrict__ beta, const double2* 
     const double2 v = make_double2(fma(bv.x, wv.x, -bv.y * wv.y), fma(bv.x, wv.y, bv.y * wv.x));
     bw[i] = v;
     bws[i] = v.x + v.y;
+    const bool odd = (n - (L - 1) / 2) & 1;                  // (-1)^{order n}
+    bwr[i] = odd ? make_double2(-v.x, -v.y) : v;
+    bwsr[i] = odd ? -(v.x + v.y) : v.x + v.y;
   }
 }
 
@@ -459,20 +468,25 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   const size_t nbp = (size_t)a.NB * kTT * S::L;
   const size_t npart = na + nbp;
   const size_t nbw = (size_t)ctx->M * a.ncp * S::L;
-  if (ctx->partial_elems < npart + nbw + nbw) {
+  if (ctx->partial_elems < npart + 4 * nbw) {
     if (ctx->d_partial) cudaFree(ctx->d_partial);
     ctx->d_partial = nullptr;
     ctx->partial_elems = 0;
-    PS_CUDA_TRY(ctx, cudaMalloc(&ctx->d_partial, (npart + nbw + nbw) * sizeof(double2)));
-    ctx->partial_elems = npart + nbw + nbw;
+    PS_CUDA_TRY(ctx, cudaMalloc(&ctx->d_partial, (npart + 4 * nbw) * sizeof(double2)));
+    ctx->partial_elems = npart + 4 * nbw;
   }
   a.apart = ctx->d_partial;
   a.bpart = ctx->d_partial + na;
   double2* bw = ctx->d_partial + npart;
   a.bw = bw;
-  a.bws = reinterpret_cast<double*>(bw + nbw);
-  bloch_weight_1<<<2 * ctx->sm_count, 256, 0, st>>>(beta, bpow - 1, ctx->M, S::L, a.ncp, bw,
-                                                    const_cast<double*>(a.bws));
+  double* bws = reinterpret_cast<double*>(bw + nbw);
+  double2* bwr = bw + 2 * nbw;
+  double* bwsr = reinterpret_cast<double*>(bw + 3 * nbw);
+  a.bws = bws;
+  a.bwr = bwr;
+  a.bwsr = bwsr;
+  bloch_weight_1<<<2 * ctx->sm_count, 256, 0, st>>>(beta, bpow - 1, ctx->M, S::L, a.ncp, bw, bws,
+                                                    bwr, bwsr);
   PS_CUDA_TRY(ctx, cudaGetLastError());
   static bool attr_done = false;
   if (!attr_done) {
