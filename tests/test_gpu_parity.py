@@ -70,6 +70,28 @@ def test_apply_T_small_orders(O, p, copies, M):
         assert rel(got, ref) <= MATVEC_TOL
 
 
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("p,copies,M", [(0, 1, 1), (1, 1, 2), (2, 0, 17), (3, 1, 9), (7, 2, 33),
+                                        (12, 1, 24), (20, 1, 41), (25, 1, 70)])
+def test_apply_T_small_orders_kernel_variants(O, variant, p, copies, M):
+    """Tiled K1 (1) and symmetric K1s (2) forced at every block size BO the
+    swizzled K1s layout sees (p = 0..25), ragged tiles, 0..2 image copies."""
+    import torch
+    from paper_1412_7466_b200.engine import Engine
+    rng = np.random.default_rng(1000 + p * 10 + M)
+    centers = np.column_stack([rng.uniform(-0.45, 0.45, M), rng.uniform(-0.4, 0.4, M)])
+    beta = _cplx(rng, (M, 2 * p + 1))
+    bloch = np.exp(-0.4j)
+    ref = O.apply_T(beta, centers, 9.0, p, bloch, 1.0, copies)
+    eng = Engine(0)
+    eng.set_geometry(centers, p, 9.0, 1.0, copies)
+    eng.set_bloch(np.array([bloch]))
+    eng.set_k1_variant(variant)
+    got = eng.apply_T(torch.as_tensor(beta[None]).cuda())[0].cpu().numpy()
+    eng.close()
+    assert rel(got, ref) <= MATVEC_TOL
+
+
 def test_apply_T_multi_rhs(O):
     from paper_1412_7466_b200 import multiscat
     pb = O.load_problem(1)
