@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
       // forward: row (m = w, j = s), source j = B*8+s image li
       // reverse: row (m = s, j = w), source m = A*8+s image 2c - li
       const int img = h ? 2 * a.copies - li : li;
-#pragma unroll 1
+#pragma unroll
       for (int pass = 0; pass < 2; ++pass) {
         const int s = sl + 4 * pass;
         const int jj = h ? warp : s, mm = h ? s : warp;

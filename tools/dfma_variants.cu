@@ -63,6 +63,27 @@ __global__ void mixed(double* out, int iters, int mode) {
   }
   if (s == 12345.678) out[0] = s;
 }
+
+// half-active warps: do DFMA instructions with 16 of 32 lanes predicated
+// off cost half the FP64 pipe time?  mode 0: all lanes, 1: lanes 0-15 only,
+// 2: even lanes only
+__global__ void halfwarp(double* out, int iters, int mode) {
+  const int lane = threadIdx.x & 31;
+  const bool on = mode == 0 || (mode == 1 && lane < 16) || (mode == 2 && !(lane & 1));
+  double x[16], wv[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { x[i] = threadIdx.x * 1e-3 + i; wv[i] = 0.999 + i * 1e-6; }
+  if (on) {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = fma(wv[i], 1e-7, x[i]);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += x[i];
+  if (s == 12345.678) out[0] = s;
+}
 template <typename K>
 void run(const char* name, K k, int blocks, int threads, double fl_per_iter_thread, int iters) {
   double* d; cudaMalloc(&d, 8);
@@ -80,6 +101,21 @@ void run(const char* name, K k, int blocks, int threads, double fl_per_iter_thre
 int main(int argc, char** argv) {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int it = 1 << 14;
+  if (argc > 1 && argv[1][0] == 'h') {
+    for (int mode = 0; mode < 3; ++mode) {
+      double* d; cudaMalloc(&d, 8);
+      cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+      halfwarp<<<sms * 4, 256>>>(d, 1024, mode);
+      float best = 1e30f;
+      for (int r = 0; r < 3; ++r) {
+        cudaEventRecord(e0); halfwarp<<<sms * 4, 256>>>(d, it, mode); cudaEventRecord(e1); cudaEventSynchronize(e1);
+        float t; cudaEventElapsedTime(&t, e0, e1); if (t < best) best = t;
+      }
+      printf("halfwarp mode=%d  %.3f ms (same warp-instruction count in every mode)\n", mode, best);
+      cudaFree(d);
+    }
+    return 0;
+  }
   if (argc > 1 && argv[1][0] == 'm') {
     // per-warp flops per iteration: DFMA warp 32 thr x 16 fma x 2; DMMA warp 8/8 iters x 8 mma x 512
     for (int thr : {256, 512, 1024}) {
