@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mma_kernel(ArgsD a) {
       const double2* bw1 = a.bw + ((size_t)min(rb + 8, a.nrhs - 1) * a.nimg + g) * L;
       const bool ok0 = rb < a.nrhs, ok1 = rb + 8 < a.nrhs;
       const double2* rowb = symc + (size_t)s * kTT * S::NSP + S::OFF;
-#pragma unroll 1
+#pragma unroll
       for (int kt = 0; kt < S::KT; ++kt) {
         const int n = kt * 4 + fc;
         double2 b0 = make_double2(0.0, 0.0), b1 = b0;
