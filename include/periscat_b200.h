@@ -104,6 +104,12 @@ int ps_set_k1_variant(ps_ctx* ctx, int variant);
 /* Multi-RHS M2L kernel choice: 0 auto (FP64 tensor cores, mma.sync f64, for
  * >= 12 RHS; DFMA K1m below), 1 force DFMA K1m, 2 force DMMA K1d. */
 int ps_set_mrhs_variant(ps_ctx* ctx, int variant);
+/* SM partitioning of ps_apply_schur for one RHS with the symmetric M2L and
+ * pre-assembled coupling blocks: the M2L runs on (SM count - sms) CTAs in a
+ * high-priority stream while the HBM-bound C -> A^+ -> B chain streams on the
+ * other SMs (sms = 0: only the M2L tail is shared); sms < 0 runs them back
+ * to back.  Default 2 (best at cfg3). */
+int ps_set_overlap(ps_ctx* ctx, int sms);
 /* 1 if the pre-assembled coupling blocks are in use, 0 if matrix-free. */
 int ps_coupling_mode(const ps_ctx* ctx);
 

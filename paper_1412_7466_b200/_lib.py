@@ -49,6 +49,7 @@ SIGNATURES = {
     "ps_coupling_mode": (_I, [_P]),
     "ps_set_k1_variant": (_I, [_P, _I]),
     "ps_set_mrhs_variant": (_I, [_P, _I]),
+    "ps_set_overlap": (_I, [_P, _I]),
     "ps_stats": (_I, [_P, ctypes.POINTER(ctypes.c_longlong), _DP, ctypes.POINTER(ctypes.c_longlong)]),
     "ps_stats_reset": (_I, [_P]),
 }

@@ -86,6 +86,11 @@ void ps_destroy(ps_ctx* h) {
   }
   ps::release_dense_coupling(c);
   ps::gmres_release(c);
+  if (c->s_hi) cudaStreamDestroy(c->s_hi);
+  if (c->s_lo) cudaStreamDestroy(c->s_lo);
+  cudaEvent_t evs[] = {c->ev_fork, c->ev_k1, c->ev_cpl};
+  for (cudaEvent_t e : evs)
+    if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -451,6 +456,12 @@ int ps_set_mrhs_variant(ps_ctx* h, int variant) {
     return PS_ERR_ARG;
   }
   c->mrhs_variant = variant;
+  return PS_OK;
+}
+
+int ps_set_overlap(ps_ctx* h, int sms) {
+  if (!h) return PS_ERR_ARG;
+  C(h)->overlap_sms = sms < 0 ? -1 : sms;
   return PS_OK;
 }
 

@@ -695,9 +695,40 @@ int apply_schur_g(Ctx* c, const double2* v, const double2* g, double2* y, cudaSt
   return PS_OK;
 }
 
+// One RHS, K1s, dense coupling blocks covering every source, diagonal S:
+// K1s on sm_count - overlap_sms CTAs (high-priority stream) runs concurrently
+// with the HBM-bound chain C -> A^+ -> B (low-priority stream, which gets
+// the SMs K1s leaves free); the deterministic K1s reduce joins both.
+static int schur_overlapped(Ctx* c, const double2* v, double2* y, cudaStream_t st) {
+  if (!c->s_hi) {
+    int lo = 0, hi = 0;
+    PS_CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    PS_CUDA_TRY(c, cudaStreamCreateWithPriority(&c->s_hi, cudaStreamNonBlocking, hi));
+    PS_CUDA_TRY(c, cudaStreamCreateWithPriority(&c->s_lo, cudaStreamNonBlocking, lo));
+    PS_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    PS_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_k1, cudaEventDisableTiming));
+    PS_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_cpl, cudaEventDisableTiming));
+  }
+  Work w;
+  if (int rc = work(c, 0, &w)) return rc;
+  PS_CUDA_TRY(c, cudaEventRecord(c->ev_fork, st));
+  PS_CUDA_TRY(c, cudaStreamWaitEvent(c->s_hi, c->ev_fork, 0));
+  PS_CUDA_TRY(c, cudaStreamWaitEvent(c->s_lo, c->ev_fork, 0));
+  SymOverlap ov{c->s_hi, c->sm_count - c->overlap_sms, c->ev_k1, c->ev_cpl};
+  // the coupling chain is enqueued first on the host but K1s' CTAs are
+  // dispatched first (stream priority); the reduce waits on ev_cpl
+  if (int rc = dense_apply_C(c, 0, v, w.gpart, w.g, c->s_lo)) return rc;
+  if (int rc = b_pinv(c, 0, w.g, &w, c->s_lo)) return rc;
+  PS_CUDA_TRY(c, cudaEventRecord(c->ev_cpl, c->s_lo));
+  return m2l_apply_sym(c, v, bpow_of(c, 0) + 1, y, 1, v, w.bsub, st, &ov);
+}
+
 int apply_schur(Ctx* c, const double2* v, double2* y, cudaStream_t st) {
   const bool coupled = c->have_layers && c->rhs[0].d_Uh;
   if (!coupled) return apply_schur_g(c, v, nullptr, y, st);
+  if (c->overlap_sms >= 0 && c->overlap_sms < c->sm_count && c->nrhs == 1 && c->s_diag &&
+      c->dense && c->dcs0 == 0 && c->dcs1 == c->M && m2l_sym_selected(c))
+    return schur_overlapped(c, v, y, st);
   const size_t in_stride = (size_t)c->M * c->L;
   const size_t out_stride = (size_t)(c->t_end - c->t_begin) * c->L;
   const int nrhs = c->nrhs;

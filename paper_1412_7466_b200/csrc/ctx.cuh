@@ -60,6 +60,12 @@ struct Ctx {
   int mrhs_variant = 0;     // 0 auto (K1d DMMA for >= 12 RHS), 1 DFMA K1m, 2 DMMA K1d
   int dense = 0;            // 1: apply C and B from the pre-assembled matrices
   int dcs0 = 0, dcs1 = 0;   // source range the stored C^T covers
+  // SM partitioning (1 RHS, K1s + dense coupling): K1s runs on sm_count -
+  // overlap_sms CTAs in a high-priority stream while the HBM-bound coupling
+  // chain streams on the remaining SMs in a low-priority stream
+  int overlap_sms = 2;      // < 0: serial (swept with tools/probe_k1.py: 2 is best at cfg3)
+  cudaStream_t s_hi = nullptr, s_lo = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_k1 = nullptr, ev_cpl = nullptr;
 
   // right-hand sides
   int nrhs = 1;

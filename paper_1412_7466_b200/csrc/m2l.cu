@@ -396,13 +396,17 @@ int launch_p(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
 
 int m2l_max_order() { return PS_M2L_MAX_P; }
 
-int m2l_apply_1(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
-                const double2* v_own, const double2* bsub, cudaStream_t st) {
+bool m2l_sym_selected(const Ctx* ctx) {
   const bool full = ctx->t_begin == 0 && ctx->t_end == ctx->M;
   // crossover measured with tools/probe_variant.py (Karatsuba K1 / K1s): the
   // symmetric kernel wins from M ~ 500 (4% at M = 1000), the tiled one below
   const bool sym = ctx->k1_variant == 2 || (ctx->k1_variant == 0 && full && ctx->M >= 512);
-  if (sym && full) return m2l_apply_sym(ctx, beta, bpow, out, mode, v_own, bsub, st);
+  return sym && full;
+}
+
+int m2l_apply_1(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
+                const double2* v_own, const double2* bsub, cudaStream_t st) {
+  if (m2l_sym_selected(ctx)) return m2l_apply_sym(ctx, beta, bpow, out, mode, v_own, bsub, st);
   return m2l_apply(ctx, beta, bpow, out, mode, v_own, bsub, st);
 }
 

@@ -10,6 +10,14 @@
   X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25)
 
 namespace ps {
+// K1s launched on its own stream with a reduced grid; the deterministic
+// reduce waits for both the M2L and the coupling chain (SM partitioning).
+struct SymOverlap {
+  cudaStream_t k1_stream;   // bloch weights + K1s
+  int grid;                 // CTAs for K1s
+  cudaEvent_t k1_done;      // recorded on k1_stream after K1s
+  cudaEvent_t cpl_done;     // coupling chain finished (recorded by the caller)
+};
 int m2l_max_order();
 // out: [nt][L] for the owned targets; see m2l.cu for the epilogue modes.
 int m2l_apply(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
@@ -19,7 +27,9 @@ int m2l_apply(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, 
 // One RHS, full target range: symmetric variant (m2l_sym.cu), same contract
 // as m2l_apply.
 int m2l_apply_sym(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
-                  const double2* v_own, const double2* bsub, cudaStream_t st);
+                  const double2* v_own, const double2* bsub, cudaStream_t st,
+                  const SymOverlap* ov = nullptr);
+bool m2l_sym_selected(const Ctx* ctx);
 // dispatch: K1s when ctx owns every target and k1_variant allows it, else K1
 int m2l_apply_1(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
                 const double2* v_own, const double2* bsub, cudaStream_t st);

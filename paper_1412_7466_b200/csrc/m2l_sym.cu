@@ -450,7 +450,8 @@ int max_rows_per_cta(int T, int NB, int G) {
 
 template <int P>
 int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
-             const double2* v_own, const double2* bsub, cudaStream_t st) {
+             const double2* v_own, const double2* bsub, cudaStream_t st, const SymOverlap* ov) {
+  cudaStream_t ks = ov ? ov->k1_stream : st;
   using S = ShapeS<P>;
   ArgsS a;
   a.centers = ctx->d_centers;
@@ -461,7 +462,7 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   a.ncp = 2 * ctx->copies + 1;
   a.period = ctx->period;
   a.k2 = ctx->k2;
-  int G = ctx->sm_count;
+  int G = ov ? ov->grid : ctx->sm_count;
   if (G > a.NB) G = a.NB;
   a.maxseg = max_rows_per_cta(a.T, a.NB, G);
   const size_t na = (size_t)G * a.maxseg * kTT * S::L;
@@ -485,7 +486,7 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   a.bws = bws;
   a.bwr = bwr;
   a.bwsr = bwsr;
-  bloch_weight_1<<<2 * ctx->sm_count, 256, 0, st>>>(beta, bpow - 1, ctx->M, S::L, a.ncp, bw, bws,
+  bloch_weight_1<<<2 * ctx->sm_count, 256, 0, ks>>>(beta, bpow - 1, ctx->M, S::L, a.ncp, bw, bws,
                                                     bwr, bwsr);
   PS_CUDA_TRY(ctx, cudaGetLastError());
   static bool attr_done = false;
@@ -498,15 +499,20 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   if (ctx->profile) {
     PS_CUDA_TRY(ctx, cudaEventCreate(&e0));
     PS_CUDA_TRY(ctx, cudaEventCreate(&e1));
-    PS_CUDA_TRY(ctx, cudaEventRecord(e0, st));
+    PS_CUDA_TRY(ctx, cudaEventRecord(e0, ks));
   }
-  m2l_sym_kernel<P><<<G, kThreads, S::SMEM, st>>>(a);
+  m2l_sym_kernel<P><<<G, kThreads, S::SMEM, ks>>>(a);
   PS_CUDA_TRY(ctx, cudaGetLastError());
   if (ctx->profile) {
-    PS_CUDA_TRY(ctx, cudaEventRecord(e1, st));
+    PS_CUDA_TRY(ctx, cudaEventRecord(e1, ks));
     ctx->k1_events.push_back({e0, e1});
   }
   const int n = ctx->M * S::L;
+  if (ov) {
+    PS_CUDA_TRY(ctx, cudaEventRecord(ov->k1_done, ks));
+    PS_CUDA_TRY(ctx, cudaStreamWaitEvent(st, ov->k1_done, 0));
+    PS_CUDA_TRY(ctx, cudaStreamWaitEvent(st, ov->cpl_done, 0));
+  }
   k1s_reduce<<<(n + 255) / 256, 256, 0, st>>>(a.apart, a.bpart, a.T, a.NB, G, a.maxseg, ctx->M,
                                               S::L, mode, v_own, ctx->d_S, bsub, out);
   PS_CUDA_TRY(ctx, cudaGetLastError());
@@ -517,11 +523,12 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
 }  // namespace
 
 int m2l_apply_sym(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
-                  const double2* v_own, const double2* bsub, cudaStream_t st) {
+                  const double2* v_own, const double2* bsub, cudaStream_t st,
+                  const SymOverlap* ov) {
   switch (ctx->p) {
 #define PS_CASE(P) \
   case P:          \
-    return launch_s<P>(ctx, beta, bpow, out, mode, v_own, bsub, st);
+    return launch_s<P>(ctx, beta, bpow, out, mode, v_own, bsub, st, ov);
     PS_M2L_ORDERS(PS_CASE)
 #undef PS_CASE
     default:

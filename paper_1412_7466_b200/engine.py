@@ -137,6 +137,10 @@ class Engine:
         """0 auto, 1 tiled K1, 2 symmetric K1s (see include/periscat_b200.h)."""
         self._check(self.lib.ps_set_k1_variant(self.ctx, int(variant)))
 
+    def set_overlap(self, sms: int):
+        """SMs left to the coupling chain while K1s runs (< 0: serial)."""
+        self._check(self.lib.ps_set_overlap(self.ctx, int(sms)))
+
     def set_mrhs_variant(self, variant: int):
         """0 auto, 1 DFMA K1m, 2 DMMA K1d (see include/periscat_b200.h)."""
         self._check(self.lib.ps_set_mrhs_variant(self.ctx, int(variant)))

@@ -263,6 +263,22 @@ def test_matvec_vs_golden(O, cfg, dense_gb):
     assert rel(op.rhs().cpu().numpy()[0][tids], z["rhs"]) <= MATVEC_TOL
 
 
+@pytest.mark.parametrize("sms", [-1, 0, 2, 8, 40])
+def test_schur_sm_partition_vs_golden(O, sms):
+    """K1s on a reduced grid overlapped with the coupling chain on the other
+    SMs (ps_set_overlap): same operator as the serial path and the golden."""
+    z = _golden(3)
+    pb, op = _operator(O, 3)
+    op.eng.set_overlap(sms)
+    v = torch.as_tensor(z["v"][None]).cuda()
+    tids = z["targets"]
+    sch = op(v).cpu().numpy()[0]
+    assert rel(sch[tids], z["schur"]) <= MATVEC_TOL
+    op.eng.set_overlap(-1)
+    ser = op(v).cpu().numpy()[0]
+    assert rel(sch, ser) <= 1e-13
+
+
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4])
 def test_solve_full_vs_golden(O, cfg):
     """Full device solve vs the oracle's solve (c, d <= 1e-9 rel, |dflux| <= 1e-9)."""

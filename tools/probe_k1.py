@@ -43,6 +43,19 @@ for cfg in (3, 2):
         fl = tr * 8 * L * L
         print(f"cfg{cfg} {name}: {t*1e3:.3f} ms  {tr/t:.3e} tr/s  {fl/t/1e12:.2f} TFLOP/s "
               f"({fl/t/1e12/tf.value*100:.1f}% of DFMA peak)", flush=True)
+    for X in (-1, 0, 2, 4, 6, 8):
+        op.eng.set_overlap(X)
+        for _ in range(3):
+            op(v, out)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            op(v, out)
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"cfg{cfg} schur overlap_sms={X}: {e0.elapsed_time(e1) / 20:.3f} ms", flush=True)
+    op.eng.set_overlap(8)
     t0 = time.perf_counter()
     sol = solver.solve_full(sysm, centers, p, radius=radius)
     print(f"cfg{cfg} full solve {time.perf_counter()-t0:.3f}s iters={sol.iterations} "
