@@ -20,11 +20,11 @@ namespace {
 template <typename T>
 int dev_upload(Ctx* c, T** dst, const T* src, size_t n) {
   if (*dst) {
-    cudaFree(*dst);
+    ps::dev_free(*dst);
     *dst = nullptr;
   }
   if (n == 0) return PS_OK;
-  PS_CUDA_TRY(c, cudaMalloc(reinterpret_cast<void**>(dst), n * sizeof(T)));
+  PS_CUDA_TRY(c, ps::dev_malloc(reinterpret_cast<void**>(dst), n * sizeof(T)));
   if (src) PS_CUDA_TRY(c, cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
   return PS_OK;
 }
@@ -78,11 +78,11 @@ void ps_destroy(ps_ctx* h) {
   void* ptrs[] = {c->d_centers, c->d_S, c->d_rot, c->d_g1, c->d_g2, c->d_w2, c->d_blochpow,
                   c->d_partial, c->d_work};
   for (void* p : ptrs)
-    if (p) cudaFree(p);
+    if (p) ps::dev_free(p);
   for (auto& r : c->rhs) {
     void* rp[] = {r.d_Uh, r.d_sinv, r.d_Vb, r.d_cscale, r.d_f};
     for (void* p : rp)
-      if (p) cudaFree(p);
+      if (p) ps::dev_free(p);
   }
   ps::release_dense_coupling(c);
   ps::gmres_release(c);
@@ -168,7 +168,7 @@ int ps_set_rhs_bloch(ps_ctx* h, int nrhs, const double* bloch) {
       auto& d = c->rhs[r];
       void* rp[] = {d.d_Uh, d.d_sinv, d.d_Vb, d.d_cscale, d.d_f};
       for (void* q : rp)
-        if (q) cudaFree(q);
+        if (q) ps::dev_free(q);
     }
   }
   c->rhs.resize(nrhs);
@@ -190,7 +190,7 @@ int ps_set_smatrix(ps_ctx* h, const double* S, int diagonal, const double* rot) 
   if (int rc = dev_upload(c, &c->d_S, reinterpret_cast<const double2*>(S), n)) return rc;
   if (!diagonal && rot) return dev_upload(c, &c->d_rot, rot, (size_t)c->M);
   if (c->d_rot) {
-    cudaFree(c->d_rot);
+    ps::dev_free(c->d_rot);
     c->d_rot = nullptr;
   }
   return PS_OK;

@@ -574,10 +574,10 @@ int work(Ctx* c, int r, Work* w) {
   const size_t per = work_stride(c);
   const size_t need = per * c->nrhs;
   if (c->work_elems < need) {
-    if (c->d_work) cudaFree(c->d_work);
+    if (c->d_work) ps::dev_free(c->d_work);
     c->d_work = nullptr;
     c->work_elems = 0;
-    PS_CUDA_TRY(c, cudaMalloc(&c->d_work, need * sizeof(double2)));
+    PS_CUDA_TRY(c, ps::dev_malloc(&c->d_work, need * sizeof(double2)));
     c->work_elems = need;
   }
   double2* b = c->d_work + per * r;

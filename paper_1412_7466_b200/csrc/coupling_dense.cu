@@ -328,8 +328,8 @@ int precompute_coupling(Ctx* c, double max_bytes) {
   c->dcs1 = c->t_end;
   for (int r = 0; r < c->nrhs; ++r) {
     auto& R = c->rhs[r];
-    PS_CUDA_TRY(c, cudaMalloc(&R.d_CT, ct * sizeof(double2) + 16));
-    PS_CUDA_TRY(c, cudaMalloc(&R.d_B, bb * sizeof(double2) + 16));
+    PS_CUDA_TRY(c, ps::dev_malloc(&R.d_CT, ct * sizeof(double2) + 16));
+    PS_CUDA_TRY(c, ps::dev_malloc(&R.d_B, bb * sizeof(double2) + 16));
     int rc = PS_OK;
     switch (c->p) {
 #define PS_CASE(P) \
@@ -351,8 +351,8 @@ int precompute_coupling(Ctx* c, double max_bytes) {
 
 void release_dense_coupling(Ctx* c) {
   for (auto& R : c->rhs) {
-    if (R.d_CT) cudaFree(R.d_CT);
-    if (R.d_B) cudaFree(R.d_B);
+    if (R.d_CT) ps::dev_free(R.d_CT);
+    if (R.d_B) ps::dev_free(R.d_B);
     R.d_CT = nullptr;
     R.d_B = nullptr;
   }

@@ -91,6 +91,39 @@ struct Ctx {
 
 inline Ctx* C(ps_ctx* h) { return reinterpret_cast<Ctx*>(h); }
 
+// Device memory of every context comes from the device's stream-ordered
+// default pool with a 4 GiB release threshold: freed blocks stay cached, so a
+// new context (e.g. each solve_full) reuses the previous one's coupling
+// blocks and Krylov basis instead of paying cudaMalloc/cudaFree of ~1 GB.
+// Allocation and free are rare (setup, growth, destroy) and fully
+// synchronise, so the non-blocking worker streams never race them.
+inline cudaError_t dev_malloc_raw(void** p, size_t bytes) {
+  static int pool_ready[64] = {0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 0 && dev < 64 && !pool_ready[dev]) {
+    cudaMemPool_t pool;
+    if ((e = cudaDeviceGetDefaultMemPool(&pool, dev)) != cudaSuccess) return e;
+    uint64_t thr = 4ull << 30;
+    if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr)) != cudaSuccess)
+      return e;
+    pool_ready[dev] = 1;
+  }
+  if ((e = cudaMallocAsync(p, bytes, 0)) != cudaSuccess) return e;
+  return cudaStreamSynchronize(0);
+}
+template <class T>
+inline cudaError_t dev_malloc(T** p, size_t bytes) {
+  return dev_malloc_raw(reinterpret_cast<void**>(p), bytes);
+}
+inline void dev_free(void* p) {
+  if (!p) return;
+  cudaDeviceSynchronize();
+  cudaFreeAsync(p, 0);
+  cudaStreamSynchronize(0);
+}
+
 }  // namespace ps
 
 #define PS_CUDA_TRY(ctx, call)                                                 \

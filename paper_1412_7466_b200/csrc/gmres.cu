@@ -22,7 +22,7 @@ namespace ps {
 namespace {
 
 constexpr int kDotThreads = 256;
-constexpr int kChunk = 16384;   // elements per partial-sum CTA
+constexpr int kChunk = 2048;    // elements per partial-sum CTA (25 CTAs per Krylov vector at cfg3)
 
 __device__ __forceinline__ double2 cfma_conj(double2 a, double2 b, double2 c) {
   // c + conj(a) * b
@@ -277,17 +277,17 @@ static int scratch(Ctx* c, size_t bytes, void** out) {
   for (auto& e : g_scratch)
     if (e.first == c) {
       if (e.second.bytes < bytes) {
-        cudaFree(e.second.p);
+        ps::dev_free(e.second.p);
         e.second.p = nullptr;
         e.second.bytes = 0;
-        PS_CUDA_TRY(c, cudaMalloc(&e.second.p, bytes));
+        PS_CUDA_TRY(c, ps::dev_malloc(&e.second.p, bytes));
         e.second.bytes = bytes;
       }
       *out = e.second.p;
       return PS_OK;
     }
   Scratch s;
-  PS_CUDA_TRY(c, cudaMalloc(&s.p, bytes));
+  PS_CUDA_TRY(c, ps::dev_malloc(&s.p, bytes));
   s.bytes = bytes;
   g_scratch.push_back({c, s});
   *out = s.p;
@@ -297,7 +297,7 @@ static int scratch(Ctx* c, size_t bytes, void** out) {
 void gmres_release(Ctx* c) {
   for (size_t i = 0; i < g_scratch.size(); ++i)
     if (g_scratch[i].first == c) {
-      cudaFree(g_scratch[i].second.p);
+      ps::dev_free(g_scratch[i].second.p);
       g_scratch.erase(g_scratch.begin() + i);
       return;
     }

@@ -359,10 +359,10 @@ int launch_p(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   a.maxseg = (int)((a.W / G + 1) / a.nbatch) + 2;
   const size_t need = (size_t)G * a.maxseg * kTT * S::L;
   if (ctx->partial_elems < need) {
-    if (ctx->d_partial) cudaFree(ctx->d_partial);
+    if (ctx->d_partial) ps::dev_free(ctx->d_partial);
     ctx->d_partial = nullptr;
     ctx->partial_elems = 0;
-    PS_CUDA_TRY(ctx, cudaMalloc(&ctx->d_partial, need * sizeof(double2)));
+    PS_CUDA_TRY(ctx, ps::dev_malloc(&ctx->d_partial, need * sizeof(double2)));
     ctx->partial_elems = need;
   }
   a.partial = ctx->d_partial;

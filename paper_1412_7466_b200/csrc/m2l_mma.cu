@@ -336,10 +336,10 @@ int launch_d(Ctx* ctx, const double2* beta, double2* out, int mode, const double
   const size_t need_p = (size_t)G * a.maxseg * kRG * kTT * S::L;
   const size_t need = need_p + (size_t)total;
   if (ctx->partial_elems < need) {
-    if (ctx->d_partial) cudaFree(ctx->d_partial);
+    if (ctx->d_partial) ps::dev_free(ctx->d_partial);
     ctx->d_partial = nullptr;
     ctx->partial_elems = 0;
-    PS_CUDA_TRY(ctx, cudaMalloc(&ctx->d_partial, need * sizeof(double2)));
+    PS_CUDA_TRY(ctx, ps::dev_malloc(&ctx->d_partial, need * sizeof(double2)));
     ctx->partial_elems = need;
   }
   a.partial = ctx->d_partial;

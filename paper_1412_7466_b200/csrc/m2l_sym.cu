@@ -470,10 +470,10 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   const size_t npart = na + nbp;
   const size_t nbw = (size_t)ctx->M * a.ncp * S::L;
   if (ctx->partial_elems < npart + 4 * nbw) {
-    if (ctx->d_partial) cudaFree(ctx->d_partial);
+    if (ctx->d_partial) ps::dev_free(ctx->d_partial);
     ctx->d_partial = nullptr;
     ctx->partial_elems = 0;
-    PS_CUDA_TRY(ctx, cudaMalloc(&ctx->d_partial, (npart + 4 * nbw) * sizeof(double2)));
+    PS_CUDA_TRY(ctx, ps::dev_malloc(&ctx->d_partial, (npart + 4 * nbw) * sizeof(double2)));
     ctx->partial_elems = npart + 4 * nbw;
   }
   a.apart = ctx->d_partial;
