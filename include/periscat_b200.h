@@ -102,7 +102,8 @@ int ps_precompute_coupling(ps_ctx* ctx, double max_gb);
  * target, else tiled K1), 1 force tiled K1, 2 force K1s (full range only). */
 int ps_set_k1_variant(ps_ctx* ctx, int variant);
 /* Multi-RHS M2L kernel choice: 0 auto (FP64 tensor cores, mma.sync f64, for
- * >= 12 RHS; DFMA K1m below), 1 force DFMA K1m, 2 force DMMA K1d. */
+ * >= 12 RHS; below that one single-RHS launch per RHS), 1 force the DFMA
+ * multi-RHS K1m, 2 force DMMA K1d. */
 int ps_set_mrhs_variant(ps_ctx* ctx, int variant);
 /* SM partitioning of ps_apply_schur for one RHS with the symmetric M2L and
  * pre-assembled coupling blocks: the M2L runs on (SM count - sms) CTAs in a

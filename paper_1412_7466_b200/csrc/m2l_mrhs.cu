@@ -431,9 +431,23 @@ int launch_m(Ctx* ctx, const double2* beta, double2* out, int mode, const double
 
 int m2l_apply_mrhs(Ctx* ctx, const double2* beta, double2* out, int mode, const double2* bsub,
                    long long b_stride, cudaStream_t st) {
-  const bool mma = ctx->mrhs_variant == 2 || (ctx->mrhs_variant == 0 && ctx->nrhs >= 12);
-  if (mma) return m2l_apply_mma(ctx, beta, out, mode, bsub, b_stride, st);
-  return m2l_apply_mrhs_dfma(ctx, beta, out, mode, bsub, b_stride, st);
+  // K1d and K1m process RHS in groups of 16: below 12 RHS most of their
+  // MMA columns / consumer warps would idle, and the single-RHS kernels (K1s /
+  // K1 at ~80% of the DFMA peak, one launch per RHS) are faster
+  if (ctx->mrhs_variant == 2 || (ctx->mrhs_variant == 0 && ctx->nrhs >= 12))
+    return m2l_apply_mma(ctx, beta, out, mode, bsub, b_stride, st);
+  if (ctx->mrhs_variant == 1) return m2l_apply_mrhs_dfma(ctx, beta, out, mode, bsub, b_stride, st);
+  const size_t in_stride = (size_t)ctx->M * ctx->L;
+  const size_t out_stride = (size_t)(ctx->t_end - ctx->t_begin) * ctx->L;
+  const int np = 2 * ctx->copies + 3;
+  for (int r = 0; r < ctx->nrhs; ++r) {
+    const double2* br = beta + r * in_stride;
+    if (int rc = m2l_apply_1(ctx, br, ctx->d_blochpow + (size_t)r * np + 1, out + r * out_stride,
+                             mode, br + (size_t)ctx->t_begin * ctx->L,
+                             bsub ? bsub + r * b_stride : nullptr, st))
+      return rc;
+  }
+  return PS_OK;
 }
 
 int m2l_apply_mrhs_dfma(Ctx* ctx, const double2* beta, double2* out, int mode,
