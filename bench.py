@@ -40,12 +40,13 @@ UNIT = "translations/s"
 CFG = 3
 
 
-def _config_block(cfg_id, M, p, nrhs, world):
+def _config_block(cfg_id, M, p, nrhs, world, decomposition="targets"):
     return {"workload": f"cfg{cfg_id}: S-preconditioned Schur matvec, M={M} inclusions, p={p} "
                         f"(L={2 * p + 1}), {nrhs} RHS, 3-layer grating omega=10, "
                         "theta_ref=-7pi/10, P=1 near-field copies",
             "M": M, "p": p, "nrhs": nrhs, "translations_per_step": M * (3 * M - 1) * nrhs,
-            "parallelism": f"target-sharded x{world}",
+            "parallelism": (f"tile-pair-sharded x{world} (symmetric K1s + reduce-scatter)"
+                            if decomposition == "pairs" else f"target-sharded x{world}"),
             "coupling": "pre-assembled C^T / B_phys (device GEMVs)",
             "l2": "flushed (256 MiB write) before every timed step"}
 
@@ -209,7 +210,9 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     # one Schur matvec: N=1 -> the operator on the resident full vector;
     # N>1 -> parallel.ShardedSchur (NCCL all-gather of beta, C partial over own
-    # sources + all-reduce, own-target T/B/S) -- the path gmres_dist drives
+    # sources + all-reduce, own-target B/S; the M2L either over all sources for
+    # the own targets or, while M / N >= 200, the symmetric K1s over 1/N of the
+    # tile pairs + NCCL reduce-scatter) -- the path gmres_dist drives
     sharded = parallel.ShardedSchur(op) if world > 1 else None
 
     def step():
@@ -346,11 +349,13 @@ def run_ours(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "c128 (f64)", "data": "synthetic (seeded reference geometry fixture)",
-                "config": _config_block(CFG, M, p, 1, world),
+                "config": _config_block(CFG, M, p, 1, world,
+                                        sharded.mode if sharded is not None else "targets"),
                 "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value,
                              "unit": "TFLOP/s", "frac": achieved / peak.value,
                              "traffic": traffic,
-                             "kernel": "m2l_sym_kernel (K1s, symmetric single-RHS M2L)" if world == 1
+                             "kernel": "m2l_sym_kernel (K1s, symmetric single-RHS M2L)"
+                                       if world == 1 or sharded.mode == "pairs"
                                        else "m2l_kernel (K1, tiled; target shard)",
                              "k1_avg_ms": k1_avg_ms,
                              "algorithmic": "8(2p+1)^2 flops per translation",

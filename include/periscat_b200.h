@@ -120,6 +120,18 @@ int ps_coupling_mode(const ps_ctx* ctx);
  * excluded (multiscat.apply_T).  beta [nrhs][M][L] for ALL
  * inclusions; out [nrhs][t_end-t_begin][L] for the owned targets. */
 int ps_apply_T(ps_ctx* ctx, const void* beta_dev, void* out_dev, void* stream);
+/* Multi-GPU symmetric split (one RHS): the symmetric M2L over part `part` of
+ * `nparts` equal ranges of the unordered tile-pair list, for ALL M targets:
+ * out [M][L] holds this part's contributions (each pair's forward and
+ * reverse translations); summing the parts of all ranks (a reduce-scatter)
+ * gives apply_T.  beta: the full coefficient vector [M][L]. */
+int ps_apply_T_blocks(ps_ctx* ctx, int part, int nparts, const void* beta, void* out,
+                      void* stream);
+/* Epilogue of the split: y_own = v_own - S (a_own - B A^+ g) for the owned
+ * targets (solver.apply_schur_operator), given the summed
+ * M2L rows a_own and the all-reduced coupling rows g (NULL: uncoupled). */
+int ps_schur_finish(ps_ctx* ctx, const void* v_own, const void* a_own, const void* g, void* y,
+                    void* stream);
 
 /* g = C beta restricted to sources [s_begin, s_end): particle field values
  * and normal derivatives on Gamma1 (negated), Gamma2 and the telescoped L2

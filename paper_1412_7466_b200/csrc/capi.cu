@@ -306,6 +306,56 @@ int ps_apply_T(ps_ctx* h, const void* beta, void* out, void* stream) {
   return PS_OK;
 }
 
+int ps_apply_T_blocks(ps_ctx* h, int part, int nparts, const void* beta, void* out, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (c->p < 0) {
+    c->err = "ps_apply_T_blocks: geometry not set";
+    return PS_ERR_STATE;
+  }
+  if (!beta || !out || nparts < 1 || part < 0 || part >= nparts) {
+    c->err = "ps_apply_T_blocks: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (c->nrhs != 1) {
+    c->err = "ps_apply_T_blocks: one right-hand side only";
+    return PS_ERR_UNSUPPORTED;
+  }
+  if (int rc = set_device(c)) return rc;
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  c->sym_part = part;
+  c->sym_nparts = nparts;
+  const int rc = ps::m2l_apply_sym(c, reinterpret_cast<const double2*>(beta),
+                                   c->d_blochpow + 1, reinterpret_cast<double2*>(out), 0, nullptr,
+                                   nullptr, st);
+  c->sym_part = 0;
+  c->sym_nparts = 1;
+  return rc;
+}
+
+int ps_schur_finish(ps_ctx* h, const void* v_own, const void* a_own, const void* g, void* y,
+                    void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (c->p < 0 || c->rhs.empty()) {
+    c->err = "ps_schur_finish: operator not set up";
+    return PS_ERR_STATE;
+  }
+  if (!v_own || !a_own || !y) {
+    c->err = "ps_schur_finish: null pointer";
+    return PS_ERR_ARG;
+  }
+  if (c->nrhs != 1) {
+    c->err = "ps_schur_finish: one right-hand side only";
+    return PS_ERR_UNSUPPORTED;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::schur_finish(c, reinterpret_cast<const double2*>(v_own),
+                          reinterpret_cast<const double2*>(a_own),
+                          reinterpret_cast<const double2*>(g), reinterpret_cast<double2*>(y),
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
 int ps_apply_C(ps_ctx* h, const void* beta, void* g, int s_begin, int s_end, void* stream) {
   if (!h) return PS_ERR_ARG;
   Ctx* c = C(h);

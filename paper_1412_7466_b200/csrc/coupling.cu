@@ -695,6 +695,54 @@ int apply_schur_g(Ctx* c, const double2* v, const double2* g, double2* y, cudaSt
   return PS_OK;
 }
 
+__global__ void finish_diag(const double2* __restrict__ v, const double2* __restrict__ a,
+                            const double2* __restrict__ bsub, const double2* __restrict__ sd,
+                            int n, int L, double2* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2 u = a[i];
+  if (bsub) {
+    u.x -= bsub[i].x;
+    u.y -= bsub[i].y;
+  }
+  const double2 s = sd[i % L], vv = v[i];
+  y[i] = make_double2(vv.x - fma(s.x, u.x, -s.y * u.y), vv.y - fma(s.x, u.y, s.y * u.x));
+}
+
+__global__ void sub_rows(const double2* __restrict__ a, const double2* __restrict__ b, int n,
+                         double2* __restrict__ u) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  u[i] = b ? make_double2(a[i].x - b[i].x, a[i].y - b[i].y) : a[i];
+}
+
+// Epilogue of a Schur matvec whose M2L sums a_own arrived from elsewhere (the
+// multi-GPU symmetric split: partial K1s over a block range on every rank,
+// reduce-scattered): y = v_own - S (a_own - B A^+ g), one RHS.
+int schur_finish(Ctx* c, const double2* v_own, const double2* a_own, const double2* g,
+                 double2* y, cudaStream_t st) {
+  const bool coupled = c->have_layers && c->rhs[0].d_Uh && g;
+  Work w;
+  if (int rc = work(c, 0, &w)) return rc;
+  const double2* bsub = nullptr;
+  if (coupled) {
+    if (int rc = b_pinv(c, 0, g, &w, st)) return rc;
+    bsub = w.bsub;
+  }
+  const int n = (c->t_end - c->t_begin) * c->L;
+  if (n <= 0) return PS_OK;
+  if (c->s_diag) {
+    finish_diag<<<(n + 255) / 256, 256, 0, st>>>(v_own, a_own, bsub, c->d_S, n, c->L, y);
+    PS_CUDA_TRY(c, cudaGetLastError());
+    c->launches += 1;
+    return PS_OK;
+  }
+  sub_rows<<<(n + 255) / 256, 256, 0, st>>>(a_own, bsub, n, w.u);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  c->launches += 1;
+  return s_apply(c, v_own, w.u, y, st);
+}
+
 // One RHS, K1s, dense coupling blocks covering every source, diagonal S:
 // K1s on sm_count - overlap_sms CTAs (high-priority stream) runs concurrently
 // with the HBM-bound chain C -> A^+ -> B (low-priority stream, which gets

@@ -81,6 +81,7 @@ struct ArgsS {
   double2* apart;          // [G][maxseg][kTT][L]  forward parts, one per (CTA, block row)
   double2* bpart;          // [NB][kTT][L]         reverse parts, one per cross block
   int M, T, NB, copies, ncp, maxseg;
+  long long kb0, nb;       // block range [kb0, kb0 + nb) of this launch (multi-GPU part)
   double period, k2;
 };
 
@@ -249,8 +250,8 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
   extern __shared__ double2 smem[];
   double2* sym0 = smem;
   double2* sym1 = smem + S::SYM;
-  const long long k0 = ((long long)a.NB * blockIdx.x) / gridDim.x;
-  const long long k1 = ((long long)a.NB * (blockIdx.x + 1)) / gridDim.x;
+  const long long k0 = a.kb0 + (a.nb * blockIdx.x) / gridDim.x;
+  const long long k1 = a.kb0 + (a.nb * (blockIdx.x + 1)) / gridDim.x;
   if (k0 >= k1) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp >= kCW;
@@ -377,42 +378,51 @@ __global__ void bloch_weight_1(const double2* __restrict__ beta, const double2* 
 }
 
 // out[m][r] for tile X = m / 8, fixed order: reverse parts of the cross
-// blocks (A, X), A < X, then the forward parts of the CTAs covering block row X.
+// blocks (A, X), A < X, then the forward parts of the CTAs covering block row
+// X -- restricted to the launch's block range [kb0, kb0 + nb) (a multi-GPU
+// part; the other parts' contributions arrive through the reduce-scatter).
 __global__ void k1s_reduce(const double2* __restrict__ apart, const double2* __restrict__ bpart,
-                           int T, int NB, int G, int maxseg, int M, int L, int mode,
-                           const double2* __restrict__ v_own, const double2* __restrict__ sdiag,
-                           const double2* __restrict__ bsub, double2* __restrict__ out) {
+                           int T, long long kb0, long long nb, int G, int maxseg, int M, int L,
+                           int mode, const double2* __restrict__ v_own,
+                           const double2* __restrict__ sdiag, const double2* __restrict__ bsub,
+                           double2* __restrict__ out) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= M * L) return;
   const int m = idx / L, r = idx % L;
   const int X = m / kTT, w = m % kTT;
+  const long long kb1 = kb0 + nb;
   auto off = [&](int a) -> long long { return (long long)a * T - (long long)a * (a - 1) / 2; };
-  auto kbeg = [&](int c) -> long long { return ((long long)NB * c) / G; };
+  auto kbeg = [&](int c) -> long long { return kb0 + (nb * c) / G; };
   double2 sum = make_double2(0.0, 0.0);
   for (int A = 0; A < X; ++A) {
     const long long k = off(A) + (X - A);
+    if (k < kb0 || k >= kb1) continue;
     const double2 v = bpart[((size_t)k * kTT + w) * L + r];
     sum.x += v.x;
     sum.y += v.y;
   }
-  const long long ra = off(X), rb = off(X + 1);          // block range of row X
-  int c = (int)((ra * G) / NB);
-  if (c >= G) c = G - 1;
-  while (c > 0 && kbeg(c) > ra) --c;
-  while (c < G - 1 && kbeg(c + 1) <= ra) ++c;
-  for (; c < G; ++c) {
-    const long long c0 = kbeg(c), c1 = kbeg(c + 1);
-    if (c0 >= rb) break;
-    if (c1 <= c0 || c1 <= ra) continue;
-    // first block row of CTA c
-    int a0 = (int)(((2.0 * T + 1.0) - sqrt((2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * (double)c0)) * 0.5);
-    if (a0 < 0) a0 = 0;
-    if (a0 > T - 1) a0 = T - 1;
-    while (a0 > 0 && off(a0) > c0) --a0;
-    while (a0 < T - 1 && off(a0 + 1) <= c0) ++a0;
-    const double2 v = apart[(((size_t)c * maxseg + (X - a0)) * kTT + w) * L + r];
-    sum.x += v.x;
-    sum.y += v.y;
+  const long long ra = off(X) > kb0 ? off(X) : kb0;                 // in-range blocks of row X
+  const long long rb = off(X + 1) < kb1 ? off(X + 1) : kb1;
+  if (ra < rb) {
+    int c = (int)(((ra - kb0) * G) / nb);
+    if (c >= G) c = G - 1;
+    while (c > 0 && kbeg(c) > ra) --c;
+    while (c < G - 1 && kbeg(c + 1) <= ra) ++c;
+    for (; c < G; ++c) {
+      const long long c0 = kbeg(c), c1 = kbeg(c + 1);
+      if (c0 >= rb) break;
+      if (c1 <= c0 || c1 <= ra) continue;
+      // first block row of CTA c
+      int a0 = (int)(((2.0 * T + 1.0) - sqrt((2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * (double)c0)) *
+                     0.5);
+      if (a0 < 0) a0 = 0;
+      if (a0 > T - 1) a0 = T - 1;
+      while (a0 > 0 && off(a0) > c0) --a0;
+      while (a0 < T - 1 && off(a0 + 1) <= c0) ++a0;
+      const double2 v = apart[(((size_t)c * maxseg + (X - a0)) * kTT + w) * L + r];
+      sum.x += v.x;
+      sum.y += v.y;
+    }
   }
   if (mode == 0) {
     out[idx] = sum;
@@ -432,7 +442,7 @@ __global__ void k1s_reduce(const double2* __restrict__ apart, const double2* __r
 }
 
 // number of block rows a CTA's range touches (host, exact)
-int max_rows_per_cta(int T, int NB, int G) {
+int max_rows_per_cta(int T, long long kb0, long long nb, int G) {
   auto off = [&](long long a) { return a * T - a * (a - 1) / 2; };
   auto row_of = [&](long long k) {
     long long a = 0;
@@ -441,7 +451,7 @@ int max_rows_per_cta(int T, int NB, int G) {
   };
   int mx = 1;
   for (int c = 0; c < G; ++c) {
-    const long long k0 = ((long long)NB * c) / G, k1 = ((long long)NB * (c + 1)) / G;
+    const long long k0 = kb0 + (nb * c) / G, k1 = kb0 + (nb * (c + 1)) / G;
     if (k1 <= k0) continue;
     mx = std::max(mx, (int)(row_of(k1 - 1) - row_of(k0) + 1));
   }
@@ -462,9 +472,13 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   a.ncp = 2 * ctx->copies + 1;
   a.period = ctx->period;
   a.k2 = ctx->k2;
+  // multi-GPU part: this launch covers blocks [NB part / nparts, NB (part+1) / nparts)
+  a.kb0 = ((long long)a.NB * ctx->sym_part) / ctx->sym_nparts;
+  a.nb = ((long long)a.NB * (ctx->sym_part + 1)) / ctx->sym_nparts - a.kb0;
   int G = ov ? ov->grid : ctx->sm_count;
-  if (G > a.NB) G = a.NB;
-  a.maxseg = max_rows_per_cta(a.T, a.NB, G);
+  if (G > a.nb) G = (int)a.nb;
+  if (G < 1) G = 1;
+  a.maxseg = max_rows_per_cta(a.T, a.kb0, a.nb, G);
   const size_t na = (size_t)G * a.maxseg * kTT * S::L;
   const size_t nbp = (size_t)a.NB * kTT * S::L;
   const size_t npart = na + nbp;
@@ -513,7 +527,7 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
     PS_CUDA_TRY(ctx, cudaStreamWaitEvent(st, ov->k1_done, 0));
     PS_CUDA_TRY(ctx, cudaStreamWaitEvent(st, ov->cpl_done, 0));
   }
-  k1s_reduce<<<(n + 255) / 256, 256, 0, st>>>(a.apart, a.bpart, a.T, a.NB, G, a.maxseg, ctx->M,
+  k1s_reduce<<<(n + 255) / 256, 256, 0, st>>>(a.apart, a.bpart, a.T, a.kb0, a.nb, G, a.maxseg, ctx->M,
                                               S::L, mode, v_own, ctx->d_S, bsub, out);
   PS_CUDA_TRY(ctx, cudaGetLastError());
   ctx->launches += 3;

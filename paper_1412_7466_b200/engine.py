@@ -170,6 +170,29 @@ class Engine:
         self._check(self.lib.ps_apply_T(self.ctx, b, o, _stream(self.device)))
         return out
 
+    def apply_T_blocks(self, beta: torch.Tensor, part: int, nparts: int,
+                       out: torch.Tensor | None = None) -> torch.Tensor:
+        """This part's share of apply_T for ALL M targets (symmetric split;
+        one RHS).  Summing the parts over ranks gives apply_T."""
+        out = torch.empty((1, self.M, self.L), dtype=torch.complex128,
+                          device=self.device) if out is None else out
+        b = self._dev(beta, (1, self.M, self.L))
+        o = self._dev(out, (1, self.M, self.L))
+        self._check(self.lib.ps_apply_T_blocks(self.ctx, int(part), int(nparts), b, o,
+                                               _stream(self.device)))
+        return out
+
+    def schur_finish(self, v_own: torch.Tensor, a_own: torch.Tensor, g: torch.Tensor | None,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+        """y_own = v_own - S (a_own - B A^+ g) (one RHS)."""
+        out = self.empty_own() if out is None else out
+        v = self._dev(v_own, (1, self.n_own, self.L))
+        a = self._dev(a_own, (1, self.n_own, self.L))
+        gp = None if g is None else self._dev(g, (1, self.nrow_c))
+        o = self._dev(out, (1, self.n_own, self.L))
+        self._check(self.lib.ps_schur_finish(self.ctx, v, a, gp, o, _stream(self.device)))
+        return out
+
     def apply_C(self, beta: torch.Tensor, s_range=None, out=None) -> torch.Tensor:
         s0, s1 = (0, self.M) if s_range is None else s_range
         out = torch.empty((self.nrhs, self.nrow_c), dtype=torch.complex128,

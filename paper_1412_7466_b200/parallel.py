@@ -5,7 +5,9 @@ coefficient vector, of T, S and B, and their slices of the Krylov basis.
 Per Schur matvec:
   1. all-gather beta (NCCL over NVLink) -> full vector on every rank;
   2. partial g = C beta over the rank's own SOURCE inclusions, all-reduce;
-  3. local y = v_own - S (T v - B A^+ g)  (K1 over all sources, own targets).
+  3. local y = v_own - S (T v - B A^+ g): either K1 over all sources for the
+     own targets, or (one RHS) the symmetric K1s over 1/world of the tile
+     pairs for all targets followed by a reduce-scatter (ShardedSchur).
 GMRES dot products are local partial sums followed by an all-reduce; the
 Hessenberg least-squares bookkeeping (O(k) scalars) is replicated.
 
@@ -52,6 +54,35 @@ def all_gather_rows(v_own: torch.Tensor, M: int, group=None) -> torch.Tensor:
     return torch.view_as_complex(full.contiguous())
 
 
+def reduce_scatter_rows(x_full: torch.Tensor, M: int, group=None) -> torch.Tensor:
+    """[nrhs][M][L] partial sums on every rank -> this rank's rows
+    shard_range(M, rank, world) of the sum over ranks (NCCL reduce-scatter;
+    uneven shards are padded; gloo, which has no reduce-scatter here, sums
+    with an all-reduce and slices)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return x_full
+    rank = dist.get_rank(group)
+    t0, t1 = shard_range(M, rank, world)
+    xr = torch.view_as_real(x_full.contiguous())
+    if not x_full.is_cuda:
+        dist.all_reduce(xr, group=group)
+        return torch.view_as_complex(xr)[:, t0:t1].contiguous()
+    sizes = shard_sizes(M, world)
+    mx = max(sizes)
+    if len(set(sizes)) == 1:
+        inp = xr.reshape(xr.shape[0], world, mx, *xr.shape[2:]).transpose(0, 1).contiguous()
+    else:
+        inp = torch.zeros((world, xr.shape[0], mx) + tuple(xr.shape[2:]), dtype=xr.dtype,
+                          device=xr.device)
+        for r in range(world):
+            a, b = shard_range(M, r, world)
+            inp[r, :, :b - a] = xr[:, a:b]
+    out = torch.empty(inp.shape[1:], dtype=xr.dtype, device=xr.device)
+    dist.reduce_scatter_tensor(out, inp, group=group)
+    return torch.view_as_complex(out[:, :t1 - t0].contiguous())
+
+
 def all_reduce_(t: torch.Tensor, group=None) -> torch.Tensor:
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         if t.is_complex():
@@ -64,22 +95,55 @@ def all_reduce_(t: torch.Tensor, group=None) -> torch.Tensor:
 
 class ShardedSchur:
     """Distributed S-preconditioned Schur operator on top of a SchurOperator
-    whose engine owns targets shard_range(M, rank, world)."""
+    whose engine owns targets shard_range(M, rank, world).
 
-    def __init__(self, op, group=None):
+    Two decompositions of the M2L (both with the same all-gather of beta and
+    the same C / B coupling split):
+      * "targets": every rank runs the tiled K1 for its own targets over all
+        sources (no M2L exchange);
+      * "pairs" (one RHS, M >= 512 and M / world >= 200, the default there):
+        every rank runs the symmetric K1s over 1/world of the unordered tile
+        pairs -- each symbol row serves a pair and its reverse, half the
+        producer work of the tiled kernel -- for ALL targets, and a
+        reduce-scatter sums the parts into each rank's own rows
+        (ps_apply_T_blocks / ps_schur_finish).
+    """
+
+    def __init__(self, op, group=None, mode: str = "auto"):
         self.op = op
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.t0, self.t1 = shard_range(op.M, self.rank, self.world)
         self.s_range = (self.t0, self.t1)     # own sources for the C partial sum
+        if mode == "auto":
+            # measured per-rank compute at cfg3 (tools/probe_shard.py): pairs
+            # wins at 2 and 4 ranks (1.25 vs 1.34 ms, 0.70 vs 0.72 ms), the
+            # tiled target split at 8 (0.38 vs 0.40 ms: 125 targets per rank
+            # leave too few tile pairs per CTA) -> pairs while M / world >= 200
+            mode = "pairs" if (op.nrhs == 1 and self.world > 1 and op.M >= 512
+                               and op.M >= 200 * self.world) else "targets"
+        if mode not in ("pairs", "targets"):
+            raise ValueError(f"unknown decomposition {mode!r}")
+        self.mode = mode
+
+    def _coupling(self, v_full):
+        if not self.op.coupled:
+            return None
+        g = self.op.eng.apply_C(v_full, s_range=self.s_range)
+        all_reduce_(g, self.group)
+        return g
 
     def __call__(self, v_own: torch.Tensor, out=None) -> torch.Tensor:
         v_full = all_gather_rows(v_own, self.op.M, self.group)
-        if not self.op.coupled:
+        if self.mode == "pairs":
+            a_part = self.op.eng.apply_T_blocks(v_full, self.rank, self.world)
+            a_own = reduce_scatter_rows(a_part, self.op.M, self.group)
+            g = self._coupling(v_full)
+            return self.op.eng.schur_finish(v_own.contiguous(), a_own, g, out=out)
+        g = self._coupling(v_full)
+        if g is None:
             return self.op(v_full, out=out)
-        g = self.op.eng.apply_C(v_full, s_range=self.s_range)
-        all_reduce_(g, self.group)
         return self.op(v_full, out=out, g=g)
 
     def rhs(self) -> torch.Tensor:

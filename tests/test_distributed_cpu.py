@@ -50,6 +50,10 @@ def _body(rank, world, q):
     own = torch.as_tensor(b[:, t0:t1]).contiguous()
     full = parallel.all_gather_rows(own, M)
     assert np.array_equal(full.numpy(), b)
+    # reduce-scatter of full-length partials (the "pairs" decomposition)
+    part = torch.as_tensor(b * (rank + 1)).contiguous()
+    mine = parallel.reduce_scatter_rows(part, M)
+    assert np.allclose(mine.numpy(), (b * sum(range(1, world + 1)))[:, t0:t1])
     # complex all-reduce
     z = torch.tensor([1.0 + 2.0j * rank, -1.0j], dtype=torch.complex128)
     parallel.all_reduce_(z)

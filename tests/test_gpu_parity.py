@@ -408,3 +408,53 @@ def test_target_shards_reassemble(O, ranks):
     parts = [op(vd, g=g).cpu().numpy()[0] for op in ops]
     got = np.concatenate(parts, axis=0)
     assert rel(got, ref) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 3, 8])
+@pytest.mark.parametrize("p,M", [(25, 1000), (5, 40), (2, 9)])
+def test_apply_T_blocks_sum_to_apply_T(O, nparts, p, M):
+    """The symmetric split (ps_apply_T_blocks): the parts of the tile-pair list
+    sum to the full M2L for every target, including empty parts."""
+    from paper_1412_7466_b200 import grating
+    from paper_1412_7466_b200.engine import Engine
+    rng = np.random.default_rng(M + nparts)
+    if M == 1000:
+        centers = O.load_problem(3).centers
+    else:
+        centers = np.column_stack([rng.uniform(-0.45, 0.45, M), rng.uniform(-0.4, 0.4, M)])
+    beta = _cplx(rng, (1, M, 2 * p + 1))
+    eng = Engine(0)
+    eng.set_geometry(centers, p, 12.0, 1.0, 1)
+    eng.set_bloch(np.array([np.exp(0.3j)]))
+    vd = _dev(beta)
+    full = eng.apply_T(vd).cpu().numpy()
+    tot = sum(eng.apply_T_blocks(vd, r, nparts).cpu().numpy() for r in range(nparts))
+    eng.close()
+    assert rel(tot, full) <= 1e-13
+
+
+@pytest.mark.parametrize("ranks", [2, 3])
+def test_pair_split_shards_reassemble(O, ranks):
+    """The 'pairs' multi-GPU decomposition simulated rank by rank on this GPU:
+    partial K1s over each rank's tile-pair range for all targets, summed as
+    the reduce-scatter would, then each rank's epilogue (ps_schur_finish) with
+    the all-reduced coupling rows -- equals the oracle Schur matvec."""
+    from paper_1412_7466_b200 import grating, parallel, solver
+    pb = O.load_problem(2)
+    rng = np.random.default_rng(10 + ranks)
+    v = pb.smat[None, :] * _cplx(rng, (pb.M, pb.L))
+    ref = O.apply_schur_operator(pb, v).reshape(pb.M, pb.L)
+    sysm = grating.load_fixture("w10")
+    vd = _dev(v[None])
+    rngs = [parallel.shard_range(pb.M, r, ranks) for r in range(ranks)]
+    ops = [solver.SchurOperator(sysm, pb.centers, pb.p, smat=pb.smat, target_range=rngs[r])
+           for r in range(ranks)]
+    a_parts = [op.eng.apply_T_blocks(vd, r, ranks) for r, op in enumerate(ops)]
+    a_sum = sum(a_parts)
+    g = sum(op.eng.apply_C(vd, s_range=rngs[r]) for r, op in enumerate(ops))
+    got = []
+    for r, op in enumerate(ops):
+        t0, t1 = rngs[r]
+        y = op.eng.schur_finish(vd[:, t0:t1].contiguous(), a_sum[:, t0:t1].contiguous(), g)
+        got.append(y.cpu().numpy()[0])
+    assert rel(np.concatenate(got, axis=0), ref) <= MATVEC_TOL

@@ -56,6 +56,23 @@ def cfg3():
             del op
         base = base or ts[0]
         tr = M * (3 * M - 1)
+        if G > 1:   # "pairs" decomposition: K1s over 1/G of the tile pairs + epilogue
+            tp = []
+            for r in range(G):
+                t0, t1 = shard_range(M, r, G)
+                op = solver.SchurOperator(sysm, centers, p, radius=radius, target_range=(t0, t1))
+                a_full = torch.empty((1, M, L), dtype=torch.complex128, device="cuda")
+                y = torch.empty((1, t1 - t0, L), dtype=torch.complex128, device="cuda")
+                vo = v[:, t0:t1].contiguous()
+
+                def fp():
+                    op.eng.apply_T_blocks(v, r, G, out=a_full)
+                    g = op.eng.apply_C(v, s_range=(t0, t1))
+                    op.eng.schur_finish(vo, a_full[:, t0:t1].contiguous(), g, out=y)
+                tp.append(timed(fp, 20))
+                del op
+            print(f"cfg3 G={G} pairs: per-rank ms {['%.3f' % (t * 1e3) for t in tp]}  max "
+                  f"{max(tp)*1e3:.3f}  predicted compute speed-up {base / max(tp):.2f}x", flush=True)
         print(f"cfg3 G={G}: per-rank ms {['%.3f' % (t * 1e3) for t in ts]}  max {max(ts)*1e3:.3f}  "
               f"predicted compute speed-up {base / max(ts):.2f}x  ({tr / max(ts):.3e} tr/s)",
               flush=True)
