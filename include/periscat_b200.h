@@ -111,6 +111,11 @@ int ps_set_mrhs_variant(ps_ctx* ctx, int variant);
  * other SMs (sms = 0: only the M2L tail is shared); sms < 0 runs them back
  * to back.  Default 2 (best at cfg3). */
 int ps_set_overlap(ps_ctx* ctx, int sms);
+/* Single-RHS M2L launches (ps_apply_T, ps_apply_T_blocks) use SM count - sms
+ * CTAs, leaving SMs free for work the caller overlaps on other streams (the
+ * multi-GPU driver runs the coupling chain and its NCCL all-reduce there).
+ * Default 0. */
+int ps_set_k1_reserve(ps_ctx* ctx, int sms);
 /* 1 if the pre-assembled coupling blocks are in use, 0 if matrix-free. */
 int ps_coupling_mode(const ps_ctx* ctx);
 

@@ -509,6 +509,17 @@ int ps_set_mrhs_variant(ps_ctx* h, int variant) {
   return PS_OK;
 }
 
+int ps_set_k1_reserve(ps_ctx* h, int sms) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (sms < 0 || sms >= c->sm_count) {
+    c->err = "ps_set_k1_reserve: need 0 <= sms < SM count";
+    return PS_ERR_ARG;
+  }
+  c->k1_reserve_sms = sms;
+  return PS_OK;
+}
+
 int ps_set_overlap(ps_ctx* h, int sms) {
   if (!h) return PS_ERR_ARG;
   C(h)->overlap_sms = sms < 0 ? -1 : sms;

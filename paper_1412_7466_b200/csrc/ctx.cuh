@@ -64,6 +64,7 @@ struct Ctx {
   // overlap_sms CTAs in a high-priority stream while the HBM-bound coupling
   // chain streams on the remaining SMs in a low-priority stream
   int sym_part = 0, sym_nparts = 1;   // K1s block range (ps_apply_T_blocks)
+  int k1_reserve_sms = 0;   // single-RHS M2L grids leave this many SMs free (multi-GPU overlap)
   int overlap_sms = 2;      // < 0: serial (swept with tools/probe_k1.py: 2 is best at cfg3)
   cudaStream_t s_hi = nullptr, s_lo = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_k1 = nullptr, ev_cpl = nullptr;

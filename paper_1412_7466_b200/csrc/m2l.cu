@@ -354,7 +354,7 @@ int launch_p(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   a.period = ctx->period;
   a.k2 = ctx->k2;
   if (a.nt <= 0) return PS_OK;
-  int G = ctx->sm_count;
+  int G = ctx->sm_count - ctx->k1_reserve_sms;
   if ((long long)G > a.W) G = (int)a.W;
   a.maxseg = (int)((a.W / G + 1) / a.nbatch) + 2;
   const size_t need = (size_t)G * a.maxseg * kTT * S::L;

@@ -475,7 +475,7 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   // multi-GPU part: this launch covers blocks [NB part / nparts, NB (part+1) / nparts)
   a.kb0 = ((long long)a.NB * ctx->sym_part) / ctx->sym_nparts;
   a.nb = ((long long)a.NB * (ctx->sym_part + 1)) / ctx->sym_nparts - a.kb0;
-  int G = ov ? ov->grid : ctx->sm_count;
+  int G = ov ? ov->grid : ctx->sm_count - ctx->k1_reserve_sms;
   if (G > a.nb) G = (int)a.nb;
   if (G < 1) G = 1;
   a.maxseg = max_rows_per_cta(a.T, a.kb0, a.nb, G);

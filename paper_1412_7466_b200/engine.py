@@ -141,6 +141,10 @@ class Engine:
         """SMs left to the coupling chain while K1s runs (< 0: serial)."""
         self._check(self.lib.ps_set_overlap(self.ctx, int(sms)))
 
+    def set_k1_reserve(self, sms: int):
+        """Single-RHS M2L grids leave `sms` SMs free for overlapped work."""
+        self._check(self.lib.ps_set_k1_reserve(self.ctx, int(sms)))
+
     def set_mrhs_variant(self, variant: int):
         """0 auto, 1 DFMA K1m, 2 DMMA K1d (see include/periscat_b200.h)."""
         self._check(self.lib.ps_set_mrhs_variant(self.ctx, int(variant)))

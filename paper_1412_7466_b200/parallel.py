@@ -109,7 +109,7 @@ class ShardedSchur:
         (ps_apply_T_blocks / ps_schur_finish).
     """
 
-    def __init__(self, op, group=None, mode: str = "auto"):
+    def __init__(self, op, group=None, mode: str = "auto", overlap="auto", reserve: int = 4):
         self.op = op
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -126,6 +126,16 @@ class ShardedSchur:
         if mode not in ("pairs", "targets"):
             raise ValueError(f"unknown decomposition {mode!r}")
         self.mode = mode
+        # overlap of the M2L with the coupling chain + its all-reduce (one RHS,
+        # CUDA, diagonal or dense S): K1/K1s leave `reserve` SMs to the chain
+        want = (self.world > 1) if overlap == "auto" else bool(overlap)
+        self.overlap = (want and op.nrhs == 1 and op.coupled
+                        and str(op.device).startswith("cuda"))
+        if self.overlap:
+            self.s_hi = torch.cuda.Stream(device=op.device, priority=-1)
+            shape = (1, op.M if mode == "pairs" else self.t1 - self.t0, op.L)
+            self._a_buf = torch.empty(shape, dtype=torch.complex128, device=op.device)
+            op.eng.set_k1_reserve(reserve)
 
     def _coupling(self, v_full):
         if not self.op.coupled:
@@ -136,6 +146,8 @@ class ShardedSchur:
 
     def __call__(self, v_own: torch.Tensor, out=None) -> torch.Tensor:
         v_full = all_gather_rows(v_own, self.op.M, self.group)
+        if self.overlap:
+            return self._call_overlapped(v_own, v_full, out)
         if self.mode == "pairs":
             a_part = self.op.eng.apply_T_blocks(v_full, self.rank, self.world)
             a_own = reduce_scatter_rows(a_part, self.op.M, self.group)
@@ -145,6 +157,30 @@ class ShardedSchur:
         if g is None:
             return self.op(v_full, out=out)
         return self.op(v_full, out=out, g=g)
+
+    def _call_overlapped(self, v_own, v_full, out):
+        """One RHS on CUDA: the M2L runs on a high-priority stream with
+        `reserve` SMs left free, while the coupling chain (C partial over own
+        sources, NCCL all-reduce) runs on the caller's stream on those SMs;
+        the epilogue joins both (the reduce-scatter of the pairs split waits
+        for the M2L part only)."""
+        eng = self.op.eng
+        cur = torch.cuda.current_stream(v_full.device)
+        fork = torch.cuda.Event()
+        fork.record(cur)
+        v_full.record_stream(self.s_hi)
+        with torch.cuda.stream(self.s_hi):
+            self.s_hi.wait_event(fork)
+            if self.mode == "pairs":
+                a = eng.apply_T_blocks(v_full, self.rank, self.world, out=self._a_buf)
+            else:
+                a = eng.apply_T(v_full, out=self._a_buf)
+            done = torch.cuda.Event()
+            done.record(self.s_hi)
+        g = self._coupling(v_full)
+        cur.wait_event(done)
+        a_own = reduce_scatter_rows(a, self.op.M, self.group) if self.mode == "pairs" else a
+        return eng.schur_finish(v_own.contiguous(), a_own, g, out=out)
 
     def rhs(self) -> torch.Tensor:
         return self.op.rhs()

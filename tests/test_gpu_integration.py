@@ -61,5 +61,18 @@ def test_sharded_driver_nccl_world1():
         c, d = op.split_cd(xe)
         assert rel(c[0], z["c"]) <= 1e-9 and rel(d[0], z["d"]) <= 1e-9
         assert abs(its[0] - int(z["iterations"])) <= 1
+        # both decompositions with the overlapped stream schedule (M2L on a
+        # high-priority stream, coupling + NCCL all-reduce beside it) give the
+        # same matvec as the serial one
+        rng = np.random.default_rng(3)
+        v = torch.as_tensor(pb.smat[None, None, :] * (rng.standard_normal((1, pb.M, pb.L))
+                            + 1j * rng.standard_normal((1, pb.M, pb.L)))).cuda()
+        ref = sh(v).cpu().numpy()
+        for mode in ("targets", "pairs"):
+            sho = parallel.ShardedSchur(op, mode=mode, overlap=True)
+            for _ in range(2):
+                got = sho(v).cpu().numpy()
+                assert rel(got, ref) <= 1e-12
+            op.eng.set_k1_reserve(0)
     finally:
         dist.destroy_process_group()
