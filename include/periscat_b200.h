@@ -130,6 +130,15 @@ int ps_apply_T(ps_ctx* ctx, const void* beta_dev, void* out_dev, void* stream);
  * out [M][L] holds this part's contributions (each pair's forward and
  * reverse translations); summing the parts of all ranks (a reduce-scatter)
  * gives apply_T.  beta: the full coefficient vector [M][L]. */
+/* Particle field at points (M2P; SPEC.md:619-627 eval_total_field_grid, the
+ * "particle phased multipole sums" of the layer-2 representation, PAPER.md
+ * Eq. repre3_mod): out[r][i] = sum_l bloch_r^l sum_j sum_n beta_r,j[n]
+ * H_n(k2 rho) e^{i n phi}, (rho, phi) = polar(pts[i] - x_j - l d e_x).
+ * beta [nrhs][M][L], pts [npts][2] f64, out [nrhs][npts]; device pointers.
+ * Points inside a particle get its (invalid there) outgoing sum; callers
+ * mask them. */
+int ps_particle_field(ps_ctx* ctx, const void* beta, int npts, const double* pts, void* out,
+                      void* stream);
 int ps_apply_T_blocks(ps_ctx* ctx, int part, int nparts, const void* beta, void* out,
                       void* stream);
 /* Epilogue of the split: y_own = v_own - S (a_own - B A^+ g) for the owned

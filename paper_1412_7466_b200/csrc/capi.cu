@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "coupling.cuh"
+#include "field.cuh"
 #include "ctx.cuh"
 #include "gmres.cuh"
 #include "m2l.cuh"
@@ -304,6 +305,23 @@ int ps_apply_T(ps_ctx* h, const void* beta, void* out, void* stream) {
     if (rc) return rc;
   }
   return PS_OK;
+}
+
+int ps_particle_field(ps_ctx* h, const void* beta, int npts, const double* pts, void* out,
+                      void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (c->p < 0) {
+    c->err = "ps_particle_field: geometry not set";
+    return PS_ERR_STATE;
+  }
+  if (npts < 0 || (npts > 0 && (!beta || !pts || !out))) {
+    c->err = "ps_particle_field: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::particle_field(c, reinterpret_cast<const double2*>(beta), pts, npts,
+                            reinterpret_cast<double2*>(out), reinterpret_cast<cudaStream_t>(stream));
 }
 
 int ps_apply_T_blocks(ps_ctx* h, int part, int nparts, const void* beta, void* out, void* stream) {

@@ -186,6 +186,20 @@ class Engine:
                                                _stream(self.device)))
         return out
 
+    def particle_field(self, beta: torch.Tensor, points) -> torch.Tensor:
+        """[nrhs][npts] particle multipole field at points (ps_particle_field)."""
+        pts = torch.as_tensor(np.ascontiguousarray(np.asarray(points, dtype=float).reshape(-1, 2)),
+                              device=self.device)
+        out = torch.empty((self.nrhs, pts.shape[0]), dtype=torch.complex128, device=self.device)
+        if pts.shape[0] == 0:
+            return out
+        b = self._dev(beta, (self.nrhs, self.M, self.L))
+        self._check(self.lib.ps_particle_field(self.ctx, b, int(pts.shape[0]),
+                                               ctypes.c_void_p(pts.data_ptr()),
+                                               ctypes.c_void_p(out.data_ptr()),
+                                               _stream(self.device)))
+        return out
+
     def schur_finish(self, v_own: torch.Tensor, a_own: torch.Tensor, g: torch.Tensor | None,
                      out: torch.Tensor | None = None) -> torch.Tensor:
         """y_own = v_own - S (a_own - B A^+ g) (one RHS)."""

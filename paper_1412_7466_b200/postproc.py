@@ -1,4 +1,7 @@
-"""Flux-balance diagnostic (postproc.flux_error)."""
+"""Post-processing: flux balance (flux_error, SPEC.md:599-607;
+PAPER.md:915-921), Wood's-anomaly report, and field evaluation on a grid
+(eval_total_field_grid) with the particle multipole sums on
+the device."""
 from __future__ import annotations
 
 import math
@@ -31,3 +34,96 @@ def wood_anomaly_report(config, tolerance: float = 1e-8) -> list:
             if abs(gap) <= tolerance:
                 out.append((layer, int(n), float(gap)))
     return out
+
+
+def particle_field(op, beta, points) -> np.ndarray:
+    """[nrhs][npts] particle phased multipole sums (PAPER.md Eq. repre3_mod) at
+    points, on the device (ps_particle_field, field.cu).  ``op`` is a
+    SchurOperator (or anything with ``.eng``); beta [nrhs][M][L]."""
+    import torch
+    eng = op.eng if hasattr(op, "eng") else op
+    b = torch.as_tensor(np.asarray(beta, dtype=complex)) if not isinstance(beta, torch.Tensor) \
+        else beta
+    b = b.to(device=eng.device, dtype=torch.complex128).reshape(eng.nrhs, eng.M, eng.L).contiguous()
+    return eng.particle_field(b, points).cpu().numpy()
+
+
+def _interface_heights(config, system, x):
+    if hasattr(config, "interface_top"):                      # reference ProblemConfig
+        return (config.interface_top.height(x, config.period),
+                config.interface_bottom.height(x, config.period))
+    g1 = system.curves["g1"].nodes[:, 1]                       # flat fixture interfaces
+    g2 = system.curves["g2"].nodes[:, 1]
+    return np.full_like(x, g1.mean()), np.full_like(x, g2.mean())
+
+
+def classify_points(config, points, centers, radius: float, system=None,
+                    mask_nodes: float = 5.0,
+                    nodes_per_period: int | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """Region of every point: layer 1 / 2 / 3 by the flat
+    interfaces (eg.classify_layer, empty_grating.py:341-349), and a mask for
+    points inside a particle (any phased copy) or within ``mask_nodes`` local
+    node spacings of an interface (the near-evaluation contract, SPEC design
+    decision "5 local node spacings")."""
+    pts = np.atleast_2d(np.asarray(points, dtype=float))
+    top, bot = _interface_heights(config, system, pts[:, 0])
+    layer = np.full(pts.shape[0], 2, dtype=int)
+    layer[pts[:, 1] > top] = 1
+    layer[pts[:, 1] < bot] = 3
+    n_nodes = nodes_per_period or (system.curves["g1"].n if system is not None else 120)
+    h = config.period / n_nodes
+    masked = (np.abs(pts[:, 1] - top) < mask_nodes * h) | (np.abs(pts[:, 1] - bot) < mask_nodes * h)
+    cen = np.asarray(centers, dtype=float)
+    P = config.near_field_copies
+    for l in range(-P - 1, P + 2):
+        dx = pts[:, 0, None] - cen[None, :, 0] - l * config.period
+        dy = pts[:, 1, None] - cen[None, :, 1]
+        masked |= np.any(dx * dx + dy * dy < radius * radius, axis=1)
+    return layer, masked
+
+
+def eval_total_field_grid(op, beta, centers, radius: float, nx: int = 128, ny: int = 128,
+                          y_plot: float | None = None, layer_field=None) -> dict:
+    """SPEC.md:619-627 on a uniform grid over [-d/2, d/2] x [-y_plot, y_plot].
+
+    Particle phased multipole sums come from the device (layer-2 points);
+    ``layer_field(points) -> [nrhs][npts]`` supplies the empty-grating layer
+    fields + u_inc (the reference's ``empty_grating.eval_empty_field`` on the
+    solution x_empty = A^+(f - C beta), eg:352-393); without it the result is
+    the particle part only.  Masked points (inside particles, near interfaces)
+    are NaN and flagged in ``mask``."""
+    cfg = op.config
+    d = cfg.period
+    y_plot = 1.0 if y_plot is None else y_plot
+    xs = np.linspace(-d / 2, d / 2, nx)
+    ys = np.linspace(-y_plot, y_plot, ny)
+    X, Y = np.meshgrid(xs, ys, indexing="xy")
+    pts = np.column_stack([X.ravel(), Y.ravel()])
+    # layers + interface mask per point; particle interiors rasterised per disk
+    # copy on the uniform grid (O(M r^2 / h^2) instead of O(points x M))
+    layer, masked = classify_points(cfg, pts, np.empty((0, 2)), radius, system=op.systems[0])
+    inside = np.zeros((ny, nx), dtype=bool)
+    hx = xs[1] - xs[0] if nx > 1 else 1.0
+    hy = ys[1] - ys[0] if ny > 1 else 1.0
+    P = cfg.near_field_copies
+    for l in range(-P - 1, P + 2):
+        for cx, cy in np.asarray(centers, dtype=float):
+            cx = cx + l * d
+            i0 = max(0, int(np.floor((cx - radius - xs[0]) / hx)))
+            i1 = min(nx - 1, int(np.ceil((cx + radius - xs[0]) / hx)))
+            j0 = max(0, int(np.floor((cy - radius - ys[0]) / hy)))
+            j1 = min(ny - 1, int(np.ceil((cy + radius - ys[0]) / hy)))
+            if i0 > i1 or j0 > j1:
+                continue
+            sub = (xs[None, i0:i1 + 1] - cx) ** 2 + (ys[j0:j1 + 1, None] - cy) ** 2 < radius * radius
+            inside[j0:j1 + 1, i0:i1 + 1] |= sub
+    masked |= inside.ravel()
+    u = np.zeros((op.nrhs, pts.shape[0]), dtype=complex)
+    in2 = (layer == 2) & ~masked
+    if np.any(in2):
+        u[:, in2] = particle_field(op, beta, pts[in2])
+    if layer_field is not None:
+        u += np.asarray(layer_field(pts), dtype=complex).reshape(op.nrhs, -1)
+    u[:, masked] = np.nan
+    return dict(x=xs, y=ys, field=u.reshape(op.nrhs, ny, nx), layer=layer.reshape(ny, nx),
+                mask=masked.reshape(ny, nx))

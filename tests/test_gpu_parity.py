@@ -458,3 +458,53 @@ def test_pair_split_shards_reassemble(O, ranks):
         y = op.eng.schur_finish(vd[:, t0:t1].contiguous(), a_sum[:, t0:t1].contiguous(), g)
         got.append(y.cpu().numpy()[0])
     assert rel(np.concatenate(got, axis=0), ref) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("nrhs,p,M", [(1, 20, 100), (3, 5, 17), (5, 25, 9)])
+def test_particle_field_matches_oracle(O, nrhs, p, M):
+    """ps_particle_field (M2P over grid points) vs the
+    oracle's phased multipole sums, points outside every particle copy."""
+    from paper_1412_7466_b200 import postproc
+    from paper_1412_7466_b200.engine import Engine
+    rng = np.random.default_rng(100 + M)
+    centers = np.column_stack([rng.uniform(-0.45, 0.45, M), rng.uniform(-0.4, 0.4, M)])
+    beta = _cplx(rng, (nrhs, M, 2 * p + 1))
+    bl = np.exp(1j * rng.uniform(-3, 3, nrhs))
+    pts = np.column_stack([rng.uniform(-0.5, 0.5, 300), rng.uniform(-0.45, 0.45, 300)])
+    dmin = np.min(np.hypot(pts[:, None, 0] - centers[None, :, 0], pts[:, None, 1] - centers[None, :, 1]), axis=1)
+    pts = pts[dmin > 0.01]
+    eng = Engine(0)
+    eng.set_geometry(centers, p, 12.0, 1.0, 1)
+    eng.set_bloch(bl)
+    got = postproc.particle_field(eng, beta, pts)
+    eng.close()
+    for r in range(nrhs):
+        ref = sum((bl[r] ** l) * O._particle_field(12.0, beta[r], centers, pts, float(l))[0]
+                  for l in (-1, 0, 1))
+        assert rel(got[r], ref) <= 1e-12
+
+
+def test_eval_total_field_grid_cfg2(O):
+    """Grid evaluation: the rasterised particle mask equals
+    the brute-force classification, masked points are NaN, and the layer-2
+    particle field matches the oracle's phased multipole sums."""
+    from paper_1412_7466_b200 import grating, postproc, solver
+    pb = O.load_problem(2)
+    sysm = grating.load_fixture("w10")
+    op = solver.SchurOperator(sysm, pb.centers, pb.p, smat=pb.smat)
+    rng = np.random.default_rng(4)
+    beta = pb.smat[None, None, :] * _cplx(rng, (1, pb.M, pb.L))
+    res = postproc.eval_total_field_grid(op, beta, pb.centers, 0.04, nx=60, ny=50, y_plot=0.7)
+    xx, yy = np.meshgrid(res["x"], res["y"])
+    pts = np.column_stack([xx.ravel(), yy.ravel()])
+    layer, masked = postproc.classify_points(op.config, pts, pb.centers, 0.04, system=sysm)
+    assert np.array_equal(masked, res["mask"].ravel())
+    assert np.array_equal(layer, res["layer"].ravel())
+    f = res["field"][0].ravel()
+    assert np.all(np.isnan(f[masked]))
+    sel = np.flatnonzero((layer == 2) & ~masked)[::25]
+    al = op.config.bloch_phase
+    ref = sum((al ** l) * O._particle_field(pb.es.k2, beta[0], pb.centers, pts[sel], float(l))[0]
+              for l in (-1, 0, 1))
+    assert rel(f[sel], ref) <= 1e-12
+    assert np.all(f[(layer != 2) & ~masked] == 0)
