@@ -10,7 +10,8 @@
 // exactly L row tiles of 8, so only the K = L dimension is padded).  It runs
 // as mma.sync.m8n8k4.f64 (DMMA, 256 FMA per warp instruction; measured
 // 37.1 TF/s on B200 against 34.2 TF/s for DFMA), three real MMAs per complex
-// tile (Karatsuba: Ar Br, Ai Bi, (Ar + Ai)(Br + Bi)).  The symbol rows come from the same producer warpgroup as K1/K1m.
+// tile (Karatsuba: Ar Br, Ai Bi, (Ar + Ai)(Br + Bi)); the producer stores
+// Ar + Ai beside each symbol so the consumers add nothing on the A side.  The symbol rows come from the same producer warpgroup as K1/K1m.
 //
 // Warps: 12 consumer warps own (row tile, RHS tile) accumulator units
 // (2L units per CTA group, <= 7 per warp); 4 producer warps (setmaxnreg).
@@ -28,14 +29,14 @@ namespace ps {
 namespace {
 
 constexpr int kTT = 8;                 // targets per tile (stacked)
-constexpr int kSB = 8;                 // source images per batch
+constexpr int kSBMax = 8;              // source images per batch (at most; see ShapeD::SB)
 constexpr int kCW = 12;                // consumer warps
 constexpr int kPW = 4;                 // producer warps
 constexpr int kThreads = (kCW + kPW) * 32;
 constexpr int kRG = 16;                // RHS per group (2 MMA column tiles)
 constexpr int kNT = kRG / 8;
 constexpr int kPhases = 8;
-static_assert(kTT * kSB * 2 == kPW * 32, "64 rows, two producer lanes each");
+static_assert(kTT * kSBMax * 2 == kPW * 32, "up to 64 rows, two producer lanes each");
 // per sub-partition: 3 consumer + 1 producer warp; 3*Rc + Rp <= 512
 constexpr int kConsumerRegs = 152;
 constexpr int kProducerRegs = 56;
@@ -49,8 +50,16 @@ struct ShapeD {
   static constexpr int OFF = L - 1;               // slot of nu = 0
   static constexpr int NSPR = 4 * KT + L - 1;     // nu in [-(L-1), 4 KT - 1]
   static constexpr int NSP = NSPR | 1;            // odd row stride
-  static constexpr int SYM = kTT * kSB * NSP;     // double2 per buffer
-  static constexpr size_t SMEM = 2 * (size_t)SYM * sizeof(double2);
+  // Each buffer also holds re + im of every symbol (double, the Karatsuba A
+  // operand) so the consumers issue no DADD per A fragment, with as many
+  // source images per batch as fit two such buffers in 227 KB (7 at p = 20,
+  // 5 at p = 25).  Measured (tools/probe_k1d_p25.py) faster than the
+  // in-register DADD with 8 images per batch at every p from 10 to 25.
+  static constexpr int SBFIT = 232448 / (2 * kTT * NSP * 24);
+  static constexpr int SB = SBFIT < kSBMax ? SBFIT : kSBMax;
+  static_assert(SB >= 1, "symbol buffers exceed shared memory");
+  static constexpr int SYM = kTT * SB * NSP;      // symbols (double2) or sums (double) per buffer
+  static constexpr size_t SMEM = 2 * (size_t)SYM * (sizeof(double2) + sizeof(double));
 };
 
 struct ArgsD {
@@ -75,17 +84,18 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 // rows (s, t) at (s * kTT + t) * NSP; slot = nu + OFF
 template <int P>
-__device__ __forceinline__ void produce_d(const ArgsD& a, long long w, double2* sym, int pw,
-                                          int lane) {
+__device__ __forceinline__ void produce_d(const ArgsD& a, long long w, double2* sym, double* sum,
+                                          int pw, int lane) {
   using S = ShapeD<P>;
   const int tile = (int)(w / a.nbatch);
-  const int sb = (int)(w % a.nbatch) * kSB;
+  const int sb = (int)(w % a.nbatch) * S::SB;
   const int row = pw * 16 + (lane & 15);         // quarter-warps write consecutive rows
+  const bool rok = row < kTT * S::SB;
   const bool mirror = lane >> 4;
   const int s = row / kTT, t = row % kTT;
   const int mloc = tile * kTT + t;
   const int g = sb + s;
-  bool live = (mloc < a.nt) && (g < a.nimg);
+  bool live = rok && (mloc < a.nt) && (g < a.nimg);
   double dx = 1.0, dy = 0.0;
   if (live) {
     const int m = a.t_begin + mloc;
@@ -103,9 +113,12 @@ __device__ __forceinline__ void produce_d(const ArgsD& a, long long w, double2* 
   N = __reduce_max_sync(0xffffffffu, N);
   const double inv = live ? 1.0 / rho : 0.0;
   double2* base = sym + (size_t)row * S::NSP + S::OFF;
+  double* sbase = sum + (size_t)row * S::NSP + S::OFF;
   hankel_symbols_half<2 * P>(z, dx * inv, dy * inv, N, mirror, [&](int nu, double re, double im) {
+    if (!rok) return;
     if (nu == 0 && !live) re = im = 0.0;
     base[nu] = make_double2(re, im);
+    sbase[nu] = re + im;
   });
 }
 
@@ -113,11 +126,11 @@ __device__ __forceinline__ void produce_d(const ArgsD& a, long long w, double2* 
 template <int P>
 __device__ __forceinline__ void prefetch_bw_d(const ArgsD& a, long long w, int pl) {
   using S = ShapeD<P>;
-  const int sb = (int)(w % a.nbatch) * kSB;
+  const int sb = (int)(w % a.nbatch) * S::SB;
   const int nr = min(kRG, a.nrhs - a.rg0);
-  for (int row = pl; row < nr * kSB; row += kPW * 32) {
-    const int r = a.rg0 + row / kSB;
-    const int g = sb + row % kSB;
+  for (int row = pl; row < nr * S::SB; row += kPW * 32) {
+    const int r = a.rg0 + row / S::SB;
+    const int g = sb + row % S::SB;
     if (g >= a.nimg) continue;
     const char* p = reinterpret_cast<const char*>(a.bw + ((size_t)r * a.nimg + g) * S::L);
     for (int off = 0; off < S::L * 16; off += 128)
@@ -132,6 +145,8 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mma_kernel(ArgsD a) {
   extern __shared__ double2 smem[];
   double2* sym0 = smem;
   double2* sym1 = smem + S::SYM;
+  double* sum0 = reinterpret_cast<double*>(smem + 2 * S::SYM);
+  double* sum1 = sum0 + S::SYM;
   const int G = gridDim.x;
   const long long w0 = work_begin(a.W, G, blockIdx.x, a.q);
   const long long w1 = work_begin(a.W, G, blockIdx.x + 1, a.q);
@@ -141,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mma_kernel(ArgsD a) {
 
   // zero both buffers once: slots outside |nu| <= 2P are read (padding K
   // columns whose B is zero) and must be finite
-  for (int i = threadIdx.x; i < 2 * S::SYM; i += kThreads) smem[i] = make_double2(0.0, 0.0);
+  for (int i = threadIdx.x; i < 3 * S::SYM; i += kThreads) smem[i] = make_double2(0.0, 0.0);
   __syncthreads();
 
   if (producer) {
@@ -150,12 +165,12 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mma_kernel(ArgsD a) {
     const int pl = pw * 32 + lane;
     prefetch_bw_d<P>(a, w0, pl);
     if (w0 + 1 < w1) prefetch_bw_d<P>(a, w0 + 1, pl);
-    produce_d<P>(a, w0, sym0, pw, lane);
+    produce_d<P>(a, w0, sym0, sum0, pw, lane);
     __syncthreads();
     for (long long w = w0; w < w1; ++w) {
       const int cur = (int)((w - w0) & 1);
       if (w + 2 < w1) prefetch_bw_d<P>(a, w + 2, pl);
-      if (w + 1 < w1) produce_d<P>(a, w + 1, cur ? sym0 : sym1, pw, lane);
+      if (w + 1 < w1) produce_d<P>(a, w + 1, cur ? sym0 : sym1, cur ? sum0 : sum1, pw, lane);
       __syncthreads();
     }
     return;
@@ -166,18 +181,16 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mma_kernel(ArgsD a) {
   // fragment coordinates (PTX m8n8k4 f64): A[r][c], B[c][r'], C[r][2c'+i]
   const int fr = lane >> 2, fc = lane & 3;
   // this warp's units u = warp + kCW * k: row tile u / kNT, RHS tile u % kNT
-  int rt[UPW], nt_[UPW], tA[UPW], mA[UPW];
-  bool uok[UPW];
+  // = warp % kNT for every k (kCW is a multiple of kNT); only the row offset
+  // of the lane's A element is kept per unit (register pressure at p >= 24)
+  static_assert(kCW % kNT == 0, "uniform RHS tile per warp");
+  const int ntw = warp % kNT;
+  const int nk = (S::UNITS - warp + kCW - 1) / kCW;   // valid units of this warp
+  int offA[UPW];
 #pragma unroll
   for (int k = 0; k < UPW; ++k) {
-    const int u = warp + kCW * k;
-    uok[k] = u < S::UNITS;
-    const int uu = uok[k] ? u : 0;
-    rt[k] = uu / kNT;
-    nt_[k] = uu % kNT;
-    const int srow = rt[k] * 8 + fr;             // stacked row of this lane's A element
-    tA[k] = srow / L;                            // target slot
-    mA[k] = srow % L;                            // row m'
+    const int srow = ((warp + kCW * k) / kNT) * 8 + fr;   // stacked row of the A element
+    offA[k] = (srow / L) * S::NSP - (srow % L);           // target slot * NSP - row m'
   }
   // Karatsuba: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi);
   // Re C = P1 - P2, Im C = P3 - P1 - P2 -> three real MMAs per complex tile
@@ -190,14 +203,16 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mma_kernel(ArgsD a) {
   for (long long w = w0; w < w1; ++w) {
     const int cur = (int)((w - w0) & 1);
     const double2* symc = cur ? sym1 : sym0;
-    const int sb = (int)(w % a.nbatch) * kSB;
+    const double* sumc = cur ? sum1 : sum0;
+    const int sb = (int)(w % a.nbatch) * S::SB;
 #pragma unroll 1
-    for (int s = 0; s < kSB; ++s) {
+    for (int s = 0; s < S::SB; ++s) {
       const int g = min(sb + s, a.nimg - 1);      // dead images have zero symbols
       const double2* bw0 = a.bw + ((size_t)min(rb, a.nrhs - 1) * a.nimg + g) * L;
       const double2* bw1 = a.bw + ((size_t)min(rb + 8, a.nrhs - 1) * a.nimg + g) * L;
       const bool ok0 = rb < a.nrhs, ok1 = rb + 8 < a.nrhs;
       const double2* rowb = symc + (size_t)s * kTT * S::NSP + S::OFF;
+      const double* rows = sumc + (size_t)s * kTT * S::NSP + S::OFF;
 #pragma unroll
       for (int kt = 0; kt < S::KT; ++kt) {
         const int n = kt * 4 + fc;
@@ -209,13 +224,15 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mma_kernel(ArgsD a) {
         const double bs0 = b0.x + b0.y, bs1 = b1.x + b1.y;
 #pragma unroll
         for (int k = 0; k < UPW; ++k) {
-          if (!uok[k]) continue;
-          const double2 av = rowb[(size_t)tA[k] * S::NSP + (n - mA[k])];
-          const double2 bb = nt_[k] ? b1 : b0;
-          const double bs = nt_[k] ? bs1 : bs0;
+          if (k >= nk) continue;
+          const int ia = offA[k] + n;
+          const double2 av = rowb[ia];
+          const double as = rows[ia];
+          const double2 bb = ntw ? b1 : b0;
+          const double bs = ntw ? bs1 : bs0;
           dmma(p1[k], av.x, bb.x);
           dmma(p2[k], av.y, bb.y);
-          dmma(p3[k], av.x + av.y, bs);
+          dmma(p3[k], as, bs);
         }
       }
     }
@@ -223,12 +240,12 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_mma_kernel(ArgsD a) {
       double2* dst = a.partial + ((size_t)blockIdx.x * a.maxseg + seg) * kRG * kTT * L;
 #pragma unroll
       for (int k = 0; k < UPW; ++k) {
-        if (uok[k]) {
-          const int srow = rt[k] * 8 + fr;
+        if (k < nk) {
+          const int srow = ((warp + kCW * k) / kNT) * 8 + fr;
           const int t = srow / L, mp = srow % L;
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
-            const int rl = nt_[k] * 8 + 2 * fc + i;        // RHS within the group
+            const int rl = ntw * 8 + 2 * fc + i;           // RHS within the group
             dst[((size_t)rl * kTT + t) * L + mp] =
                 make_double2(p1[k][i] - p2[k][i], p3[k][i] - p1[k][i] - p2[k][i]);
           }
@@ -319,7 +336,7 @@ int launch_d(Ctx* ctx, const double2* beta, double2* out, int mode, const double
   a.copies = ctx->copies;
   a.ncp = 2 * ctx->copies + 1;
   a.nimg = ctx->M * a.ncp;
-  a.nbatch = (a.nimg + kSB - 1) / kSB;
+  a.nbatch = (a.nimg + S::SB - 1) / S::SB;
   const int ntiles = (nt + kTT - 1) / kTT;
   a.W = (long long)ntiles * a.nbatch;
   a.period = ctx->period;
