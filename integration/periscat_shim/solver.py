@@ -30,4 +30,44 @@ def solve_full(config, system=None, particles=None, standoff=None):
                        radius=shape.base_radius, tol=config.gmres_tol, maxit=config.gmres_maxit)
 
 
-__all__ = ["SchurOperator", "Solution", "apply_schur_operator", "gmres", "solve_full"]
+def _assemble_factorize(config):
+    from periscat.empty_grating import assemble_empty_system, factorize
+    system = assemble_empty_system(config)
+    factorize(system)
+    return system
+
+
+def assemble_systems(configs, threads: int | None = None):
+    """Empty-grating systems + SVDs for several incidence angles (SURVEY 8f
+    row 1: setup off the critical path).  The reference assembly (eg:139-261)
+    is host NumPy/SciPy, ~2.7 s + 0.36 s SVD per angle.  The angles are
+    independent and the systems hold closures (no pickling to processes), so
+    they run in threads: SciPy's special-function ufuncs and LAPACK release
+    the GIL (3.6x on 8 threads here)."""
+    import concurrent.futures as cf
+    import os
+    configs = list(configs)
+    n = min(len(configs), threads or os.cpu_count() or 1)
+    if n <= 1:
+        return [_assemble_factorize(c) for c in configs]
+    with cf.ThreadPoolExecutor(n) as ex:
+        return list(ex.map(_assemble_factorize, configs))
+
+
+def solve_full_batch(configs, particles, threads: int | None = None):
+    """Several incidence angles sharing k2, the period and the particles,
+    solved as ONE batch of right-hand sides (BASELINE cfg5: 16 angles): the
+    per-angle setup in parallel host threads, then the batched GPU solve
+    (multi-RHS M2L on the FP64 tensor cores, batched device GMRES)."""
+    systems = assemble_systems(configs, threads)
+    shape = particles.shape
+    if shape.bump_amplitude != 0.0:
+        raise NotImplementedError("general-shape scattering matrices (Mueller BIE) are not built "
+                                  "here; pass smat= to paper_1412_7466_b200.solver.solve_full")
+    c0 = configs[0]
+    return _solve_full(systems, particles.centers, c0.multipole_order, radius=shape.base_radius,
+                       tol=c0.gmres_tol, maxit=c0.gmres_maxit)
+
+
+__all__ = ["SchurOperator", "Solution", "apply_schur_operator", "assemble_systems", "gmres",
+           "solve_full", "solve_full_batch"]
