@@ -394,9 +394,16 @@ __global__ void k1s_reduce(const double2* __restrict__ apart, const double2* __r
   auto off = [&](int a) -> long long { return (long long)a * T - (long long)a * (a - 1) / 2; };
   auto kbeg = [&](int c) -> long long { return kb0 + (nb * c) / G; };
   double2 sum = make_double2(0.0, 0.0);
-  for (int A = 0; A < X; ++A) {
+  // the blocks (A, X), A < X, have increasing indices off(A) + X - A: the
+  // in-range ones are a contiguous run of A
+  int A0 = 0, A1 = X;
+  if (kb0 > 0 || kb1 < off(T)) {
+    while (A0 < X && off(A0) + (X - A0) < kb0) ++A0;
+    A1 = A0;
+    while (A1 < X && off(A1) + (X - A1) < kb1) ++A1;
+  }
+  for (int A = A0; A < A1; ++A) {
     const long long k = off(A) + (X - A);
-    if (k < kb0 || k >= kb1) continue;
     const double2 v = bpart[((size_t)k * kTT + w) * L + r];
     sum.x += v.x;
     sum.y += v.y;
