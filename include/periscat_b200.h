@@ -189,6 +189,68 @@ int ps_norm2(ps_ctx* ctx, int nrhs, int n, const void* w_dev, double* nrm2_dev, 
 int ps_gmres(ps_ctx* ctx, const void* rhs_dev, void* x_dev, double tol, int maxit,
              int* iters_host, double* hist_host, void* stream);
 
+/* ---- empty-grating setup on the device --------- */
+
+/* One discretised curve of empty_grating.build_geometry (empty_grating.py:
+ * 113-119; geometry.py:188-254): host rows of 8 doubles per node
+ *   x, y, nx, ny, speed, weight, t, arc_weight (= weight * speed). */
+typedef struct ps_curve_desc {
+  int n;
+  const double* data;
+} ps_curve_desc;
+
+/* InterfaceSpec (geometry.py:67-96): y = mean + sum_j a_j sin(2 pi j x/d)
+ * + b_j cos(2 pi j x/d), j = 1..; at most 8 coefficients of each kind. */
+typedef struct ps_interface_desc {
+  double mean;
+  int nsin, ncos;
+  const double* sin_coeffs;
+  const double* cos_coeffs;
+} ps_interface_desc;
+
+/* Everything assemble_empty_system (empty_grating.py:139-256) reads from a
+ * ProblemConfig (geometry.py:317-406) and its curves. */
+typedef struct ps_empty_desc {
+  double period, k1, k2, k3;
+  double y0;                   /* artificial boundary (ProblemConfig.y0) */
+  double eps;                  /* regularization (apply_pinv, eg:270) */
+  int copies;                  /* near_field_copies P */
+  int Q;                       /* j_expansion_order */
+  int nrb;                     /* rb_modes_per_direction (odd) */
+  double centers[6];           /* expansion_centers() 1, 2, 3 (geometry.py:398-406) */
+  ps_curve_desc g1, g2;        /* top / bottom interface (sample_interface) */
+  ps_curve_desc wall[3];       /* left walls L1, L2, L3; right walls are +d translates */
+  ps_curve_desc lid_up, lid_down;   /* Gu at +y0, Gd at -y0 */
+  ps_interface_desc top, bottom;    /* parametrisation for the off-grid Alpert nodes */
+  int rule_n, rule_skip, rule_interp;   /* CorrectionRule (quadrature.py:41-56) */
+  const double* rule_x;
+  const double* rule_w;
+} ps_empty_desc;
+
+/* Assemble the column-scaled empty-grating matrix A and rhs f for every RHS
+ * on the device (one launch; empty_grating.assemble_empty_system), take its
+ * SVD with cuSOLVER (empty_grating.factorize, eg:259-261), and install the
+ * restricted A^+ factors and the layer-coupling curves exactly as
+ * ps_set_layers + ps_set_pinv would from host factors.  theta_host[nrhs]:
+ * incidence angles (ProblemConfig.incident_angle, measured from +x); the
+ * Bloch phases are the ones given to ps_set_rhs_bloch (call it first).
+ * PS_ERR_NUMERICAL if an SVD does not converge. */
+int ps_setup_empty(ps_ctx* ctx, const ps_empty_desc* desc, const double* theta_host);
+/* Rows/columns of the device-assembled A (856 x 781 at the BASELINE geometry). */
+int ps_empty_shape(const ps_ctx* ctx, int* nrow, int* ncol);
+/* Copy one RHS's device-assembled data back (any pointer may be NULL):
+ * A complex [nrow][ncol] row-major (column-scaled, as EmptyGratingSystem.matrix),
+ * f complex [nrow], col_scale [ncol], singular values s [ncol] (descending). */
+int ps_get_empty(ps_ctx* ctx, int irhs, double* A_host, double* f_host, double* col_scale_host,
+                 double* s_host);
+/* Concurrent cuSOLVER streams used for the per-RHS SVDs (default 4). */
+int ps_set_svd_workers(ps_ctx* ctx, int workers);
+/* SVD algorithm of ps_setup_empty: 0 cuSOLVER zgesvd (default; bidiagonal
+ * QR like LAPACK), 1 cuSOLVER Xgesvdp (QDWH polar decomposition). */
+int ps_set_svd_method(ps_ctx* ctx, int method);
+/* Device time of the last ps_setup_empty: assembly and SVD + factor restriction. */
+int ps_setup_timings(const ps_ctx* ctx, double* assemble_ms, double* svd_ms);
+
 /* ---- instrumentation ---------------------------------------------------- */
 /* Record CUDA events around every K1 (M2L) launch of this context. */
 int ps_profile(ps_ctx* ctx, int enable);

@@ -56,7 +56,34 @@ SIGNATURES = {
     "ps_schur_finish": (_I, [_P, _P, _P, _P, _P, _P]),
     "ps_stats": (_I, [_P, ctypes.POINTER(ctypes.c_longlong), _DP, ctypes.POINTER(ctypes.c_longlong)]),
     "ps_stats_reset": (_I, [_P]),
+    "ps_setup_empty": (_I, [_P, _P, _P]),
+    "ps_empty_shape": (_I, [_P, _IP, _IP]),
+    "ps_get_empty": (_I, [_P, _I, _P, _P, _P, _P]),
+    "ps_set_svd_workers": (_I, [_P, _I]),
+    "ps_set_svd_method": (_I, [_P, _I]),
+    "ps_setup_timings": (_I, [_P, _DP, _DP]),
 }
+
+
+class CurveDesc(ctypes.Structure):
+    """ps_curve_desc: n nodes, rows (x, y, nx, ny, speed, weight, t, arc_weight)."""
+    _fields_ = [("n", _I), ("data", _P)]
+
+
+class InterfaceDesc(ctypes.Structure):
+    """ps_interface_desc (InterfaceSpec, geometry.py:67-96)."""
+    _fields_ = [("mean", _D), ("nsin", _I), ("ncos", _I), ("sin_coeffs", _P), ("cos_coeffs", _P)]
+
+
+class EmptyDesc(ctypes.Structure):
+    """ps_empty_desc (include/periscat_b200.h)."""
+    _fields_ = [("period", _D), ("k1", _D), ("k2", _D), ("k3", _D), ("y0", _D), ("eps", _D),
+                ("copies", _I), ("Q", _I), ("nrb", _I), ("centers", _D * 6),
+                ("g1", CurveDesc), ("g2", CurveDesc), ("wall", CurveDesc * 3),
+                ("lid_up", CurveDesc), ("lid_down", CurveDesc),
+                ("top", InterfaceDesc), ("bottom", InterfaceDesc),
+                ("rule_n", _I), ("rule_skip", _I), ("rule_interp", _I),
+                ("rule_x", _P), ("rule_w", _P)]
 
 _lib = None
 

@@ -10,6 +10,7 @@
 #include "coupling.cuh"
 #include "field.cuh"
 #include "ctx.cuh"
+#include "empty.cuh"
 #include "gmres.cuh"
 #include "m2l.cuh"
 
@@ -87,6 +88,7 @@ void ps_destroy(ps_ctx* h) {
   }
   ps::release_dense_coupling(c);
   ps::gmres_release(c);
+  ps::empty_release(c);
   if (c->s_hi) cudaStreamDestroy(c->s_hi);
   if (c->s_lo) cudaStreamDestroy(c->s_lo);
   cudaEvent_t evs[] = {c->ev_fork, c->ev_k1, c->ev_cpl};

@@ -15,6 +15,8 @@ struct Dev2 {  // tiny RAII-free device buffer record (freed in ps_destroy)
   size_t bytes = 0;
 };
 
+struct EmptyState;   // device empty-grating setup (empty.cu)
+
 struct RhsData {          // per right-hand side (incidence angle)
   double2 bloch{1.0, 0.0};
   // A^+ factors restricted to what the Schur correction touches
@@ -79,6 +81,11 @@ struct Ctx {
   size_t partial_elems = 0;
   double2* d_work = nullptr;       // misc per-call workspace
   size_t work_elems = 0;
+
+  // device empty-grating assembly + SVD (ps_setup_empty, empty.cu)
+  EmptyState* empty = nullptr;
+  int svd_workers = 4;             // concurrent cuSOLVER streams for multi-RHS setup
+  int svd_method = 0;              // 0 zgesvd, 1 Xgesvdp (polar decomposition)
 
   std::vector<void*> owned;        // everything cudaMalloc'ed
 

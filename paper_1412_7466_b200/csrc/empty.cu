@@ -1,0 +1,1129 @@
+// Empty-grating setup on the device: assembly of the
+// column-scaled block matrix A and right-hand side f of the inclusion-free
+// three-layer grating, its SVD, and the restricted A^+ factors the Schur
+// correction streams every GMRES iteration.
+//
+// Replaces, per right-hand side (incidence angle):
+//   empty_grating.assemble_empty_system   (empty_grating.py:139-256)
+//     + layerpot.boundary_operator_matrices (layerpot.py:171-208)
+//     + quadrature.nystrom_selfmatrix       (quadrature.py:106-186; Alpert
+//       log-corrections with the quasi-periodic stencil wrap)
+//     + layerpot._t_difference              (layerpot.py:106-141)
+//     + layerpot.wall_discrepancy_blocks    (layerpot.py:211-237)
+//     + specialfn.regular_wave_block        (specialfn.py:86-125)
+//     + empty_grating.rb_basis / incident_field (empty_grating.py:32-61)
+//   empty_grating.factorize                 (empty_grating.py:259-261; cuSOLVER
+//                                             zgesvd in place of LAPACK gesdd)
+//   and the restriction ps_set_pinv performs on host factors (capi.cu).
+//
+// Work decomposition: every matrix entry is owned by exactly one work item of
+// one task (a (row block, column block) pair of eg:164-238); one launch covers
+// all tasks of all right-hand sides (grid.y = RHS).  Interface/lid/wall items
+// are (target node, source node) pairs that evaluate H0/H1 once per phased
+// copy and write the 2x2 [[D, S], [T, N]] entries; regular-expansion items are
+// (node, order) pairs with a Miller sweep per item.  The Alpert corrections of
+// the two self blocks are gathered, not scattered: a first kernel evaluates the
+// kernel at the 2 x rule_n off-grid nodes of every row, and each entry (i, j)
+// sums the (at most one per off-grid node) Lagrange stencil weight landing on
+// column j -- the same terms np.add.at accumulates (quadrature.py:166-186).
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "bessel.cuh"
+#include "coupling.cuh"
+#include "ctx.cuh"
+#include "empty.cuh"
+
+namespace ps {
+
+namespace {
+
+constexpr int kCS = 8;          // doubles per curve node: x y nx ny speed weight t aw
+constexpr int kMaxTasks = 24;
+constexpr int kMaxRule = 16;
+constexpr int kMaxCoef = 8;     // trig coefficients per interface
+constexpr int kPsiTerms = 14;   // layerpot._y1_series_coeffs (layerpot.py:94-103)
+
+enum Kind { K_SELF = 0, K_CROSS, K_WALL, K_REG, K_WALLREG, K_RB, K_INC };
+enum CurveId { C_G1 = 0, C_G2, C_L1, C_L2, C_L3, C_GU, C_GD, C_NCURVE };
+
+struct Task {
+  int kind, src, tgt;
+  int row_v, row_d, col_a, col_b;
+  int nt, ns;              // items = nt * ns
+  int spec;                // interface spec (SELF)
+  int up;                  // RB direction
+  double k, ksub, sign;
+  double cx, cy;           // expansion centre (REG / WALLREG)
+  long long item0;
+};
+
+struct Spec {
+  double mean;
+  int nsin, ncos;
+  double sc[kMaxCoef], cc[kMaxCoef];
+};
+
+struct Tables {
+  Task task[kMaxTasks];
+  int ntask;
+  long long nitems;
+  const double* curve[C_NCURVE];
+  int ncurve[C_NCURVE];
+  Spec spec[2];
+  int m, ncol, copies, Q, nrb;
+  double period, y0, k1, k3;
+  int rule_n, skip, interp;
+  double rule_x[kMaxRule], rule_w[kMaxRule];
+  int lag_start[2][kMaxRule];
+  double lag_w[2][kMaxRule][kMaxRule];
+  double psi[kPsiTerms];
+};
+
+struct RhsPar {   // per incidence angle
+  double ar, ai;        // bloch alpha
+  double kappa;         // k1 cos(theta)
+  double kix, kiy;      // k1 (cos theta, sin theta)
+  double pad;
+};
+
+// ---------------------------------------------------------------- complex helpers
+__device__ __forceinline__ double2 c2(double a, double b) { return make_double2(a, b); }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return c2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return c2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return c2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return c2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 cmuli(double2 a) { return c2(-a.y, a.x); }   // i a
+__device__ __forceinline__ double2 cexpi(double t) {
+  double s, c;
+  sincos(t, &s, &c);
+  return c2(c, s);
+}
+__device__ __forceinline__ double2 cexp(double2 z) {
+  const double e = exp(z.x);
+  double s, c;
+  sincos(z.y, &s, &c);
+  return c2(e * c, e * s);
+}
+// principal complex sqrt of a real number (numpy sqrt of x + 0j)
+__device__ __forceinline__ double2 csqrt_real(double x) {
+  return x >= 0.0 ? c2(sqrt(x), 0.0) : c2(0.0, sqrt(-x));
+}
+
+// alpha^l for small integer l (|alpha| = 1 for real kappa; the inverse is the
+// complex quotient 1 / alpha^|l|, as Python's complex power does)
+__device__ __forceinline__ double2 cpow_int(double2 a, int l) {
+  double2 r = c2(1.0, 0.0);
+  const int n = l < 0 ? -l : l;
+  for (int i = 0; i < n; ++i) r = cmul(r, a);
+  if (l < 0) {
+    const double d = r.x * r.x + r.y * r.y;
+    r = c2(r.x / d, -r.y / d);
+  }
+  return r;
+}
+
+__device__ __forceinline__ void hankel01(double z, double2* h0, double2* h1) {
+  double j0, j1, y0, y1;
+  bessel_jy01(z, miller_start_j01(z), &j0, &j1, &y0, &y1);
+  *h0 = c2(j0, y0);
+  *h1 = c2(j1, y1);
+}
+
+// The four Helmholtz kernels at one (target, source) pair, target-minus-source
+// vector (u0, u1): layerpot._kernel_values_diff (layerpot.py:69-91).
+struct K4 {
+  double2 S, D, N, T;
+};
+__device__ __forceinline__ K4 kernel4(double k, double u0, double u1, double tnx, double tny,
+                                      double snx, double sny) {
+  const double r = hypot(u0, u1);
+  double2 h0, h1;
+  hankel01(k * r, &h0, &h1);
+  const double udy = (u0 * snx + u1 * sny) / r;
+  const double udx = (u0 * tnx + u1 * tny) / r;
+  const double nxny = tnx * snx + tny * sny;
+  K4 o;
+  o.S = cmuli(cscale(h0, 0.25));
+  o.D = cmuli(cscale(h1, 0.25 * k * udy));
+  o.N = cmuli(cscale(h1, -0.25 * k * udx));
+  const double2 h1p = csub(h0, cscale(h1, 1.0 / (k * r)));
+  const double2 t = cadd(cscale(h1p, k * udx * udy), cscale(h1, (nxny - udx * udy) / r));
+  o.T = cmuli(cscale(t, 0.25 * k));
+  return o;
+}
+
+// T^{ka} - T^{kb} with the 1/r^2 singularity removed (layerpot.py:106-141).
+__device__ double2 t_difference(const Tables& tb, double ka, double kb, double u0, double u1,
+                                double tnx, double tny, double snx, double sny) {
+  const double r = hypot(u0, u1);
+  const double p = ((u0 * tnx + u1 * tny) * (u0 * snx + u1 * sny)) / (r * r);
+  const double nxny = tnx * snx + tny * sny;
+  double ja0, ja1, ya0, ya1, jb0, jb1, yb0, yb1;
+  bessel_jy01(ka * r, miller_start_j01(ka * r), &ja0, &ja1, &ya0, &ya1);
+  bessel_jy01(kb * r, miller_start_j01(kb * r), &jb0, &jb1, &yb0, &yb1);
+  const double2 h0t = csub(cscale(c2(ja0, ya0), ka * ka), cscale(c2(jb0, yb0), kb * kb));
+  const double wj = (ka * ja1 - kb * jb1) / r;
+  double wy;
+  if (fmax(ka, kb) * r < 1.0) {
+    auto smooth = [&](double k, double j1) {
+      const double z = k * r;
+      const double q = -0.25 * z * z;
+      double series = 0.0, qm = 1.0;
+      for (int m = 0; m < kPsiTerms; ++m) {
+        series += tb.psi[m] * qm;
+        qm *= q;
+      }
+      return (2.0 / kPi) * k * k * log(0.5 * z) * (j1 / z) - k * k / (2.0 * kPi) * series;
+    };
+    wy = smooth(ka, ja1) - smooth(kb, jb1);
+  } else {
+    wy = (ka * ya1 - kb * yb1) / r;
+  }
+  const double2 w = c2(wj, wy);
+  return cmuli(cscale(cadd(cscale(h0t, p), cscale(w, nxny - 2.0 * p)), 0.25));
+}
+
+// Interface graph y(x) = mean + sum a_j sin(2 pi j x/d) + b_j cos(2 pi j x/d)
+// at parameter tau (geometry.py:198-207): point, tangent speed, unit normal.
+__device__ void spec_eval(const Spec& s, double d, double tau, double* px, double* py,
+                          double* speed, double* nx, double* ny) {
+  const double x = d * (tau - 0.5);
+  double y = s.mean, dy = 0.0;
+  for (int j = 0; j < s.nsin; ++j) {
+    const double w = 2.0 * kPi * (j + 1) / d;
+    y += s.sc[j] * sin(2.0 * kPi * (j + 1) * x / d);
+    dy += s.sc[j] * w * cos(2.0 * kPi * (j + 1) * x / d);
+  }
+  for (int j = 0; j < s.ncos; ++j) {
+    const double w = 2.0 * kPi * (j + 1) / d;
+    y += s.cc[j] * cos(2.0 * kPi * (j + 1) * x / d);
+    dy -= s.cc[j] * w * sin(2.0 * kPi * (j + 1) * x / d);
+  }
+  *px = x;
+  *py = y;
+  *speed = hypot(d, d * dy);
+  const double nn = hypot(-dy, 1.0);
+  *nx = -dy / nn;
+  *ny = 1.0 / nn;
+}
+
+// x(s) - x(tau) without cancellation (geometry.py:209-217)
+__device__ void spec_diff(const Spec& sp, double d, double s, double tau, double* u0, double* u1) {
+  double dy = 0.0;
+  for (int j = 0; j < sp.nsin; ++j)
+    dy += 2.0 * sp.sc[j] * cos(kPi * (j + 1) * (s + tau - 1.0)) * sin(kPi * (j + 1) * (s - tau));
+  for (int j = 0; j < sp.ncos; ++j)
+    dy -= 2.0 * sp.cc[j] * sin(kPi * (j + 1) * (s + tau - 1.0)) * sin(kPi * (j + 1) * (s - tau));
+  *u0 = d * (s - tau);
+  *u1 = dy;
+}
+
+__device__ __forceinline__ int floordiv(int a, int b) {
+  const int q = a / b;
+  return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+
+// ---------------------------------------------------------------- kernels
+// Alpert off-grid kernel values of the two self blocks:
+// kv[slot][i][side*rule_n + m] = {D, S, T, N} * speed(tau) * w_m h
+// (quadrature.py:166-178, with the stable parameter difference).
+__global__ void alpert_kv_kernel(Tables tb, double2* kv) {
+  const int n = tb.rule_n;
+  const int per_slot_rows[2] = {tb.ncurve[C_G1], tb.ncurve[C_G2]};
+  const int total0 = per_slot_rows[0] * 2 * n;
+  const int total = total0 + per_slot_rows[1] * 2 * n;
+  for (int id = blockIdx.x * blockDim.x + threadIdx.x; id < total; id += gridDim.x * blockDim.x) {
+    const int slot = id < total0 ? 0 : 1;
+    const int rem = id - (slot ? total0 : 0);
+    const int i = rem / (2 * n);
+    const int sm = rem % (2 * n);
+    const int side = sm / n, m = sm % n;
+    const Task& t = tb.task[slot == 0 ? 0 : 2];    // SELF tasks sit at 0 (g1) and 2 (g2)
+    const double* cv = tb.curve[t.src];
+    const int nn = tb.ncurve[t.src];
+    const double h = 1.0 / nn;                      // curve.dt, parameter period 1
+    const double sgn = side == 0 ? 1.0 : -1.0;
+    const double ti = cv[i * kCS + 6];
+    const double tau = ti + sgn * tb.rule_x[m] * h;
+    double px, py, sp, nx, ny;
+    spec_eval(tb.spec[t.spec], tb.period, tau, &px, &py, &sp, &nx, &ny);
+    double u0, u1;
+    spec_diff(tb.spec[t.spec], tb.period, ti, tau, &u0, &u1);
+    const double tnx = cv[i * kCS + 2], tny = cv[i * kCS + 3];
+    const K4 a = kernel4(t.k, u0, u1, tnx, tny, nx, ny);
+    const K4 b = kernel4(t.ksub, u0, u1, tnx, tny, nx, ny);
+    const double2 T = t_difference(tb, t.k, t.ksub, u0, u1, tnx, tny, nx, ny);
+    const double w = sp * (tb.rule_w[m] * h);
+    double2* o = kv + (size_t)id * 4;
+    o[0] = cscale(csub(a.D, b.D), w);
+    o[1] = cscale(csub(a.S, b.S), w);
+    o[2] = cscale(T, w);
+    o[3] = cscale(csub(a.N, b.N), w);
+  }
+}
+
+__device__ __forceinline__ void put(double2* A, int m, int row, int col, double2 v) {
+  A[(size_t)col * m + row] = v;
+}
+
+// regular wave J_n(k r) e^{i n theta} about (cx, cy): value and Cartesian
+// gradient (specialfn.regular_wave_block, specialfn.py:86-125)
+__device__ void regular_wave(double k, double cx, double cy, int n, int nmax, double x, double y,
+                             double2* val, double2* gx, double2* gy) {
+  const double dx = x - cx, dy = y - cy;
+  const double r = hypot(dx, dy);
+  if (r == 0.0) {
+    *val = c2(n == 0 ? 1.0 : 0.0, 0.0);
+    if (n == 1) {
+      *gx = c2(0.5 * k, 0.0);
+      *gy = c2(0.0, 0.5 * k);
+    } else if (n == -1) {
+      *gx = c2(-0.5 * k, 0.0);
+      *gy = c2(0.0, 0.5 * k);
+    } else {
+      *gx = c2(0.0, 0.0);
+      *gy = c2(0.0, 0.0);
+    }
+    return;
+  }
+  const double theta = atan2(dy, dx);
+  const int a0 = n < 0 ? -n : n;
+  const int a1 = (n + 1) < 0 ? -(n + 1) : (n + 1);
+  double ja = 0.0, jb = 0.0, inv, y0, y1;
+  bessel_jy_sweep(k * r, nmax + 1, [&](int nu, double v) {
+    if (nu == a0) ja = v;
+    if (nu == a1) jb = v;
+  }, &inv, &y0, &y1);
+  double jn = ja * inv, jn1 = jb * inv;
+  if (n < 0 && (a0 & 1)) jn = -jn;
+  if (n + 1 < 0 && (a1 & 1)) jn1 = -jn1;
+  const double2 ph = cexpi(n * theta);
+  *val = cscale(ph, jn);
+  const double2 dr = cscale(ph, k * (n * jn / (k * r) - jn1));
+  const double2 dth = cmuli(cscale(ph, n * jn / r));
+  const double ct = cos(theta), st = sin(theta);
+  *gx = csub(cscale(dr, ct), cscale(dth, st));
+  *gy = cadd(cscale(dr, st), cscale(dth, ct));
+}
+
+__global__ void assemble_kernel(Tables tb, const RhsPar* __restrict__ rp,
+                                const double2* __restrict__ kv, double2* __restrict__ Aall,
+                                double2* __restrict__ fall) {
+  const int r = blockIdx.y;
+  const RhsPar P = rp[r];
+  const double2 alpha = c2(P.ar, P.ai);
+  const int m = tb.m;
+  double2* A = Aall + (size_t)r * m * tb.ncol;
+  double2* f = fall + (size_t)r * m;
+  const int cp = tb.copies;
+  for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x; id < tb.nitems;
+       id += (long long)gridDim.x * blockDim.x) {
+    int ti = 0;
+    while (ti + 1 < tb.ntask && tb.task[ti + 1].item0 <= id) ++ti;
+    const Task& t = tb.task[ti];
+    const int loc = (int)(id - t.item0);
+    const int i = loc / t.ns, j = loc % t.ns;
+    const double* tc = tb.curve[t.tgt];
+    const double tx = tc[i * kCS], ty = tc[i * kCS + 1];
+    const double tnx = tc[i * kCS + 2], tny = tc[i * kCS + 3];
+    switch (t.kind) {
+      case K_SELF: {
+        // quadrature.nystrom_selfmatrix, open_periodic window of 2P+1 copies
+        const double* sc = tb.curve[t.src];
+        const int n = t.ns;
+        const double h = 1.0 / n;
+        const double sx0 = sc[j * kCS], sy = sc[j * kCS + 1];
+        const double snx = sc[j * kCS + 2], sny = sc[j * kCS + 3];
+        const double sw = sc[j * kCS + 4] * h;
+        double2 D = c2(0, 0), S = D, T = D, N = D;
+        for (int l = -cp; l <= cp; ++l) {
+          const int off = l * n + j - i;
+          bool band;
+          if (cp == 0) {
+            const int om = ((off % n) + n) % n;
+            band = min(om, n - om) <= tb.skip - 1;
+          } else {
+            band = (off < 0 ? -off : off) <= tb.skip - 1;
+          }
+          if (band) continue;
+          const double u0 = tx - (sx0 + l * tb.period), u1 = ty - sy;
+          const K4 a = kernel4(t.k, u0, u1, tnx, tny, snx, sny);
+          const K4 b = kernel4(t.ksub, u0, u1, tnx, tny, snx, sny);
+          const double2 Td = t_difference(tb, t.k, t.ksub, u0, u1, tnx, tny, snx, sny);
+          const double2 w = cscale(cpow_int(alpha, l), sw);
+          D = cadd(D, cmul(csub(a.D, b.D), w));
+          S = cadd(S, cmul(csub(a.S, b.S), w));
+          T = cadd(T, cmul(Td, w));
+          N = cadd(N, cmul(csub(a.N, b.N), w));
+        }
+        // gathered Alpert corrections (quadrature.py:166-186)
+        const int slot = ti == 0 ? 0 : 1;
+        const int rn = tb.rule_n;
+        const double2* kr = kv + ((size_t)(slot ? tb.ncurve[C_G1] * 2 * rn : 0) +
+                                  (size_t)i * 2 * rn) * 4;
+        for (int side = 0; side < 2; ++side)
+          for (int mm = 0; mm < rn; ++mm) {
+            const int st = tb.lag_start[side][mm];
+            int rr = (j - i - st) % n;
+            if (rr < 0) rr += n;
+            if (rr >= tb.interp) continue;
+            const int qr = i + st + rr;
+            const double2 cw = cscale(cpow_int(alpha, floordiv(qr, n)), tb.lag_w[side][mm][rr]);
+            const double2* q = kr + (size_t)(side * rn + mm) * 4;
+            D = cadd(D, cmul(q[0], cw));
+            S = cadd(S, cmul(q[1], cw));
+            T = cadd(T, cmul(q[2], cw));
+            N = cadd(N, cmul(q[3], cw));
+          }
+        if (i == j) {
+          D.x += 1.0;
+          N.x -= 1.0;
+        }
+        put(A, m, t.row_v + i, t.col_a + j, D);
+        put(A, m, t.row_v + i, t.col_b + j, S);
+        put(A, m, t.row_d + i, t.col_a + j, T);
+        put(A, m, t.row_d + i, t.col_b + j, N);
+        break;
+      }
+      case K_CROSS: {
+        // layerpot.boundary_operator_matrices, disjoint curves (layerpot.py:194-208)
+        const double* sc = tb.curve[t.src];
+        const double sx0 = sc[j * kCS], sy = sc[j * kCS + 1];
+        const double snx = sc[j * kCS + 2], sny = sc[j * kCS + 3];
+        const double aw = sc[j * kCS + 7];
+        double2 D = c2(0, 0), S = D, T = D, N = D;
+        for (int l = -cp; l <= cp; ++l) {
+          const K4 a = kernel4(t.k, tx - (sx0 + l * tb.period), ty - sy, tnx, tny, snx, sny);
+          const double2 w = cpow_int(alpha, l);
+          D = cadd(D, cmul(w, a.D));
+          S = cadd(S, cmul(w, a.S));
+          T = cadd(T, cmul(w, a.T));
+          N = cadd(N, cmul(w, a.N));
+        }
+        const double s = t.sign * aw;
+        put(A, m, t.row_v + i, t.col_a + j, cscale(D, s));
+        put(A, m, t.row_v + i, t.col_b + j, cscale(S, s));
+        put(A, m, t.row_d + i, t.col_a + j, cscale(T, s));
+        put(A, m, t.row_d + i, t.col_b + j, cscale(N, s));
+        break;
+      }
+      case K_WALL: {
+        // telescoped wall discrepancy (layerpot.wall_discrepancy_blocks, lp:211-237)
+        const double* sc = tb.curve[t.src];
+        const double sx0 = sc[j * kCS], sy = sc[j * kCS + 1];
+        const double snx = sc[j * kCS + 2], sny = sc[j * kCS + 3];
+        const double aw = sc[j * kCS + 7];
+        double2 D = c2(0, 0), S = D, T = D, N = D;
+        for (int e = 0; e < 2; ++e) {
+          const int l = e == 0 ? cp : -(cp + 1);
+          const double2 coef = cscale(cpow_int(alpha, e == 0 ? cp + 1 : -cp), e == 0 ? 1.0 : -1.0);
+          const K4 a = kernel4(t.k, tx - (sx0 + l * tb.period), ty - sy, tnx, tny, snx, sny);
+          D = cadd(D, cmul(coef, a.D));
+          S = cadd(S, cmul(coef, a.S));
+          T = cadd(T, cmul(coef, a.T));
+          N = cadd(N, cmul(coef, a.N));
+        }
+        put(A, m, t.row_v + i, t.col_a + j, cscale(D, aw));
+        put(A, m, t.row_v + i, t.col_b + j, cscale(S, aw));
+        put(A, m, t.row_d + i, t.col_a + j, cscale(T, aw));
+        put(A, m, t.row_d + i, t.col_b + j, cscale(N, aw));
+        break;
+      }
+      case K_REG: {
+        // regular-expansion traces (empty_grating._regular_block, eg:121-124)
+        const int n = j - tb.Q;
+        double2 v, gx, gy;
+        regular_wave(t.k, t.cx, t.cy, n, tb.Q, tx, ty, &v, &gx, &gy);
+        const double2 der = cadd(cscale(gx, tnx), cscale(gy, tny));
+        put(A, m, t.row_v + i, t.col_a + j, cscale(v, t.sign));
+        put(A, m, t.row_d + i, t.col_a + j, cscale(der, t.sign));
+        break;
+      }
+      case K_WALLREG: {
+        // alpha * u(L) - u(R) for the layer's regular expansion (eg:215-218)
+        const int n = j - tb.Q;
+        double2 vl, gl, gyl, vr, gr, gyr;
+        regular_wave(t.k, t.cx, t.cy, n, tb.Q, tx, ty, &vl, &gl, &gyl);
+        regular_wave(t.k, t.cx, t.cy, n, tb.Q, tx + tb.period, ty, &vr, &gr, &gyr);
+        put(A, m, t.row_v + i, t.col_a + j, csub(cmul(alpha, vl), vr));
+        put(A, m, t.row_d + i, t.col_a + j, csub(cmul(alpha, gl), gr));
+        break;
+      }
+      case K_RB: {
+        // Rayleigh-Bloch modes on the artificial boundary (empty_grating.rb_basis, eg:44-61)
+        const int half = tb.nrb / 2;
+        const double kapn = P.kappa + 2.0 * kPi * (double)(j - half) / tb.period;
+        const double k = t.up ? tb.k1 : tb.k3;
+        // k^2 - kappa_n^2 rounded exactly as numpy does (no FMA contraction):
+        // at a Wood anomaly it is a near-cancellation and kyn ~ 1e-7
+        const double2 kyn = csqrt_real(__dsub_rn(__dmul_rn(k, k), __dmul_rn(kapn, kapn)));
+        const double2 ph = cexpi(tx * kapn);
+        const double yy = t.up ? (ty - tb.y0) : (-ty - tb.y0);
+        const double2 vert = cexp(cmuli(cscale(kyn, yy)));
+        double2 dvert = cmul(cmuli(kyn), vert);
+        if (!t.up) dvert = cscale(dvert, -1.0);
+        put(A, m, t.row_v + i, t.col_a + j, cscale(cmul(ph, vert), -1.0));
+        put(A, m, t.row_d + i, t.col_a + j, cscale(cmul(ph, dvert), -1.0));
+        break;
+      }
+      case K_INC: {
+        // f = -(incident trace) on Gamma1 (empty_grating.incident_field, eg:32-42, 241-245)
+        const double2 v = cexpi(tx * P.kix + ty * P.kiy);
+        const double2 dv = cmul(c2(0.0, tnx * P.kix + tny * P.kiy), v);
+        f[t.row_v + i] = cscale(v, -1.0);
+        f[t.row_d + i] = cscale(dv, -1.0);
+        break;
+      }
+    }
+  }
+}
+
+// Column scaling of the expansion and Rayleigh-Bloch columns to unit max
+// magnitude (eg:247-254).  grid (ncol - col0, nrhs); cs [nrhs][ncol].
+__global__ void colscale_kernel(double2* __restrict__ Aall, double* __restrict__ csall, int m,
+                                int ncol, int col0) {
+  const int r = blockIdx.y;
+  const int col = blockIdx.x;
+  double2* a = Aall + (size_t)r * m * ncol + (size_t)col * m;
+  double* cs = csall + (size_t)r * ncol;
+  __shared__ double red[32];
+  if (col < col0) {
+    if (threadIdx.x == 0) cs[col] = 1.0;
+    return;
+  }
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) mx = fmax(mx, hypot(a[i].x, a[i].y));
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    mx = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (threadIdx.x == 0) red[0] = mx;
+  }
+  __syncthreads();
+  mx = red[0];
+  if (mx == 0.0) mx = 1.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) a[i] = c2(a[i].x / mx, a[i].y / mx);
+  if (threadIdx.x == 0) cs[col] = 1.0 / mx;
+}
+
+// Restricted A^+ factors from the device SVD (what ps_set_pinv builds on the
+// host): Uh[k][i] = conj(U[i][k]) for the C rows, sinv, Vb[o][k] =
+// conj(Vh[k][col(o)]), the column scales of the output columns and f on the C
+// rows.  U column-major [ncol][m], VT column-major [ncol][ncol] (= Vh).
+__global__ void pinv_extract_kernel(const double2* __restrict__ U, const double* __restrict__ s,
+                                    const double2* __restrict__ VT,
+                                    const double* __restrict__ cs_full,
+                                    const double2* __restrict__ f_full, int m, int ncol, int nrc,
+                                    int ncol_b, int nrb, int col_c, int col_d, double eps,
+                                    double2* Uh, double* sinv, double2* Vb, double* cs,
+                                    double2* f, int v_is_V) {
+  const int nout = ncol_b + 2 * nrb;
+  const long long nu = (long long)ncol * nrc, nv = (long long)nout * ncol;
+  const long long tot = nu + nv + ncol + nout + nrc;
+  for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x; id < tot;
+       id += (long long)gridDim.x * blockDim.x) {
+    if (id < nu) {
+      const int k = (int)(id / nrc), i = (int)(id % nrc);
+      const double2 u = U[(size_t)k * m + i];
+      Uh[id] = c2(u.x, -u.y);
+    } else if (id < nu + nv) {
+      const long long q = id - nu;
+      const int o = (int)(q / ncol), k = (int)(q % ncol);
+      const int col = o < ncol_b ? o : (o < ncol_b + nrb ? col_c + o - ncol_b : col_d + o - ncol_b - nrb);
+      if (v_is_V) {   // V column-major: Vh[k][col] = conj(V[col][k])
+        Vb[q] = VT[(size_t)k * ncol + col];
+      } else {        // VT column-major = Vh
+        const double2 v = VT[(size_t)col * ncol + k];
+        Vb[q] = c2(v.x, -v.y);
+      }
+    } else if (id < nu + nv + ncol) {
+      const int k = (int)(id - nu - nv);
+      sinv[k] = fmin(1.0 / s[k], 1.0 / eps);
+    } else if (id < nu + nv + ncol + nout) {
+      const int o = (int)(id - nu - nv - ncol);
+      const int col = o < ncol_b ? o : (o < ncol_b + nrb ? col_c + o - ncol_b : col_d + o - ncol_b - nrb);
+      cs[o] = cs_full[col];
+    } else {
+      const int i = (int)(id - nu - nv - ncol - nout);
+      f[i] = f_full[i];
+    }
+  }
+}
+
+// one cuSOLVER handle + workspace per (device, worker); created lazily and
+// kept for the process (cusolverDnCreate costs tens of ms)
+struct SvdWorker {
+  cusolverDnHandle_t h = nullptr;
+  cudaStream_t st = nullptr;
+  void* work = nullptr;
+  size_t work_bytes = 0;
+  double2 *A = nullptr, *U = nullptr, *VT = nullptr;
+  double* rwork = nullptr;
+  int* info = nullptr;
+  int m = 0, n = 0, method = -1;
+  cusolverDnParams_t params = nullptr;
+  std::vector<char> host_work;
+};
+std::mutex g_svd_mu;
+std::mutex g_dev_mu[64];   // one SVD phase per device at a time
+std::vector<SvdWorker> g_svd[64];
+
+std::string svd_err(const char* what, int code) {
+  return std::string(what) + " failed (status " + std::to_string(code) + ")";
+}
+
+// A (m x n column-major, m >= n, on the device) -> U, s and VT (method 0,
+// zgesvd: Golub-Kahan bidiagonalisation + QR, what LAPACK gesdd computes) or V
+// (method 1, Xgesvdp: QDWH polar decomposition + Hermitian eigensolver) in the
+// worker's buffers; blocks the calling thread until done.
+int svd_run(SvdWorker& w, const double2* A, int m, int n, int method, double* s,
+            std::string* err) {
+  if (!w.h) {
+    if (cudaStreamCreateWithFlags(&w.st, cudaStreamNonBlocking) != cudaSuccess) {
+      *err = "svd: stream create";
+      return PS_ERR_CUDA;
+    }
+    cusolverStatus_t cs = cusolverDnCreate(&w.h);
+    if (cs != CUSOLVER_STATUS_SUCCESS) {
+      *err = svd_err("cusolverDnCreate", cs);
+      return PS_ERR_CUDA;
+    }
+    cusolverDnSetStream(w.h, w.st);
+    cs = cusolverDnCreateParams(&w.params);
+    if (cs != CUSOLVER_STATUS_SUCCESS) {
+      *err = svd_err("cusolverDnCreateParams", cs);
+      return PS_ERR_CUDA;
+    }
+  }
+  if (w.m != m || w.n != n || w.method != method) {
+    void* bufs[] = {w.work, w.A, w.U, w.VT, w.rwork, w.info};
+    for (void* p : bufs)
+      if (p) dev_free(p);
+    w.work = nullptr;
+    size_t dev_bytes = 0, host_bytes = 0;
+    if (method == 0) {
+      int lwork = 0;
+      cusolverStatus_t cs = cusolverDnZgesvd_bufferSize(w.h, m, n, &lwork);
+      if (cs != CUSOLVER_STATUS_SUCCESS) {
+        *err = svd_err("cusolverDnZgesvd_bufferSize", cs);
+        return PS_ERR_CUDA;
+      }
+      dev_bytes = (size_t)lwork * sizeof(double2);
+    } else {
+      cusolverStatus_t cs = cusolverDnXgesvdp_bufferSize(
+          w.h, w.params, CUSOLVER_EIG_MODE_VECTOR, 1, m, n, CUDA_C_64F, nullptr, m, CUDA_R_64F,
+          nullptr, CUDA_C_64F, nullptr, m, CUDA_C_64F, nullptr, n, CUDA_C_64F, &dev_bytes,
+          &host_bytes);
+      if (cs != CUSOLVER_STATUS_SUCCESS) {
+        *err = svd_err("cusolverDnXgesvdp_bufferSize", cs);
+        return PS_ERR_CUDA;
+      }
+    }
+    w.work_bytes = dev_bytes;
+    w.host_work.assign(host_bytes + 1, 0);
+    if (dev_malloc(&w.work, w.work_bytes + 16) != cudaSuccess ||
+        dev_malloc(&w.A, (size_t)m * n * sizeof(double2)) != cudaSuccess ||
+        dev_malloc(&w.U, (size_t)m * n * sizeof(double2)) != cudaSuccess ||
+        dev_malloc(&w.VT, (size_t)n * n * sizeof(double2)) != cudaSuccess ||
+        dev_malloc(&w.rwork, (size_t)n * sizeof(double)) != cudaSuccess ||
+        dev_malloc(&w.info, sizeof(int)) != cudaSuccess) {
+      *err = "svd: workspace allocation";
+      return PS_ERR_CUDA;
+    }
+    w.m = m;
+    w.n = n;
+    w.method = method;
+  }
+  if (cudaMemcpyAsync(w.A, A, (size_t)m * n * sizeof(double2), cudaMemcpyDeviceToDevice, w.st) !=
+      cudaSuccess) {
+    *err = "svd: copy";
+    return PS_ERR_CUDA;
+  }
+  cusolverStatus_t cs;
+  if (method == 0) {
+    const int lwork = (int)(w.work_bytes / sizeof(double2));
+    cs = cusolverDnZgesvd(w.h, 'S', 'S', m, n, reinterpret_cast<cuDoubleComplex*>(w.A), m, s,
+                          reinterpret_cast<cuDoubleComplex*>(w.U), m,
+                          reinterpret_cast<cuDoubleComplex*>(w.VT), n,
+                          reinterpret_cast<cuDoubleComplex*>(w.work), lwork, w.rwork, w.info);
+  } else {
+    double err_sigma = 0.0;
+    cs = cusolverDnXgesvdp(w.h, w.params, CUSOLVER_EIG_MODE_VECTOR, 1, m, n, CUDA_C_64F, w.A, m,
+                           CUDA_R_64F, s, CUDA_C_64F, w.U, m, CUDA_C_64F, w.VT, n, CUDA_C_64F,
+                           w.work, w.work_bytes, w.host_work.data(), w.host_work.size() - 1,
+                           w.info, &err_sigma);
+  }
+  if (cs != CUSOLVER_STATUS_SUCCESS) {
+    *err = svd_err(method == 0 ? "cusolverDnZgesvd" : "cusolverDnXgesvdp", cs);
+    return PS_ERR_CUDA;
+  }
+  int info = 0;
+  cudaMemcpyAsync(&info, w.info, sizeof(int), cudaMemcpyDeviceToHost, w.st);
+  if (cudaStreamSynchronize(w.st) != cudaSuccess) {
+    *err = "svd: synchronize";
+    return PS_ERR_CUDA;
+  }
+  if (info != 0) {
+    *err = std::string(method == 0 ? "zgesvd" : "gesvdp") + ": info = " + std::to_string(info) +
+           " (did not converge)";
+    return PS_ERR_NUMERICAL;
+  }
+  return PS_OK;
+}
+
+// quadrature._lagrange_weights (quadrature.py:91-101)
+void lagrange(double frac, int interp, int* start, double* w) {
+  const int st = (int)std::floor(frac) - (interp / 2 - 1);
+  *start = st;
+  for (int r = 0; r < interp; ++r) {
+    double v = 1.0;
+    for (int q = 0; q < interp; ++q)
+      if (q != r) v *= (frac - (double)(st + q)) / (double)((st + r) - (st + q));
+    w[r] = v;
+  }
+}
+
+}  // namespace
+
+// per-context storage of the device-assembled systems
+struct EmptyState {
+  int m = 0, ncol = 0, nrhs = 0;
+  double* d_curves = nullptr;        // all curves, kCS doubles per node
+  double2* d_kv = nullptr;           // Alpert off-grid kernel values
+  RhsPar* d_rp = nullptr;
+  double2* d_A = nullptr;            // [nrhs][ncol][m] column-scaled, column-major
+  double2* d_f = nullptr;            // [nrhs][m]
+  double* d_cs = nullptr;            // [nrhs][ncol]
+  double* d_s = nullptr;             // [nrhs][ncol] singular values
+  double t_assemble_ms = 0, t_svd_ms = 0;
+};
+
+void empty_release(Ctx* c) {
+  if (!c->empty) return;
+  EmptyState* e = c->empty;
+  void* ptrs[] = {e->d_curves, e->d_kv, e->d_rp, e->d_A, e->d_f, e->d_cs, e->d_s};
+  for (void* p : ptrs)
+    if (p) dev_free(p);
+  delete e;
+  c->empty = nullptr;
+}
+
+}  // namespace ps
+
+using ps::Ctx;
+
+namespace {
+
+int fail(Ctx* c, int code, const std::string& msg) {
+  c->err = msg;
+  return code;
+}
+
+#define PS_TRY_CUDA(call)                                                           \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(c, PS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <typename T>
+int upload(Ctx* c, T** dst, const T* src, size_t n) {
+  if (*dst) ps::dev_free(*dst);
+  *dst = nullptr;
+  if (n == 0) return PS_OK;
+  PS_TRY_CUDA(ps::dev_malloc(reinterpret_cast<void**>(dst), n * sizeof(T)));
+  if (src) PS_TRY_CUDA(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  return PS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ps_setup_empty(ps_ctx* h, const ps_empty_desc* ds, const double* theta) {
+  using namespace ps;
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = ps::C(h);
+  release_dense_coupling(c);
+  if (!ds || !theta) return fail(c, PS_ERR_ARG, "ps_setup_empty: null argument");
+  const ps_curve_desc* cvs[C_NCURVE] = {&ds->g1, &ds->g2, &ds->wall[0], &ds->wall[1],
+                                        &ds->wall[2], &ds->lid_up, &ds->lid_down};
+  for (auto* cv : cvs)
+    if (cv->n <= 0 || !cv->data) return fail(c, PS_ERR_ARG, "ps_setup_empty: empty curve");
+  if (!(ds->period > 0) || !(ds->k1 > 0) || !(ds->k2 > 0) || !(ds->k3 > 0) || ds->copies < 0 ||
+      ds->Q < 0 || ds->nrb <= 0 || (ds->nrb % 2) == 0 || !(ds->eps > 0))
+    return fail(c, PS_ERR_ARG, "ps_setup_empty: bad scalar parameter");
+  if (ds->rule_n <= 0 || ds->rule_n > kMaxRule || ds->rule_interp <= 0 ||
+      ds->rule_interp > kMaxRule || ds->rule_skip <= 0 || !ds->rule_x || !ds->rule_w)
+    return fail(c, PS_ERR_ARG, "ps_setup_empty: bad correction rule");
+  if (ds->g1.n < 4 * ds->rule_skip || ds->g2.n < 4 * ds->rule_skip)
+    return fail(c, PS_ERR_ARG, "ps_setup_empty: need at least 4*skip interface nodes "
+                               "(quadrature.py:127-128)");
+  const ps_interface_desc* sp[2] = {&ds->top, &ds->bottom};
+  for (auto* s : sp)
+    if (s->nsin < 0 || s->ncos < 0 || s->nsin > kMaxCoef || s->ncos > kMaxCoef ||
+        (s->nsin && !s->sin_coeffs) || (s->ncos && !s->cos_coeffs))
+      return fail(c, PS_ERR_UNSUPPORTED, "ps_setup_empty: at most 8 sin/cos coefficients per interface");
+  if (c->nrhs < 1 || (int)c->rhs.size() < c->nrhs)
+    return fail(c, PS_ERR_STATE, "ps_setup_empty: call ps_set_rhs_bloch first");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, PS_ERR_CUDA, "cudaSetDevice");
+
+  const int n1 = ds->g1.n, n2 = ds->g2.n;
+  const int nw1 = ds->wall[0].n, nw2 = ds->wall[1].n, nw3 = ds->wall[2].n;
+  const int nu = ds->lid_up.n, nd = ds->lid_down.n;
+  const int nj = 2 * ds->Q + 1, nrb = ds->nrb;
+  // column layout eg:154-156 and row layout eg:157-160
+  const int c_mu1 = 0, c_s1 = n1, c_mu2 = 2 * n1, c_s2 = 2 * n1 + n2, c_a2 = 2 * n1 + 2 * n2;
+  const int c_a1 = c_a2 + nj, c_a3 = c_a1 + nj, c_c = c_a3 + nj, c_d = c_c + nrb;
+  const int ncol = c_d + nrb;
+  const int r_g1 = 0, r_g2 = 2 * n1, r_w2 = 2 * n1 + 2 * n2, r_w1 = r_w2 + 2 * nw2;
+  const int r_w3 = r_w1 + 2 * nw1, r_gu = r_w3 + 2 * nw3, r_gd = r_gu + 2 * nu;
+  const int m = r_gd + 2 * nd;
+  if (m < ncol) return fail(c, PS_ERR_ARG, "ps_setup_empty: fewer rows than unknowns");
+
+  Tables tb{};
+  tb.m = m;
+  tb.ncol = ncol;
+  tb.copies = ds->copies;
+  tb.Q = ds->Q;
+  tb.nrb = nrb;
+  tb.period = ds->period;
+  tb.y0 = ds->y0;
+  tb.k1 = ds->k1;
+  tb.k3 = ds->k3;
+  tb.rule_n = ds->rule_n;
+  tb.skip = ds->rule_skip;
+  tb.interp = ds->rule_interp;
+  for (int i = 0; i < ds->rule_n; ++i) {
+    tb.rule_x[i] = ds->rule_x[i];
+    tb.rule_w[i] = ds->rule_w[i];
+    for (int side = 0; side < 2; ++side)
+      lagrange((side == 0 ? 1.0 : -1.0) * ds->rule_x[i], ds->rule_interp, &tb.lag_start[side][i],
+               tb.lag_w[side][i]);
+  }
+  // (psi(m+1) + psi(m+2)) / (m! (m+1)!)  with psi(n) = -gamma + H_{n-1}
+  {
+    long double harm = 0.0L, fact = 1.0L;   // H_m, m!
+    for (int mm = 0; mm < kPsiTerms; ++mm) {
+      if (mm > 0) {
+        harm += 1.0L / mm;
+        fact *= mm;
+      }
+      const long double g = 0.577215664901532860606512090082402431L;
+      const long double psi1 = -g + harm, psi2 = -g + harm + 1.0L / (mm + 1);
+      tb.psi[mm] = (double)((psi1 + psi2) / (fact * fact * (mm + 1)));
+    }
+  }
+  for (int s = 0; s < 2; ++s) {
+    tb.spec[s].mean = sp[s]->mean;
+    tb.spec[s].nsin = sp[s]->nsin;
+    tb.spec[s].ncos = sp[s]->ncos;
+    for (int j = 0; j < sp[s]->nsin; ++j) tb.spec[s].sc[j] = sp[s]->sin_coeffs[j];
+    for (int j = 0; j < sp[s]->ncos; ++j) tb.spec[s].cc[j] = sp[s]->cos_coeffs[j];
+  }
+  // curves -> one device buffer
+  if (!c->empty) c->empty = new EmptyState();
+  EmptyState* e = c->empty;
+  size_t tot = 0;
+  for (auto* cv : cvs) tot += (size_t)cv->n * kCS;
+  std::vector<double> hc(tot);
+  {
+    size_t o = 0;
+    for (auto* cv : cvs) {
+      std::copy(cv->data, cv->data + (size_t)cv->n * kCS, hc.begin() + o);
+      o += (size_t)cv->n * kCS;
+    }
+  }
+  if (int rc = upload(c, &e->d_curves, hc.data(), tot)) return rc;
+  {
+    size_t o = 0;
+    for (int i = 0; i < C_NCURVE; ++i) {
+      tb.curve[i] = e->d_curves + o;
+      tb.ncurve[i] = cvs[i]->n;
+      o += (size_t)cvs[i]->n * kCS;
+    }
+  }
+  const double* ctr = ds->centers;   // centres 1, 2, 3
+  auto add = [&](Task t) { tb.task[tb.ntask++] = t; };
+  auto pair = [&](int kind, int src, int tgt, int rv, int rd, int ca, int cb, double k,
+                  double ksub, double sign, int spec) {
+    Task t{};
+    t.kind = kind; t.src = src; t.tgt = tgt; t.row_v = rv; t.row_d = rd; t.col_a = ca;
+    t.col_b = cb; t.nt = cvs[tgt]->n; t.ns = cvs[src]->n; t.k = k; t.ksub = ksub;
+    t.sign = sign; t.spec = spec;
+    add(t);
+  };
+  auto reg = [&](int kind, int tgt, int rv, int rd, int ca, double k, int cid, double sign) {
+    Task t{};
+    t.kind = kind; t.src = tgt; t.tgt = tgt; t.row_v = rv; t.row_d = rd; t.col_a = ca;
+    t.nt = cvs[tgt]->n; t.ns = nj; t.k = k; t.sign = sign;
+    t.cx = ctr[2 * (cid - 1)]; t.cy = ctr[2 * (cid - 1) + 1];
+    add(t);
+  };
+  const double k1 = ds->k1, k2 = ds->k2, k3 = ds->k3;
+  // interface continuity rows (eg:166-192); SELF tasks must stay at 0 and 2
+  pair(K_SELF, C_G1, C_G1, r_g1, r_g1 + n1, c_mu1, c_s1, k1, k2, 1.0, 0);
+  pair(K_CROSS, C_G2, C_G1, r_g1, r_g1 + n1, c_mu2, c_s2, k2, 0, -1.0, 0);
+  pair(K_SELF, C_G2, C_G2, r_g2, r_g2 + n2, c_mu2, c_s2, k2, k3, 1.0, 1);
+  pair(K_CROSS, C_G1, C_G2, r_g2, r_g2 + n2, c_mu1, c_s1, k2, 0, 1.0, 0);
+  // regular-expansion traces (eg:194-202)
+  reg(K_REG, C_G1, r_g1, r_g1 + n1, c_a2, k2, 2, -1.0);
+  reg(K_REG, C_G1, r_g1, r_g1 + n1, c_a1, k1, 1, 1.0);
+  reg(K_REG, C_G2, r_g2, r_g2 + n2, c_a2, k2, 2, 1.0);
+  reg(K_REG, C_G2, r_g2, r_g2 + n2, c_a3, k3, 3, -1.0);
+  // wall discrepancy rows (eg:204-224)
+  pair(K_WALL, C_G1, C_L2, r_w2, r_w2 + nw2, c_mu1, c_s1, k2, 0, 1.0, 0);
+  pair(K_WALL, C_G2, C_L2, r_w2, r_w2 + nw2, c_mu2, c_s2, k2, 0, 1.0, 0);
+  reg(K_WALLREG, C_L2, r_w2, r_w2 + nw2, c_a2, k2, 2, 1.0);
+  pair(K_WALL, C_G1, C_L1, r_w1, r_w1 + nw1, c_mu1, c_s1, k1, 0, 1.0, 0);
+  reg(K_WALLREG, C_L1, r_w1, r_w1 + nw1, c_a1, k1, 1, 1.0);
+  pair(K_WALL, C_G2, C_L3, r_w3, r_w3 + nw3, c_mu2, c_s2, k3, 0, 1.0, 0);
+  reg(K_WALLREG, C_L3, r_w3, r_w3 + nw3, c_a3, k3, 3, 1.0);
+  // artificial-boundary rows (eg:226-239)
+  pair(K_CROSS, C_G1, C_GU, r_gu, r_gu + nu, c_mu1, c_s1, k1, 0, 1.0, 0);
+  reg(K_REG, C_GU, r_gu, r_gu + nu, c_a1, k1, 1, 1.0);
+  {
+    Task t{};
+    t.kind = K_RB; t.src = t.tgt = C_GU; t.row_v = r_gu; t.row_d = r_gu + nu; t.col_a = c_c;
+    t.nt = nu; t.ns = nrb; t.up = 1;
+    add(t);
+  }
+  pair(K_CROSS, C_G2, C_GD, r_gd, r_gd + nd, c_mu2, c_s2, k3, 0, 1.0, 0);
+  reg(K_REG, C_GD, r_gd, r_gd + nd, c_a3, k3, 3, 1.0);
+  {
+    Task t{};
+    t.kind = K_RB; t.src = t.tgt = C_GD; t.row_v = r_gd; t.row_d = r_gd + nd; t.col_a = c_d;
+    t.nt = nd; t.ns = nrb; t.up = 0;
+    add(t);
+  }
+  {
+    Task t{};
+    t.kind = K_INC; t.src = t.tgt = C_G1; t.row_v = r_g1; t.row_d = r_g1 + n1; t.nt = n1; t.ns = 1;
+    add(t);
+  }
+  long long items = 0;
+  for (int i = 0; i < tb.ntask; ++i) {
+    tb.task[i].item0 = items;
+    items += (long long)tb.task[i].nt * tb.task[i].ns;
+  }
+  tb.nitems = items;
+
+  const int R = c->nrhs;
+  std::vector<RhsPar> hp(R);
+  for (int r = 0; r < R; ++r) {
+    hp[r].ar = c->rhs[r].bloch.x;
+    hp[r].ai = c->rhs[r].bloch.y;
+    hp[r].kappa = ds->k1 * std::cos(theta[r]);
+    hp[r].kix = ds->k1 * std::cos(theta[r]);
+    hp[r].kiy = ds->k1 * std::sin(theta[r]);
+  }
+  if (int rc = upload(c, &e->d_rp, hp.data(), (size_t)R)) return rc;
+  const size_t kv_n = (size_t)(n1 + n2) * 2 * ds->rule_n * 4;
+  if (int rc = upload<double2>(c, &e->d_kv, nullptr, kv_n)) return rc;
+  if (e->m != m || e->ncol != ncol || e->nrhs != R || !e->d_A) {
+    if (int rc = upload<double2>(c, &e->d_A, nullptr, (size_t)R * m * ncol)) return rc;
+    if (int rc = upload<double2>(c, &e->d_f, nullptr, (size_t)R * m)) return rc;
+    if (int rc = upload<double>(c, &e->d_cs, nullptr, (size_t)R * ncol)) return rc;
+    if (int rc = upload<double>(c, &e->d_s, nullptr, (size_t)R * ncol)) return rc;
+    e->m = m;
+    e->ncol = ncol;
+    e->nrhs = R;
+  }
+
+  cudaEvent_t e0, e1, e2;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreate(&e2);
+  cudaStream_t st = 0;
+  cudaEventRecord(e0, st);
+  PS_TRY_CUDA(cudaMemsetAsync(e->d_A, 0, (size_t)R * m * ncol * sizeof(double2), st));
+  PS_TRY_CUDA(cudaMemsetAsync(e->d_f, 0, (size_t)R * m * sizeof(double2), st));
+  {
+    const int tot_kv = (n1 + n2) * 2 * ds->rule_n;
+    alpert_kv_kernel<<<(tot_kv + 127) / 128, 128, 0, st>>>(tb, e->d_kv);
+    const int blocks = (int)std::min<long long>((items + 127) / 128, (long long)c->sm_count * 8);
+    assemble_kernel<<<dim3(blocks, R), 128, 0, st>>>(tb, e->d_rp, e->d_kv, e->d_A, e->d_f);
+    colscale_kernel<<<dim3(ncol, R), 256, 0, st>>>(e->d_A, e->d_cs, m, ncol, c_a2);
+    c->launches += 3;
+  }
+  PS_TRY_CUDA(cudaGetLastError());
+  cudaEventRecord(e1, st);
+  PS_TRY_CUDA(cudaStreamSynchronize(st));
+
+  // restricted factor layout of ps_set_pinv
+  c->n1 = n1;
+  c->n2 = n2;
+  c->nw = nw2;
+  c->Q = ds->Q;
+  c->nrb = nrb;
+  c->x2[0] = ctr[2];
+  c->x2[1] = ctr[3];
+  c->nrow_c = 2 * n1 + 2 * n2 + 2 * nw2;
+  c->ncol_b = 2 * n1 + 2 * n2 + nj;
+  {
+    // coupling node records [n][5] (x, y, nx, ny, arc weight) and L2 wall nodes
+    std::vector<double> g1(5 * (size_t)n1), g2(5 * (size_t)n2), w2(2 * (size_t)nw2);
+    for (int i = 0; i < n1; ++i) {
+      const double* q = ds->g1.data + (size_t)i * kCS;
+      double v[5] = {q[0], q[1], q[2], q[3], q[7]};
+      std::copy(v, v + 5, g1.begin() + 5 * (size_t)i);
+    }
+    for (int i = 0; i < n2; ++i) {
+      const double* q = ds->g2.data + (size_t)i * kCS;
+      double v[5] = {q[0], q[1], q[2], q[3], q[7]};
+      std::copy(v, v + 5, g2.begin() + 5 * (size_t)i);
+    }
+    for (int i = 0; i < nw2; ++i) {
+      w2[2 * i] = ds->wall[1].data[(size_t)i * kCS];
+      w2[2 * i + 1] = ds->wall[1].data[(size_t)i * kCS + 1];
+    }
+    if (int rc = upload(c, &c->d_g1, g1.data(), g1.size())) return rc;
+    if (int rc = upload(c, &c->d_g2, g2.data(), g2.size())) return rc;
+    if (int rc = upload(c, &c->d_w2, w2.data(), w2.size())) return rc;
+    c->have_layers = 1;
+  }
+  const int nsv = ncol, nrc = c->nrow_c, nout = c->ncol_b + 2 * nrb;
+  c->nsv = nsv;
+  for (int r = 0; r < R; ++r) {
+    auto& Rd = c->rhs[r];
+    if (int rc = upload<double2>(c, &Rd.d_Uh, nullptr, (size_t)nsv * nrc)) return rc;
+    if (int rc = upload<double>(c, &Rd.d_sinv, nullptr, (size_t)nsv)) return rc;
+    if (int rc = upload<double2>(c, &Rd.d_Vb, nullptr, (size_t)nout * nsv)) return rc;
+    if (int rc = upload<double>(c, &Rd.d_cscale, nullptr, (size_t)nout)) return rc;
+    if (int rc = upload<double2>(c, &Rd.d_f, nullptr, (size_t)nrc)) return rc;
+  }
+
+  // SVD per right-hand side, up to c->svd_workers concurrent cuSOLVER streams
+  const int dev = c->device;
+  const int nwk = std::max(1, std::min(R, c->svd_workers));
+  std::vector<int> rcs(nwk, PS_OK);
+  std::vector<std::string> errs(nwk);
+  std::lock_guard<std::mutex> dev_lock(g_dev_mu[dev & 63]);
+  {
+    std::lock_guard<std::mutex> lk(g_svd_mu);
+    if ((int)g_svd[dev].size() < nwk) g_svd[dev].resize(nwk);
+  }
+  auto work = [&](int wid) {
+    cudaSetDevice(dev);
+    SvdWorker& w = g_svd[dev][wid];
+    for (int r = wid; r < R; r += nwk) {
+      int rc = svd_run(w, e->d_A + (size_t)r * m * ncol, m, ncol, c->svd_method,
+                       e->d_s + (size_t)r * ncol, &errs[wid]);
+      if (rc) {
+        rcs[wid] = rc;
+        return;
+      }
+      auto& Rd = c->rhs[r];
+      const long long totx = (long long)nsv * nrc + (long long)nout * nsv + nsv + nout + nrc;
+      pinv_extract_kernel<<<(int)std::min<long long>((totx + 255) / 256, 4096), 256, 0, w.st>>>(
+          w.U, e->d_s + (size_t)r * ncol, w.VT, e->d_cs + (size_t)r * ncol,
+          e->d_f + (size_t)r * m, m, ncol, nrc, c->ncol_b, nrb, c_c, c_d, ds->eps, Rd.d_Uh,
+          Rd.d_sinv, Rd.d_Vb, Rd.d_cscale, Rd.d_f, c->svd_method == 1);
+      if (cudaStreamSynchronize(w.st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+        rcs[wid] = PS_ERR_CUDA;
+        errs[wid] = "pinv_extract_kernel failed";
+        return;
+      }
+    }
+  };
+  if (nwk == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int w = 0; w < nwk; ++w) th.emplace_back(work, w);
+    for (auto& t : th) t.join();
+  }
+  c->launches += R;
+  cudaEventRecord(e2, st);
+  cudaEventSynchronize(e2);
+  float ms_a = 0, ms_s = 0;
+  cudaEventElapsedTime(&ms_a, e0, e1);
+  cudaEventElapsedTime(&ms_s, e1, e2);
+  e->t_assemble_ms = ms_a;
+  e->t_svd_ms = ms_s;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  for (int w = 0; w < nwk; ++w)
+    if (rcs[w]) return fail(c, rcs[w], "ps_setup_empty: " + errs[w]);
+  return PS_OK;
+}
+
+int ps_empty_shape(const ps_ctx* h, int* nrow, int* ncol) {
+  if (!h || !nrow || !ncol) return PS_ERR_ARG;
+  const Ctx* c = reinterpret_cast<const Ctx*>(h);
+  if (!c->empty) return PS_ERR_STATE;
+  *nrow = c->empty->m;
+  *ncol = c->empty->ncol;
+  return PS_OK;
+}
+
+int ps_get_empty(ps_ctx* h, int irhs, double* A, double* f, double* col_scale, double* s) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = ps::C(h);
+  ps::EmptyState* e = c->empty;
+  if (!e) return fail(c, PS_ERR_STATE, "ps_get_empty: call ps_setup_empty first");
+  if (irhs < 0 || irhs >= e->nrhs) return fail(c, PS_ERR_ARG, "ps_get_empty: bad rhs index");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, PS_ERR_CUDA, "cudaSetDevice");
+  const int m = e->m, n = e->ncol;
+  if (A) {
+    std::vector<double2> cm((size_t)m * n);
+    PS_TRY_CUDA(cudaMemcpy(cm.data(), e->d_A + (size_t)irhs * m * n, cm.size() * sizeof(double2),
+                           cudaMemcpyDeviceToHost));
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < m; ++i) {
+        A[2 * ((size_t)i * n + j)] = cm[(size_t)j * m + i].x;
+        A[2 * ((size_t)i * n + j) + 1] = cm[(size_t)j * m + i].y;
+      }
+  }
+  if (f)
+    PS_TRY_CUDA(cudaMemcpy(f, e->d_f + (size_t)irhs * m, (size_t)m * sizeof(double2),
+                           cudaMemcpyDeviceToHost));
+  if (col_scale)
+    PS_TRY_CUDA(cudaMemcpy(col_scale, e->d_cs + (size_t)irhs * n, (size_t)n * sizeof(double),
+                           cudaMemcpyDeviceToHost));
+  if (s)
+    PS_TRY_CUDA(cudaMemcpy(s, e->d_s + (size_t)irhs * n, (size_t)n * sizeof(double),
+                           cudaMemcpyDeviceToHost));
+  return PS_OK;
+}
+
+int ps_set_svd_workers(ps_ctx* h, int workers) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = ps::C(h);
+  if (workers < 1 || workers > 32) return fail(c, PS_ERR_ARG, "ps_set_svd_workers: 1..32");
+  c->svd_workers = workers;
+  return PS_OK;
+}
+
+int ps_set_svd_method(ps_ctx* h, int method) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = ps::C(h);
+  if (method < 0 || method > 1) return fail(c, PS_ERR_ARG, "ps_set_svd_method: 0 gesvd, 1 gesvdp");
+  c->svd_method = method;
+  return PS_OK;
+}
+
+int ps_setup_timings(const ps_ctx* h, double* assemble_ms, double* svd_ms) {
+  if (!h || !assemble_ms || !svd_ms) return PS_ERR_ARG;
+  const Ctx* c = reinterpret_cast<const Ctx*>(h);
+  if (!c->empty) return PS_ERR_STATE;
+  *assemble_ms = c->empty->t_assemble_ms;
+  *svd_ms = c->empty->t_svd_ms;
+  return PS_OK;
+}
+
+}  // extern "C"

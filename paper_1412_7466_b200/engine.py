@@ -120,6 +120,54 @@ class Engine:
         self.nout = self.ncol_b + 2 * nrb
         self._layer_cols = system.cols
 
+    def set_svd_method(self, method: int):
+        """0 cuSOLVER zgesvd (default), 1 Xgesvdp (see include/periscat_b200.h)."""
+        self._check(self.lib.ps_set_svd_method(self.ctx, int(method)))
+
+    def setup_empty(self, configs, svd_workers: int | None = None):
+        """Device assembly + SVD of the empty-grating system of every RHS
+        (ps_setup_empty; replaces set_layers + set_pinv with host factors).
+        Returns one DeviceEmptySystem per config."""
+        from . import empty_setup as es
+        configs = es.validate(configs)
+        if len(configs) != self.nrhs:
+            raise ValueError("one config per right-hand side (set_bloch first)")
+        cell = es.unit_cell(configs[0])
+        desc, keep = es.build_desc(configs[0], cell)
+        theta = _f64([c.incident_angle for c in configs])
+        if svd_workers is not None:
+            self._check(self.lib.ps_set_svd_workers(self.ctx, int(svd_workers)))
+        self._check(self.lib.ps_setup_empty(self.ctx, ctypes.byref(desc), _ptr(theta)))
+        del keep
+        cfg = configs[0]
+        n1, n2, nw = cell.g1.shape[0], cell.g2.shape[0], cell.walls[1].shape[0]
+        Q, nrb = int(cfg.j_expansion_order), int(cfg.rb_modes_per_direction)
+        self.nrow_c = 2 * n1 + 2 * n2 + 2 * nw
+        self.ncol_b = 2 * n1 + 2 * n2 + 2 * Q + 1
+        self.nrb = nrb
+        self.nout = self.ncol_b + 2 * nrb
+        self._layer_cols = cell.cols
+        self.coupled = True
+        return [es.DeviceEmptySystem(c, cell.cols, cell.rows, cell.centers, self, r)
+                for r, c in enumerate(configs)]
+
+    def get_empty(self, irhs: int):
+        """(A, f, col_scale, s) of a device-assembled RHS (ps_get_empty)."""
+        m, n = ctypes.c_int(), ctypes.c_int()
+        self._check(self.lib.ps_empty_shape(self.ctx, ctypes.byref(m), ctypes.byref(n)))
+        A = np.empty((m.value, n.value), dtype=np.complex128)
+        f = np.empty(m.value, dtype=np.complex128)
+        cs = np.empty(n.value)
+        s = np.empty(n.value)
+        self._check(self.lib.ps_get_empty(self.ctx, int(irhs), _ptr(A), _ptr(f), _ptr(cs), _ptr(s)))
+        return A, f, cs, s
+
+    def setup_timings(self):
+        """Device ms of the last setup_empty: (assembly, SVD + factor restriction)."""
+        a, s = ctypes.c_double(), ctypes.c_double()
+        self._check(self.lib.ps_setup_timings(self.ctx, ctypes.byref(a), ctypes.byref(s)))
+        return a.value, s.value
+
     def set_pinv(self, irhs: int, system):
         """Upload the SVD factors of one RHS's system (computed if absent)."""
         factorize(system)

@@ -22,9 +22,42 @@ import numpy as np
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
 
 
+@dataclass(frozen=True)
+class InterfaceSpec:
+    """Graph interface y(x) = mean + sum_j a_j sin(2 pi j x/d) + b_j cos(2 pi j x/d)
+    (duck type of geometry.InterfaceSpec, geometry.py:67-96)."""
+    mean: float
+    sin_coeffs: tuple = ()
+    cos_coeffs: tuple = ()
+
+    def height(self, x, d: float = 1.0):
+        x = np.asarray(x, dtype=float)
+        y = np.full_like(x, self.mean)
+        for j, a in enumerate(self.sin_coeffs, start=1):
+            y = y + a * np.sin(2 * np.pi * j * x / d)
+        for j, b in enumerate(self.cos_coeffs, start=1):
+            y = y + b * np.cos(2 * np.pi * j * x / d)
+        return y
+
+    def slope(self, x, d: float = 1.0):
+        x = np.asarray(x, dtype=float)
+        dy = np.zeros_like(x)
+        for j, a in enumerate(self.sin_coeffs, start=1):
+            dy = dy + a * (2 * np.pi * j / d) * np.cos(2 * np.pi * j * x / d)
+        for j, b in enumerate(self.cos_coeffs, start=1):
+            dy = dy - b * (2 * np.pi * j / d) * np.sin(2 * np.pi * j * x / d)
+        return dy
+
+    def extremes(self, d: float = 1.0, samples: int = 4096):
+        y = self.height(np.linspace(-0.5 * d, 0.5 * d, samples, endpoint=False), d)
+        return float(np.min(y)), float(np.max(y))
+
+
 @dataclass
 class GratingConfig:
-    """Subset of ProblemConfig (geometry.py:317-406) the hot path reads."""
+    """Subset of ProblemConfig (geometry.py:317-406) the hot path reads; with
+    the interface / node-count fields it also drives the device assembly of
+    the empty-grating system (empty_setup.py)."""
     period: float
     k1: float
     k2: float
@@ -39,6 +72,20 @@ class GratingConfig:
     gmres_tol: float = 1e-10
     gmres_maxit: int = 150
     y0: float = 0.8
+    interface_top: InterfaceSpec = field(default_factory=lambda: InterfaceSpec(0.5))
+    interface_bottom: InterfaceSpec = field(default_factory=lambda: InterfaceSpec(-0.5))
+    interface_nodes: int = 120
+    lid_nodes: int = 50
+    wall_nodes_per_unit: int = 48
+    alpert_order: int = 16
+
+    def expansion_centers(self) -> dict:
+        """Layer expansion centres (geometry.py:398-406)."""
+        lo1, hi1 = self.interface_top.extremes(self.period)
+        lo2, hi2 = self.interface_bottom.extremes(self.period)
+        mid = 0.5 * (self.interface_top.mean + self.interface_bottom.mean)
+        return {1: np.array([0.0, 0.5 * (self.y0 + hi1)]), 2: np.array([0.0, mid]),
+                3: np.array([0.0, -0.5 * (self.y0 + abs(lo2))])}
 
     @property
     def kappa(self) -> float:
@@ -113,6 +160,13 @@ def load_fixture(name: str, directory: str = GOLDEN) -> GratingSystem:
                         near_field_copies=int(sc[6]), j_expansion_order=int(sc[7]),
                         regularization=float(sc[8]), y0=float(sc[9]),
                         rb_modes_per_direction=cols["c"].stop - cols["c"].start)
+    if "top_spec" in z.files:       # fixtures written with their interface parametrisation
+        specs = []
+        for key in ("top_spec", "bottom_spec"):
+            v = z[key]
+            ns = int(v[1])
+            specs.append(InterfaceSpec(float(v[0]), tuple(v[2:2 + ns]), tuple(v[2 + ns:])))
+        cfg.interface_top, cfg.interface_bottom = specs
     nw = z["L2_nodes"].shape[0]
     curves = {
         "g1": Curve(z["g1_nodes"], z["g1_normals"], z["g1_w"]),
@@ -139,6 +193,22 @@ def load_cfg5():
     """cfg5: M=1e4, r=0.004, p=20, 16 incidence angles at omega=10."""
     centers = np.load(os.path.join(GOLDEN, "centers_cfg5.npy"))
     return [load_fixture(n) for n in CFG5_ANGLES], centers, 20, 0.004
+
+
+def baseline_config(omega: float, theta_ref: float, **kw) -> GratingConfig:
+    """BASELINE.json grating: period 1, layer indices 1.0/1.2/1.0,
+    inclusions 1.5, flat interfaces at y = +-0.5; theta_ref measured from +x."""
+    top, bot = InterfaceSpec(0.5), InterfaceSpec(-0.5)
+    y0 = 1.6 * max(abs(v) for v in (*top.extremes(), *bot.extremes()))   # geometry.py:355-356
+    return GratingConfig(period=1.0, k1=omega, k2=1.2 * omega, k3=omega, kp=1.5 * omega,
+                         incident_angle=theta_ref, y0=y0, interface_top=top,
+                         interface_bottom=bot, **kw)
+
+
+def fixture_config(name: str) -> GratingConfig:
+    """The GratingConfig a committed fixture was assembled from (w10, wood,
+    w10_aNN): its stored scalars, BASELINE interfaces and node counts."""
+    return load_fixture(name).config
 
 
 def load_config(cfg: int):

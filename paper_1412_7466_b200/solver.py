@@ -18,18 +18,27 @@ from .engine import Engine
 from .scatmat import disk_scattering_matrix
 
 
+@dataclass
+class _ConfigOnly:
+    config: object
+
+
 class SchurOperator:
     def __init__(self, systems, centers, p: int, smat=None, radius: float | None = None,
                  rot=None, device=None, target_range=None, coupled: bool = True,
                  engine: Engine | None = None, dense_gb: float = 40.0):
         if not isinstance(systems, (list, tuple)):
             systems = [systems]
-        self.systems = list(systems)
-        cfg = self.systems[0].config
+        items = list(systems)
+        # empty-grating systems with host factors (EmptyGratingSystem /
+        # GratingSystem), or configs (ProblemConfig / GratingConfig) whose
+        # system is assembled and factorised on the device (ps_setup_empty)
+        self.device_setup = not hasattr(items[0], "matrix")
+        configs = items if self.device_setup else [s.config for s in items]
+        cfg = configs[0]
         self.config = cfg
-        for s in self.systems[1:]:
-            if (s.config.k2, s.config.period, s.config.near_field_copies) != \
-                    (cfg.k2, cfg.period, cfg.near_field_copies):
+        for c in configs[1:]:
+            if (c.k2, c.period, c.near_field_copies) != (cfg.k2, cfg.period, cfg.near_field_copies):
                 raise ValueError("batched right-hand sides must share k2, period and copies")
         if smat is None:
             if radius is None:
@@ -40,13 +49,19 @@ class SchurOperator:
         eng = self.eng
         self.centers = np.ascontiguousarray(np.asarray(centers, dtype=float).reshape(-1, 2))
         eng.set_geometry(self.centers, p, cfg.k2, cfg.period, cfg.near_field_copies)
-        eng.set_bloch([s.config.bloch_phase for s in self.systems])
+        eng.set_bloch([c.bloch_phase for c in configs])
         eng.set_smatrix(self.smat, rot)
         self.coupled = coupled
+        self.systems = items
         if coupled:
-            eng.set_layers(self.systems[0])
-            for r, s in enumerate(self.systems):
-                eng.set_pinv(r, s)
+            if self.device_setup:
+                self.systems = eng.setup_empty(configs)
+            else:
+                eng.set_layers(items[0])
+                for r, s in enumerate(items):
+                    eng.set_pinv(r, s)
+        elif self.device_setup:
+            self.systems = [_ConfigOnly(c) for c in configs]
         if target_range is not None:
             eng.set_target_range(*target_range)
         # pre-assembled B / C blocks when they fit (else matrix-free K3/K5)
@@ -115,7 +130,12 @@ class Solution:
 def solve_full(systems, centers, p: int, radius: float | None = None, smat=None, rot=None,
                tol: float | None = None, maxit: int | None = None, device=None) -> Solution:
     """beta from GMRES on (I - S T - S B A^+ C) beta = -S B A^+ f,
-    then x_empty = A^+ (f - C beta); flux balance per RHS."""
+    then x_empty = A^+ (f - C beta); flux balance per RHS.
+
+    ``systems``: one per RHS (incidence angle), either empty-grating systems
+    carrying host SVD factors or configs (ProblemConfig / GratingConfig), in
+    which case the empty-grating assembly and its SVD also run on the device
+    (SPEC.md:559 ``solve_full(config)``)."""
     import time
     t0 = time.perf_counter()
     op = SchurOperator(systems, centers, p, smat=smat, radius=radius, rot=rot, device=device)
@@ -131,5 +151,7 @@ def solve_full(systems, centers, p: int, radius: float | None = None, smat=None,
     torch.cuda.synchronize(op.device)
     t2 = time.perf_counter()
     flux = [postproc.flux_error(c[r], d[r], s.config) for r, s in enumerate(op.systems)]
-    return Solution(beta.cpu().numpy(), c, d, its, hist, flux,
-                    dict(setup=t1 - t0, solve=t2 - t1))
+    timings = dict(setup=t1 - t0, solve=t2 - t1)
+    if op.device_setup and op.coupled:
+        timings["assemble_ms"], timings["svd_ms"] = op.eng.setup_timings()
+    return Solution(beta.cpu().numpy(), c, d, its, hist, flux, timings)

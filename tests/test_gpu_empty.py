@@ -1,0 +1,131 @@
+"""Device empty-grating setup (ps_setup_empty: assembly + cuSOLVER SVD +
+restricted A^+ factors) against the reference's own assembled systems (the
+committed fixtures are bit-identical to empty_grating.assemble_empty_system,
+test_oracle_pin) and the oracle goldens.
+
+Tolerances: the device evaluates H0/H1/J_n by Miller/Neumann sweeps instead of
+AMOS, so entries agree to ~1e-14 of their column's scale, not bitwise; the
+SVD is cuSOLVER gesvd instead of LAPACK gesdd.  Solution quantities keep the
+north-star bars (c, d <= 1e-9 relative, flux <= 1e-9 absolute, matvec <= 1e-10).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+ENTRY_TOL = 1e-12     # |A_dev - A_ref| per entry, relative to max(1, column max)
+SV_TOL = 1e-13        # |s_dev - s_ref| / s_max
+MATVEC_TOL = 1e-10
+
+
+def _setup(configs, M_centers=None, svd_workers=None):
+    from paper_1412_7466_b200.engine import Engine
+    eng = Engine(0)
+    c = np.array([[0.0, 0.0]]) if M_centers is None else M_centers
+    eng.set_geometry(c, 2, configs[0].k2, configs[0].period, configs[0].near_field_copies)
+    eng.set_bloch([cf.bloch_phase for cf in configs])
+    systems = eng.setup_empty(configs, svd_workers=svd_workers)
+    return eng, systems
+
+
+def _check_against_fixture(got, ref):
+    A, f, cs, s = got
+    assert A.shape == ref.matrix.shape
+    scale = np.maximum(1.0, np.max(np.abs(ref.matrix), axis=0))
+    err = np.max(np.abs(A - ref.matrix) / scale[None, :])
+    assert err <= ENTRY_TOL, f"entry error {err:.2e}"
+    assert np.max(np.abs(f - ref.rhs)) <= 1e-14
+    assert np.max(np.abs(cs / ref.col_scale - 1.0)) <= 1e-12
+    s_ref = np.linalg.svd(ref.matrix, compute_uv=False)
+    assert np.max(np.abs(s - s_ref)) / s_ref[0] <= SV_TOL
+    assert np.all(np.diff(s) <= 0)
+
+
+@pytest.mark.parametrize("name", ["w10", "wood", "w10_a00", "w10_a15", "curved"])
+def test_device_assembly_matches_reference_system(name):
+    """A, f, col_scale and singular values of the device-assembled system vs
+    the reference's assemble_empty_system output (fixture) for the BASELINE
+    gratings: omega=10 (cfg1-3), the Wood anomaly (cfg4), cfg5's extreme
+    angles, and the reference's default sinusoidal interfaces (curved)."""
+    from paper_1412_7466_b200 import grating
+    ref = grating.load_fixture(name)
+    eng, systems = _setup([grating.fixture_config(name)])
+    try:
+        _check_against_fixture(systems[0].fetch(), ref)
+        assert systems[0].cols == ref.cols and systems[0].rows == ref.rows
+    finally:
+        eng.close()
+
+
+def test_device_assembly_batched_angles_concurrent_svd():
+    """cfg5's 16 incidence angles in one setup call (one assembly launch, SVDs
+    on 4 concurrent cuSOLVER streams): the first and last angle match their
+    reference systems, and every angle equals its own single-angle setup."""
+    from paper_1412_7466_b200 import grating
+    cfgs = [grating.fixture_config(n) for n in grating.CFG5_ANGLES]
+    eng, systems = _setup(cfgs, svd_workers=4)
+    try:
+        for i, name in ((0, "w10_a00"), (15, "w10_a15")):
+            _check_against_fixture(systems[i].fetch(), grating.load_fixture(name))
+        for i in (3, 9):
+            e1, s1 = _setup([cfgs[i]])
+            try:
+                a1 = s1[0].fetch()
+                ab = systems[i].fetch()
+                assert np.array_equal(a1[0], ab[0]) and np.array_equal(a1[1], ab[1])
+                assert np.array_equal(a1[3], ab[3])
+            finally:
+                e1.close()
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_schur_with_device_setup_matches_golden(cfg):
+    """The Schur matvec of an operator built from the config alone (device
+    assembly + SVD) equals the oracle golden (host reference factors)."""
+    from oracle import periscat_oracle as O
+    from paper_1412_7466_b200 import grating, solver
+    pb = O.load_problem(cfg)
+    z = np.load(os.path.join(O.GOLDEN, f"golden_cfg{cfg}.npz"))
+    conf = grating.fixture_config(grating.CONFIGS[cfg]["system"])
+    import torch
+    op = solver.SchurOperator(conf, pb.centers, pb.p, smat=pb.smat, device=0)
+    assert op.device_setup
+    v = torch.as_tensor(z["v"][None]).cuda()
+    tids = z["targets"]
+    sch = op(v).cpu().numpy()[0]
+    assert rel(sch[tids], z["schur"]) <= MATVEC_TOL
+    rhs = op.rhs().cpu().numpy()[0]
+    assert rel(rhs[tids], z["rhs"]) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("cfg", [1, 4])
+def test_solve_full_from_config_matches_golden(cfg):
+    """solve_full(config): assembly, SVD, GMRES and recovery all on the device
+    reproduce the oracle's Bragg coefficients and flux balance."""
+    from oracle import periscat_oracle as O
+    from paper_1412_7466_b200 import grating, solver
+    pb = O.load_problem(cfg)
+    z = np.load(os.path.join(O.GOLDEN, f"golden_cfg{cfg}.npz"))
+    conf = grating.fixture_config(grating.CONFIGS[cfg]["system"])
+    sol = solver.solve_full(conf, pb.centers, pb.p, smat=pb.smat, device=0)
+    assert rel(sol.c[0], z["c"]) <= 1e-9 and rel(sol.d[0], z["d"]) <= 1e-9
+    assert abs(sol.flux[0]["error"] - float(z["flux_error"])) <= 1e-9
+    assert abs(sol.iterations[0] - int(z["iterations"])) <= 1
+    assert sol.timings["assemble_ms"] > 0 and sol.timings["svd_ms"] > 0
+
+
+def test_setup_rejects_mixed_geometry_and_bad_angle():
+    from paper_1412_7466_b200 import grating
+    a = grating.fixture_config("w10")
+    b = grating.fixture_config("wood")
+    with pytest.raises(ValueError):
+        _setup([a, b])
+    bad = grating.baseline_config(10.0, 0.3)
+    with pytest.raises(ValueError):
+        _setup([bad])

@@ -1,0 +1,50 @@
+"""Time the device empty-grating setup (assembly + SVD) and solve_full from a config."""
+import sys, os, time, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_1412_7466_b200 import grating, solver
+from paper_1412_7466_b200.engine import Engine
+
+out = {}
+for workers in (1, 2, 4, 8):
+    cfgs = [grating.fixture_config(n) for n in grating.CFG5_ANGLES]
+    eng = Engine(0)
+    eng.set_geometry(np.array([[0.0, 0.0]]), 2, cfgs[0].k2)
+    eng.set_bloch([c.bloch_phase for c in cfgs])
+    for it in range(2):
+        t = time.perf_counter(); eng.setup_empty(cfgs, svd_workers=workers); dt = time.perf_counter() - t
+    out[f"cfg5_16angles_workers{workers}"] = dict(wall_s=dt, device_ms=eng.setup_timings())
+    eng.close()
+cfg = grating.fixture_config("w10")
+eng = Engine(0); eng.set_geometry(np.array([[0.0, 0.0]]), 2, cfg.k2); eng.set_bloch([cfg.bloch_phase])
+for it in range(3):
+    t = time.perf_counter(); eng.setup_empty([cfg]); dt = time.perf_counter() - t
+out["single_angle"] = dict(wall_s=dt, device_ms=eng.setup_timings())
+eng.close()
+sysm, centers, p, radius = grating.load_config(3)
+for it in range(3):
+    torch.cuda.synchronize(); t = time.perf_counter()
+    sol = solver.solve_full(cfg, centers, p, radius=radius, device=0)
+    torch.cuda.synchronize(); dt = time.perf_counter() - t
+out["cfg3_solve_full_from_config"] = dict(seconds=dt, timings=sol.timings, iterations=sol.iterations,
+                                          flux=sol.flux[0]["error"])
+print(json.dumps(out, indent=1))
+
+# gesvdp (polar decomposition) vs gesvd: time and solution agreement on cfg3
+from paper_1412_7466_b200 import postproc
+res = {}
+for method in (0, 1):
+    eng = Engine(0); eng.set_svd_method(method)
+    for it in range(2):
+        torch.cuda.synchronize(); t = time.perf_counter()
+        op = solver.SchurOperator(cfg, centers, p, radius=radius, engine=eng)
+        torch.cuda.synchronize(); dt = time.perf_counter() - t
+    beta, its, hist = solver.gmres(op, op.rhs(), 1e-10, 150)
+    x = op.recover(beta); c, d = op.split_cd(x)
+    res[method] = dict(setup_s=dt, device_ms=eng.setup_timings(), its=its, c=c[0], d=d[0],
+                       flux=postproc.flux_error(c[0], d[0], cfg)["error"])
+rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+print(json.dumps({"gesvd": {k: v for k, v in res[0].items() if k not in "cd"},
+                  "gesvdp": {k: v for k, v in res[1].items() if k not in "cd"},
+                  "c_rel": rel(res[1]["c"], res[0]["c"]), "d_rel": rel(res[1]["d"], res[0]["d"])},
+                 indent=1, default=str))
