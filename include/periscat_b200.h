@@ -245,11 +245,35 @@ int ps_get_empty(ps_ctx* ctx, int irhs, double* A_host, double* f_host, double* 
                  double* s_host);
 /* Concurrent cuSOLVER streams used for the per-RHS SVDs (default 4). */
 int ps_set_svd_workers(ps_ctx* ctx, int workers);
-/* SVD algorithm of ps_setup_empty: 0 cuSOLVER zgesvd (default; bidiagonal
- * QR like LAPACK), 1 cuSOLVER Xgesvdp (QDWH polar decomposition). */
-int ps_set_svd_method(ps_ctx* ctx, int method);
 /* Device time of the last ps_setup_empty: assembly and SVD + factor restriction. */
 int ps_setup_timings(const ps_ctx* ctx, double* assemble_ms, double* svd_ms);
+
+/* ---- particle scattering matrix ------------------- */
+
+/* Star-shaped particle r(t) = a1 + a2 cos(a3 t) (ParticleShape,
+ * geometry.py:99-113) sampled by geometry.sample_particle (geometry.py:
+ * 224-256) at centre 0, rotation 0: host rows of 8 doubles per node
+ * (x, y, nx, ny, speed, weight, t, arc_weight), n >= 64 nodes. */
+typedef struct ps_particle_desc {
+  double k2, kp;                      /* exterior (layer 2) and particle wavenumbers */
+  double base_radius, bump_amplitude; /* a1, a2 */
+  int lobes;                          /* a3 */
+  int n;
+  const double* curve;
+  int rule_n, rule_skip, rule_interp; /* Alpert correction rule (quadrature.py:41-56) */
+  const double* rule_x;
+  const double* rule_w;
+} ps_particle_desc;
+
+/* Scattering matrix s_ln, |l|, |n| <= p, of one particle from the Mueller
+ * BIE (scatmat.scattering_matrix): the
+ * 2n x 2n Nystrom system of Eqs. intg1-intg2 assembled on the device, solved
+ * for the 2p+1 incident regular waves (cuSOLVER LU), projected onto outgoing
+ * coefficients.  S_host: complex [2p+1][2p+1] row-major (row l, column n);
+ * residual (may be NULL): ||A X - B|| / ||B|| of the discrete solve.
+ * PS_ERR_NUMERICAL for a singular system or non-finite entries. */
+int ps_scattering_matrix(ps_ctx* ctx, const ps_particle_desc* desc, int p, double* S_host,
+                         double* residual);
 
 /* ---- instrumentation ---------------------------------------------------- */
 /* Record CUDA events around every K1 (M2L) launch of this context. */

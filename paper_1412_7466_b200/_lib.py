@@ -60,8 +60,8 @@ SIGNATURES = {
     "ps_empty_shape": (_I, [_P, _IP, _IP]),
     "ps_get_empty": (_I, [_P, _I, _P, _P, _P, _P]),
     "ps_set_svd_workers": (_I, [_P, _I]),
-    "ps_set_svd_method": (_I, [_P, _I]),
     "ps_setup_timings": (_I, [_P, _DP, _DP]),
+    "ps_scattering_matrix": (_I, [_P, _P, _I, _P, _DP]),
 }
 
 
@@ -84,6 +84,16 @@ class EmptyDesc(ctypes.Structure):
                 ("top", InterfaceDesc), ("bottom", InterfaceDesc),
                 ("rule_n", _I), ("rule_skip", _I), ("rule_interp", _I),
                 ("rule_x", _P), ("rule_w", _P)]
+
+
+
+class ParticleDesc(ctypes.Structure):
+    """ps_particle_desc (include/periscat_b200.h)."""
+    _fields_ = [("k2", _D), ("kp", _D), ("base_radius", _D), ("bump_amplitude", _D),
+                ("lobes", _I), ("n", _I), ("curve", _P),
+                ("rule_n", _I), ("rule_skip", _I), ("rule_interp", _I),
+                ("rule_x", _P), ("rule_w", _P)]
+
 
 _lib = None
 

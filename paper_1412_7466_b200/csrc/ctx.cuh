@@ -85,7 +85,6 @@ struct Ctx {
   // device empty-grating assembly + SVD (ps_setup_empty, empty.cu)
   EmptyState* empty = nullptr;
   int svd_workers = 4;             // concurrent cuSOLVER streams for multi-RHS setup
-  int svd_method = 0;              // 0 zgesvd, 1 Xgesvdp (polar decomposition)
 
   std::vector<void*> owned;        // everything cudaMalloc'ed
 

@@ -41,16 +41,15 @@
 #include "coupling.cuh"
 #include "ctx.cuh"
 #include "empty.cuh"
+#include "nystrom.cuh"
 
 namespace ps {
 
 namespace {
 
-constexpr int kCS = 8;          // doubles per curve node: x y nx ny speed weight t aw
+using namespace nys;
 constexpr int kMaxTasks = 24;
-constexpr int kMaxRule = 16;
 constexpr int kMaxCoef = 8;     // trig coefficients per interface
-constexpr int kPsiTerms = 14;   // layerpot._y1_series_coeffs (layerpot.py:94-103)
 
 enum Kind { K_SELF = 0, K_CROSS, K_WALL, K_REG, K_WALLREG, K_RB, K_INC };
 enum CurveId { C_G1 = 0, C_G2, C_L1, C_L2, C_L3, C_GU, C_GD, C_NCURVE };
@@ -95,105 +94,6 @@ struct RhsPar {   // per incidence angle
   double pad;
 };
 
-// ---------------------------------------------------------------- complex helpers
-__device__ __forceinline__ double2 c2(double a, double b) { return make_double2(a, b); }
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return c2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return c2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return c2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-__device__ __forceinline__ double2 cscale(double2 a, double s) { return c2(a.x * s, a.y * s); }
-__device__ __forceinline__ double2 cmuli(double2 a) { return c2(-a.y, a.x); }   // i a
-__device__ __forceinline__ double2 cexpi(double t) {
-  double s, c;
-  sincos(t, &s, &c);
-  return c2(c, s);
-}
-__device__ __forceinline__ double2 cexp(double2 z) {
-  const double e = exp(z.x);
-  double s, c;
-  sincos(z.y, &s, &c);
-  return c2(e * c, e * s);
-}
-// principal complex sqrt of a real number (numpy sqrt of x + 0j)
-__device__ __forceinline__ double2 csqrt_real(double x) {
-  return x >= 0.0 ? c2(sqrt(x), 0.0) : c2(0.0, sqrt(-x));
-}
-
-// alpha^l for small integer l (|alpha| = 1 for real kappa; the inverse is the
-// complex quotient 1 / alpha^|l|, as Python's complex power does)
-__device__ __forceinline__ double2 cpow_int(double2 a, int l) {
-  double2 r = c2(1.0, 0.0);
-  const int n = l < 0 ? -l : l;
-  for (int i = 0; i < n; ++i) r = cmul(r, a);
-  if (l < 0) {
-    const double d = r.x * r.x + r.y * r.y;
-    r = c2(r.x / d, -r.y / d);
-  }
-  return r;
-}
-
-__device__ __forceinline__ void hankel01(double z, double2* h0, double2* h1) {
-  double j0, j1, y0, y1;
-  bessel_jy01(z, miller_start_j01(z), &j0, &j1, &y0, &y1);
-  *h0 = c2(j0, y0);
-  *h1 = c2(j1, y1);
-}
-
-// The four Helmholtz kernels at one (target, source) pair, target-minus-source
-// vector (u0, u1): layerpot._kernel_values_diff (layerpot.py:69-91).
-struct K4 {
-  double2 S, D, N, T;
-};
-__device__ __forceinline__ K4 kernel4(double k, double u0, double u1, double tnx, double tny,
-                                      double snx, double sny) {
-  const double r = hypot(u0, u1);
-  double2 h0, h1;
-  hankel01(k * r, &h0, &h1);
-  const double udy = (u0 * snx + u1 * sny) / r;
-  const double udx = (u0 * tnx + u1 * tny) / r;
-  const double nxny = tnx * snx + tny * sny;
-  K4 o;
-  o.S = cmuli(cscale(h0, 0.25));
-  o.D = cmuli(cscale(h1, 0.25 * k * udy));
-  o.N = cmuli(cscale(h1, -0.25 * k * udx));
-  const double2 h1p = csub(h0, cscale(h1, 1.0 / (k * r)));
-  const double2 t = cadd(cscale(h1p, k * udx * udy), cscale(h1, (nxny - udx * udy) / r));
-  o.T = cmuli(cscale(t, 0.25 * k));
-  return o;
-}
-
-// T^{ka} - T^{kb} with the 1/r^2 singularity removed (layerpot.py:106-141).
-__device__ double2 t_difference(const Tables& tb, double ka, double kb, double u0, double u1,
-                                double tnx, double tny, double snx, double sny) {
-  const double r = hypot(u0, u1);
-  const double p = ((u0 * tnx + u1 * tny) * (u0 * snx + u1 * sny)) / (r * r);
-  const double nxny = tnx * snx + tny * sny;
-  double ja0, ja1, ya0, ya1, jb0, jb1, yb0, yb1;
-  bessel_jy01(ka * r, miller_start_j01(ka * r), &ja0, &ja1, &ya0, &ya1);
-  bessel_jy01(kb * r, miller_start_j01(kb * r), &jb0, &jb1, &yb0, &yb1);
-  const double2 h0t = csub(cscale(c2(ja0, ya0), ka * ka), cscale(c2(jb0, yb0), kb * kb));
-  const double wj = (ka * ja1 - kb * jb1) / r;
-  double wy;
-  if (fmax(ka, kb) * r < 1.0) {
-    auto smooth = [&](double k, double j1) {
-      const double z = k * r;
-      const double q = -0.25 * z * z;
-      double series = 0.0, qm = 1.0;
-      for (int m = 0; m < kPsiTerms; ++m) {
-        series += tb.psi[m] * qm;
-        qm *= q;
-      }
-      return (2.0 / kPi) * k * k * log(0.5 * z) * (j1 / z) - k * k / (2.0 * kPi) * series;
-    };
-    wy = smooth(ka, ja1) - smooth(kb, jb1);
-  } else {
-    wy = (ka * ya1 - kb * yb1) / r;
-  }
-  const double2 w = c2(wj, wy);
-  return cmuli(cscale(cadd(cscale(h0t, p), cscale(w, nxny - 2.0 * p)), 0.25));
-}
-
 // Interface graph y(x) = mean + sum a_j sin(2 pi j x/d) + b_j cos(2 pi j x/d)
 // at parameter tau (geometry.py:198-207): point, tangent speed, unit normal.
 __device__ void spec_eval(const Spec& s, double d, double tau, double* px, double* py,
@@ -229,11 +129,6 @@ __device__ void spec_diff(const Spec& sp, double d, double s, double tau, double
   *u1 = dy;
 }
 
-__device__ __forceinline__ int floordiv(int a, int b) {
-  const int q = a / b;
-  return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
-}
-
 // ---------------------------------------------------------------- kernels
 // Alpert off-grid kernel values of the two self blocks:
 // kv[slot][i][side*rule_n + m] = {D, S, T, N} * speed(tau) * w_m h
@@ -263,7 +158,7 @@ __global__ void alpert_kv_kernel(Tables tb, double2* kv) {
     const double tnx = cv[i * kCS + 2], tny = cv[i * kCS + 3];
     const K4 a = kernel4(t.k, u0, u1, tnx, tny, nx, ny);
     const K4 b = kernel4(t.ksub, u0, u1, tnx, tny, nx, ny);
-    const double2 T = t_difference(tb, t.k, t.ksub, u0, u1, tnx, tny, nx, ny);
+    const double2 T = t_difference(tb.psi, t.k, t.ksub, u0, u1, tnx, tny, nx, ny);
     const double w = sp * (tb.rule_w[m] * h);
     double2* o = kv + (size_t)id * 4;
     o[0] = cscale(csub(a.D, b.D), w);
@@ -275,46 +170,6 @@ __global__ void alpert_kv_kernel(Tables tb, double2* kv) {
 
 __device__ __forceinline__ void put(double2* A, int m, int row, int col, double2 v) {
   A[(size_t)col * m + row] = v;
-}
-
-// regular wave J_n(k r) e^{i n theta} about (cx, cy): value and Cartesian
-// gradient (specialfn.regular_wave_block, specialfn.py:86-125)
-__device__ void regular_wave(double k, double cx, double cy, int n, int nmax, double x, double y,
-                             double2* val, double2* gx, double2* gy) {
-  const double dx = x - cx, dy = y - cy;
-  const double r = hypot(dx, dy);
-  if (r == 0.0) {
-    *val = c2(n == 0 ? 1.0 : 0.0, 0.0);
-    if (n == 1) {
-      *gx = c2(0.5 * k, 0.0);
-      *gy = c2(0.0, 0.5 * k);
-    } else if (n == -1) {
-      *gx = c2(-0.5 * k, 0.0);
-      *gy = c2(0.0, 0.5 * k);
-    } else {
-      *gx = c2(0.0, 0.0);
-      *gy = c2(0.0, 0.0);
-    }
-    return;
-  }
-  const double theta = atan2(dy, dx);
-  const int a0 = n < 0 ? -n : n;
-  const int a1 = (n + 1) < 0 ? -(n + 1) : (n + 1);
-  double ja = 0.0, jb = 0.0, inv, y0, y1;
-  bessel_jy_sweep(k * r, nmax + 1, [&](int nu, double v) {
-    if (nu == a0) ja = v;
-    if (nu == a1) jb = v;
-  }, &inv, &y0, &y1);
-  double jn = ja * inv, jn1 = jb * inv;
-  if (n < 0 && (a0 & 1)) jn = -jn;
-  if (n + 1 < 0 && (a1 & 1)) jn1 = -jn1;
-  const double2 ph = cexpi(n * theta);
-  *val = cscale(ph, jn);
-  const double2 dr = cscale(ph, k * (n * jn / (k * r) - jn1));
-  const double2 dth = cmuli(cscale(ph, n * jn / r));
-  const double ct = cos(theta), st = sin(theta);
-  *gx = csub(cscale(dr, ct), cscale(dth, st));
-  *gy = cadd(cscale(dr, st), cscale(dth, ct));
 }
 
 __global__ void assemble_kernel(Tables tb, const RhsPar* __restrict__ rp,
@@ -360,7 +215,7 @@ __global__ void assemble_kernel(Tables tb, const RhsPar* __restrict__ rp,
           const double u0 = tx - (sx0 + l * tb.period), u1 = ty - sy;
           const K4 a = kernel4(t.k, u0, u1, tnx, tny, snx, sny);
           const K4 b = kernel4(t.ksub, u0, u1, tnx, tny, snx, sny);
-          const double2 Td = t_difference(tb, t.k, t.ksub, u0, u1, tnx, tny, snx, sny);
+          const double2 Td = t_difference(tb.psi, t.k, t.ksub, u0, u1, tnx, tny, snx, sny);
           const double2 w = cscale(cpow_int(alpha, l), sw);
           D = cadd(D, cmul(csub(a.D, b.D), w));
           S = cadd(S, cmul(csub(a.S, b.S), w));
@@ -529,7 +384,7 @@ __global__ void pinv_extract_kernel(const double2* __restrict__ U, const double*
                                     const double2* __restrict__ f_full, int m, int ncol, int nrc,
                                     int ncol_b, int nrb, int col_c, int col_d, double eps,
                                     double2* Uh, double* sinv, double2* Vb, double* cs,
-                                    double2* f, int v_is_V) {
+                                    double2* f) {
   const int nout = ncol_b + 2 * nrb;
   const long long nu = (long long)ncol * nrc, nv = (long long)nout * ncol;
   const long long tot = nu + nv + ncol + nout + nrc;
@@ -543,12 +398,8 @@ __global__ void pinv_extract_kernel(const double2* __restrict__ U, const double*
       const long long q = id - nu;
       const int o = (int)(q / ncol), k = (int)(q % ncol);
       const int col = o < ncol_b ? o : (o < ncol_b + nrb ? col_c + o - ncol_b : col_d + o - ncol_b - nrb);
-      if (v_is_V) {   // V column-major: Vh[k][col] = conj(V[col][k])
-        Vb[q] = VT[(size_t)k * ncol + col];
-      } else {        // VT column-major = Vh
-        const double2 v = VT[(size_t)col * ncol + k];
-        Vb[q] = c2(v.x, -v.y);
-      }
+      const double2 v = VT[(size_t)col * ncol + k];
+      Vb[q] = c2(v.x, -v.y);
     } else if (id < nu + nv + ncol) {
       const int k = (int)(id - nu - nv);
       sinv[k] = fmin(1.0 / s[k], 1.0 / eps);
@@ -573,9 +424,7 @@ struct SvdWorker {
   double2 *A = nullptr, *U = nullptr, *VT = nullptr;
   double* rwork = nullptr;
   int* info = nullptr;
-  int m = 0, n = 0, method = -1;
-  cusolverDnParams_t params = nullptr;
-  std::vector<char> host_work;
+  int m = 0, n = 0;
 };
 std::mutex g_svd_mu;
 std::mutex g_dev_mu[64];   // one SVD phase per device at a time
@@ -585,12 +434,10 @@ std::string svd_err(const char* what, int code) {
   return std::string(what) + " failed (status " + std::to_string(code) + ")";
 }
 
-// A (m x n column-major, m >= n, on the device) -> U, s and VT (method 0,
-// zgesvd: Golub-Kahan bidiagonalisation + QR, what LAPACK gesdd computes) or V
-// (method 1, Xgesvdp: QDWH polar decomposition + Hermitian eigensolver) in the
-// worker's buffers; blocks the calling thread until done.
-int svd_run(SvdWorker& w, const double2* A, int m, int n, int method, double* s,
-            std::string* err) {
+// A (m x n column-major, m >= n, on the device) -> U, s, VT (zgesvd:
+// Householder bidiagonalisation + implicit QR, the decomposition LAPACK gesdd
+// returns) in the worker's buffers; blocks the calling thread until done.
+int svd_run(SvdWorker& w, const double2* A, int m, int n, double* s, std::string* err) {
   if (!w.h) {
     if (cudaStreamCreateWithFlags(&w.st, cudaStreamNonBlocking) != cudaSuccess) {
       *err = "svd: stream create";
@@ -602,38 +449,20 @@ int svd_run(SvdWorker& w, const double2* A, int m, int n, int method, double* s,
       return PS_ERR_CUDA;
     }
     cusolverDnSetStream(w.h, w.st);
-    cs = cusolverDnCreateParams(&w.params);
-    if (cs != CUSOLVER_STATUS_SUCCESS) {
-      *err = svd_err("cusolverDnCreateParams", cs);
-      return PS_ERR_CUDA;
-    }
   }
-  if (w.m != m || w.n != n || w.method != method) {
+  if (w.m != m || w.n != n) {
     void* bufs[] = {w.work, w.A, w.U, w.VT, w.rwork, w.info};
     for (void* p : bufs)
       if (p) dev_free(p);
     w.work = nullptr;
-    size_t dev_bytes = 0, host_bytes = 0;
-    if (method == 0) {
-      int lwork = 0;
-      cusolverStatus_t cs = cusolverDnZgesvd_bufferSize(w.h, m, n, &lwork);
-      if (cs != CUSOLVER_STATUS_SUCCESS) {
-        *err = svd_err("cusolverDnZgesvd_bufferSize", cs);
-        return PS_ERR_CUDA;
-      }
-      dev_bytes = (size_t)lwork * sizeof(double2);
-    } else {
-      cusolverStatus_t cs = cusolverDnXgesvdp_bufferSize(
-          w.h, w.params, CUSOLVER_EIG_MODE_VECTOR, 1, m, n, CUDA_C_64F, nullptr, m, CUDA_R_64F,
-          nullptr, CUDA_C_64F, nullptr, m, CUDA_C_64F, nullptr, n, CUDA_C_64F, &dev_bytes,
-          &host_bytes);
-      if (cs != CUSOLVER_STATUS_SUCCESS) {
-        *err = svd_err("cusolverDnXgesvdp_bufferSize", cs);
-        return PS_ERR_CUDA;
-      }
+    int lwork = 0;
+    cusolverStatus_t cs = cusolverDnZgesvd_bufferSize(w.h, m, n, &lwork);
+    if (cs != CUSOLVER_STATUS_SUCCESS) {
+      *err = svd_err("cusolverDnZgesvd_bufferSize", cs);
+      return PS_ERR_CUDA;
     }
+    const size_t dev_bytes = (size_t)lwork * sizeof(double2);
     w.work_bytes = dev_bytes;
-    w.host_work.assign(host_bytes + 1, 0);
     if (dev_malloc(&w.work, w.work_bytes + 16) != cudaSuccess ||
         dev_malloc(&w.A, (size_t)m * n * sizeof(double2)) != cudaSuccess ||
         dev_malloc(&w.U, (size_t)m * n * sizeof(double2)) != cudaSuccess ||
@@ -645,29 +474,19 @@ int svd_run(SvdWorker& w, const double2* A, int m, int n, int method, double* s,
     }
     w.m = m;
     w.n = n;
-    w.method = method;
   }
   if (cudaMemcpyAsync(w.A, A, (size_t)m * n * sizeof(double2), cudaMemcpyDeviceToDevice, w.st) !=
       cudaSuccess) {
     *err = "svd: copy";
     return PS_ERR_CUDA;
   }
-  cusolverStatus_t cs;
-  if (method == 0) {
-    const int lwork = (int)(w.work_bytes / sizeof(double2));
-    cs = cusolverDnZgesvd(w.h, 'S', 'S', m, n, reinterpret_cast<cuDoubleComplex*>(w.A), m, s,
-                          reinterpret_cast<cuDoubleComplex*>(w.U), m,
-                          reinterpret_cast<cuDoubleComplex*>(w.VT), n,
-                          reinterpret_cast<cuDoubleComplex*>(w.work), lwork, w.rwork, w.info);
-  } else {
-    double err_sigma = 0.0;
-    cs = cusolverDnXgesvdp(w.h, w.params, CUSOLVER_EIG_MODE_VECTOR, 1, m, n, CUDA_C_64F, w.A, m,
-                           CUDA_R_64F, s, CUDA_C_64F, w.U, m, CUDA_C_64F, w.VT, n, CUDA_C_64F,
-                           w.work, w.work_bytes, w.host_work.data(), w.host_work.size() - 1,
-                           w.info, &err_sigma);
-  }
+  const int lwork = (int)(w.work_bytes / sizeof(double2));
+  cusolverStatus_t cs = cusolverDnZgesvd(
+      w.h, 'S', 'S', m, n, reinterpret_cast<cuDoubleComplex*>(w.A), m, s,
+      reinterpret_cast<cuDoubleComplex*>(w.U), m, reinterpret_cast<cuDoubleComplex*>(w.VT), n,
+      reinterpret_cast<cuDoubleComplex*>(w.work), lwork, w.rwork, w.info);
   if (cs != CUSOLVER_STATUS_SUCCESS) {
-    *err = svd_err(method == 0 ? "cusolverDnZgesvd" : "cusolverDnXgesvdp", cs);
+    *err = svd_err("cusolverDnZgesvd", cs);
     return PS_ERR_CUDA;
   }
   int info = 0;
@@ -677,23 +496,10 @@ int svd_run(SvdWorker& w, const double2* A, int m, int n, int method, double* s,
     return PS_ERR_CUDA;
   }
   if (info != 0) {
-    *err = std::string(method == 0 ? "zgesvd" : "gesvdp") + ": info = " + std::to_string(info) +
-           " (did not converge)";
+    *err = "zgesvd: info = " + std::to_string(info) + " (bidiagonal QR did not converge)";
     return PS_ERR_NUMERICAL;
   }
   return PS_OK;
-}
-
-// quadrature._lagrange_weights (quadrature.py:91-101)
-void lagrange(double frac, int interp, int* start, double* w) {
-  const int st = (int)std::floor(frac) - (interp / 2 - 1);
-  *start = st;
-  for (int r = 0; r < interp; ++r) {
-    double v = 1.0;
-    for (int q = 0; q < interp; ++q)
-      if (q != r) v *= (frac - (double)(st + q)) / (double)((st + r) - (st + q));
-    w[r] = v;
-  }
 }
 
 }  // namespace
@@ -814,19 +620,7 @@ int ps_setup_empty(ps_ctx* h, const ps_empty_desc* ds, const double* theta) {
       lagrange((side == 0 ? 1.0 : -1.0) * ds->rule_x[i], ds->rule_interp, &tb.lag_start[side][i],
                tb.lag_w[side][i]);
   }
-  // (psi(m+1) + psi(m+2)) / (m! (m+1)!)  with psi(n) = -gamma + H_{n-1}
-  {
-    long double harm = 0.0L, fact = 1.0L;   // H_m, m!
-    for (int mm = 0; mm < kPsiTerms; ++mm) {
-      if (mm > 0) {
-        harm += 1.0L / mm;
-        fact *= mm;
-      }
-      const long double g = 0.577215664901532860606512090082402431L;
-      const long double psi1 = -g + harm, psi2 = -g + harm + 1.0L / (mm + 1);
-      tb.psi[mm] = (double)((psi1 + psi2) / (fact * fact * (mm + 1)));
-    }
-  }
+  psi_series(tb.psi);
   for (int s = 0; s < 2; ++s) {
     tb.spec[s].mean = sp[s]->mean;
     tb.spec[s].nsin = sp[s]->nsin;
@@ -1020,8 +814,8 @@ int ps_setup_empty(ps_ctx* h, const ps_empty_desc* ds, const double* theta) {
     cudaSetDevice(dev);
     SvdWorker& w = g_svd[dev][wid];
     for (int r = wid; r < R; r += nwk) {
-      int rc = svd_run(w, e->d_A + (size_t)r * m * ncol, m, ncol, c->svd_method,
-                       e->d_s + (size_t)r * ncol, &errs[wid]);
+      int rc = svd_run(w, e->d_A + (size_t)r * m * ncol, m, ncol, e->d_s + (size_t)r * ncol,
+                       &errs[wid]);
       if (rc) {
         rcs[wid] = rc;
         return;
@@ -1031,7 +825,7 @@ int ps_setup_empty(ps_ctx* h, const ps_empty_desc* ds, const double* theta) {
       pinv_extract_kernel<<<(int)std::min<long long>((totx + 255) / 256, 4096), 256, 0, w.st>>>(
           w.U, e->d_s + (size_t)r * ncol, w.VT, e->d_cs + (size_t)r * ncol,
           e->d_f + (size_t)r * m, m, ncol, nrc, c->ncol_b, nrb, c_c, c_d, ds->eps, Rd.d_Uh,
-          Rd.d_sinv, Rd.d_Vb, Rd.d_cscale, Rd.d_f, c->svd_method == 1);
+          Rd.d_sinv, Rd.d_Vb, Rd.d_cscale, Rd.d_f);
       if (cudaStreamSynchronize(w.st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
         rcs[wid] = PS_ERR_CUDA;
         errs[wid] = "pinv_extract_kernel failed";
@@ -1106,14 +900,6 @@ int ps_set_svd_workers(ps_ctx* h, int workers) {
   Ctx* c = ps::C(h);
   if (workers < 1 || workers > 32) return fail(c, PS_ERR_ARG, "ps_set_svd_workers: 1..32");
   c->svd_workers = workers;
-  return PS_OK;
-}
-
-int ps_set_svd_method(ps_ctx* h, int method) {
-  if (!h) return PS_ERR_ARG;
-  Ctx* c = ps::C(h);
-  if (method < 0 || method > 1) return fail(c, PS_ERR_ARG, "ps_set_svd_method: 0 gesvd, 1 gesvdp");
-  c->svd_method = method;
   return PS_OK;
 }
 

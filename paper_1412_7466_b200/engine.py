@@ -120,10 +120,6 @@ class Engine:
         self.nout = self.ncol_b + 2 * nrb
         self._layer_cols = system.cols
 
-    def set_svd_method(self, method: int):
-        """0 cuSOLVER zgesvd (default), 1 Xgesvdp (see include/periscat_b200.h)."""
-        self._check(self.lib.ps_set_svd_method(self.ctx, int(method)))
-
     def setup_empty(self, configs, svd_workers: int | None = None):
         """Device assembly + SVD of the empty-grating system of every RHS
         (ps_setup_empty; replaces set_layers + set_pinv with host factors).

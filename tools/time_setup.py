@@ -30,21 +30,3 @@ out["cfg3_solve_full_from_config"] = dict(seconds=dt, timings=sol.timings, itera
                                           flux=sol.flux[0]["error"])
 print(json.dumps(out, indent=1))
 
-# gesvdp (polar decomposition) vs gesvd: time and solution agreement on cfg3
-from paper_1412_7466_b200 import postproc
-res = {}
-for method in (0, 1):
-    eng = Engine(0); eng.set_svd_method(method)
-    for it in range(2):
-        torch.cuda.synchronize(); t = time.perf_counter()
-        op = solver.SchurOperator(cfg, centers, p, radius=radius, engine=eng)
-        torch.cuda.synchronize(); dt = time.perf_counter() - t
-    beta, its, hist = solver.gmres(op, op.rhs(), 1e-10, 150)
-    x = op.recover(beta); c, d = op.split_cd(x)
-    res[method] = dict(setup_s=dt, device_ms=eng.setup_timings(), its=its, c=c[0], d=d[0],
-                       flux=postproc.flux_error(c[0], d[0], cfg)["error"])
-rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
-print(json.dumps({"gesvd": {k: v for k, v in res[0].items() if k not in "cd"},
-                  "gesvdp": {k: v for k, v in res[1].items() if k not in "cd"},
-                  "c_rel": rel(res[1]["c"], res[0]["c"]), "d_rel": rel(res[1]["d"], res[0]["d"])},
-                 indent=1, default=str))
