@@ -1,9 +1,12 @@
 """Drop-in ``periscat.solver`` on top of the reference's
 own ``empty_grating`` and ``geometry`` modules.
 
-``solve_full(config)`` follows SPEC.md:559-567: it builds the empty system
-with the reference (eg:139-261), places the particles with the reference
-sampler (geo:263-314), and runs the coupled solve on the B200.
+``solve_full(config)`` follows SPEC.md:559-567: it places the particles with
+the reference sampler (geo:263-314) and runs everything else on the B200: the
+empty-grating assembly and SVD (ps_setup_empty, replacing eg:139-261), the
+particle scattering matrix (the analytic disk, or the Mueller BIE for star
+shapes via ps_scattering_matrix), and the coupled solve.  ``setup="host"``
+keeps the reference's own host assembly + numpy SVD instead.
 """
 from __future__ import annotations
 
@@ -12,22 +15,33 @@ from paper_1412_7466_b200.solver import SchurOperator, Solution, apply_schur_ope
 from paper_1412_7466_b200.solver import solve_full as _solve_full
 
 
-def solve_full(config, system=None, particles=None, standoff=None):
-    from periscat.empty_grating import assemble_empty_system, factorize
+def _particle_smatrix(config, particles):
+    """(smat, radius, rot) for the solver: the disk's analytic diagonal, or
+    the device Mueller-BIE matrix of a star shape with the
+    particles' rotations (SPEC.md:415-423)."""
+    from paper_1412_7466_b200 import scatmat
+    shape = particles.shape
+    if shape.bump_amplitude == 0.0:
+        return None, shape.base_radius, None
+    sm = scatmat.scattering_matrix(shape, config.k2, config.kp, config.multipole_order,
+                                   N=config.particle_nodes, alpert_order=config.alpert_order)
+    return sm, None, particles.rotations
+
+
+def solve_full(config, system=None, particles=None, standoff=None, setup: str = "device"):
     from periscat.geometry import place_random_particles
-    if system is None:
-        system = assemble_empty_system(config)
-    if system.svd is None:
-        factorize(system)
     if particles is None:
         particles = place_random_particles(config, config.particle_count,
                                            config.particle_standoff if standoff is None else standoff)
-    shape = particles.shape
-    if shape.bump_amplitude != 0.0:
-        raise NotImplementedError("general-shape scattering matrices (Mueller BIE) are not built "
-                                  "here; pass smat= to paper_1412_7466_b200.solver.solve_full")
-    return _solve_full(system, particles.centers, config.multipole_order,
-                       radius=shape.base_radius, tol=config.gmres_tol, maxit=config.gmres_maxit)
+    if system is None and setup == "host":
+        system = _assemble_factorize(config)
+    if system is not None and system.svd is None:
+        from periscat.empty_grating import factorize
+        factorize(system)
+    smat, radius, rot = _particle_smatrix(config, particles)
+    return _solve_full(config if system is None else system, particles.centers,
+                       config.multipole_order, radius=radius, smat=smat, rot=rot,
+                       tol=config.gmres_tol, maxit=config.gmres_maxit)
 
 
 def _assemble_factorize(config):
@@ -54,19 +68,19 @@ def assemble_systems(configs, threads: int | None = None):
         return list(ex.map(_assemble_factorize, configs))
 
 
-def solve_full_batch(configs, particles, threads: int | None = None):
+def solve_full_batch(configs, particles, threads: int | None = None, setup: str = "device"):
     """Several incidence angles sharing k2, the period and the particles,
     solved as ONE batch of right-hand sides (BASELINE cfg5: 16 angles): the
-    per-angle setup in parallel host threads, then the batched GPU solve
-    (multi-RHS M2L on the FP64 tensor cores, batched device GMRES)."""
-    systems = assemble_systems(configs, threads)
-    shape = particles.shape
-    if shape.bump_amplitude != 0.0:
-        raise NotImplementedError("general-shape scattering matrices (Mueller BIE) are not built "
-                                  "here; pass smat= to paper_1412_7466_b200.solver.solve_full")
+    per-angle empty-grating setup (one device assembly launch + concurrent
+    cuSOLVER SVDs, or ``setup="host"``: the reference assembly in parallel host
+    threads), then the batched GPU solve (multi-RHS M2L on the FP64 tensor
+    cores, batched device GMRES)."""
+    configs = list(configs)
+    systems = assemble_systems(configs, threads) if setup == "host" else configs
     c0 = configs[0]
-    return _solve_full(systems, particles.centers, c0.multipole_order, radius=shape.base_radius,
-                       tol=c0.gmres_tol, maxit=c0.gmres_maxit)
+    smat, radius, rot = _particle_smatrix(c0, particles)
+    return _solve_full(systems, particles.centers, c0.multipole_order, radius=radius, smat=smat,
+                       rot=rot, tol=c0.gmres_tol, maxit=c0.gmres_maxit)
 
 
 __all__ = ["SchurOperator", "Solution", "apply_schur_operator", "assemble_systems", "gmres",
