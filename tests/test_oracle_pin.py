@@ -159,3 +159,76 @@ def test_C_rows_match_reference_waves(ref, O):
             der += es.bloch ** l * (np.einsum("ink,ik->in", gr, es.g2_normals) @ beta[j])
     assert rel(g[es.rows["g2_val"]], val) < 1e-12
     assert rel(g[es.rows["g2_der"]], der) < 1e-12
+
+
+def test_apply_T_local_expansion_reproduces_particle_field(ref, O):
+    """apply_T (SP:504-512, all-pairs Graf M2L over the phased images, self
+    term excluded) vs the reference's OWN wave functions: the local expansion
+    at each target, re-summed with specialfn.regular_wave_block (sf:86-125)
+    on a small circle, equals the direct phased multipole field of every other
+    source image, summed with specialfn.outgoing_wave_block (sf:128-154)."""
+    rng = np.random.default_rng(11)
+    M, p, k, d = 6, 20, 12.0, 1.0
+    bloch = np.exp(1j * 0.7)
+    centers = np.column_stack([rng.uniform(-0.45, 0.45, M), rng.uniform(-0.4, 0.4, M)])
+    beta = np.zeros((M, 2 * p + 1), complex)
+    beta[:, p - 3:p + 4] = rng.standard_normal((M, 7)) + 1j * rng.standard_normal((M, 7))
+    a = O.apply_T(beta, centers, k, p, bloch, d, 1)
+    orders = np.arange(-p, p + 1)
+    for m in range(M):
+        dmin = min(np.hypot(*(centers[m] - centers[j] - [l * d, 0.0]))
+                   for j in range(M) for l in (-1, 0, 1) if (j, l) != (m, 0))
+        th = np.linspace(0, 2 * np.pi, 9, endpoint=False)
+        pts = centers[m] + 0.2 * dmin * np.column_stack([np.cos(th), np.sin(th)])
+        direct = np.zeros(len(pts), complex)
+        for j in range(M):
+            for l in (-1, 0, 1):
+                if (j, l) == (m, 0):
+                    continue
+                vals, _ = ref["sf"].outgoing_wave_block(k, centers[j] + [l * d, 0.0], orders, pts)
+                direct += bloch ** l * (vals @ beta[j])
+        loc, _ = ref["sf"].regular_wave_block(k, centers[m], orders, pts)
+        assert rel(loc @ a[m], direct) < 1e-10, m
+
+
+def test_coupled_solution_satisfies_reference_wall_conditions(ref, O):
+    """End-to-end physics pin of the coupled solve with the reference's own
+    checker: the golden cfg1 solution (beta from the oracle GMRES, which the
+    GPU reproduces to 1e-9) plus x_empty = A^+ (f - C beta), evaluated with
+    empty_grating.wall_discrepancy_residual (eg:396-433) and the particles'
+    phased multipole field (specialfn.outgoing_wave_block) as its
+    extra_field: the quasi-periodicity alpha u(L) - u(R) of the coupled field
+    holds at fresh wall points, and fails without the particle field."""
+    import warnings
+    warnings.simplefilter("ignore")
+    from oracle.make_empty import config_for
+    pb = O.load_problem(1)
+    z = np.load(os.path.join(O.GOLDEN, "golden_cfg1.npz"))
+    beta = z["beta"]
+    conf = config_for(10.0, -0.7 * math.pi)
+    system = ref["eg"].assemble_empty_system(conf)
+    ref["eg"].factorize(system)
+    x = ref["eg"].apply_pinv(system, system.rhs - O.apply_C(pb.es, beta, pb.centers))
+    sol = ref["eg"].EmptySolution(system, x, 0.0)
+    orders = np.arange(-pb.p, pb.p + 1)
+    alpha = conf.bloch_phase
+
+    def particles(points, normals):
+        """Particle field of layer 2 (the particles' representation lives in
+        the middle layer only, PAPER Eq. repre3_mod)."""
+        vals = np.zeros(len(points), complex)
+        ders = np.zeros(len(points), complex)
+        mid = ref["eg"].classify_layer(conf, points) == 2
+        points, normals = points[mid], normals[mid]
+        for j in range(pb.M):
+            for l in range(-conf.near_field_copies, conf.near_field_copies + 1):
+                v, g = ref["sf"].outgoing_wave_block(conf.k2, pb.centers[j] + [l * conf.period, 0.0],
+                                                     orders, points)
+                vals[mid] += alpha ** l * (v @ beta[j])
+                ders[mid] += alpha ** l * (np.einsum("ijk,ik->ij", g, normals) @ beta[j])
+        return vals, ders
+
+    coupled = ref["eg"].wall_discrepancy_residual(sol, extra_field=particles)
+    without = ref["eg"].wall_discrepancy_residual(sol)
+    assert coupled < 1e-8, (coupled, without)
+    assert without > 1e3 * coupled
