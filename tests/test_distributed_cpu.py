@@ -112,3 +112,95 @@ def test_gmres_dist_single_process_matches_oracle_gmres():
     xo, its_o, _ = O.gmres(lambda v: A[0] @ v, b[0].reshape(-1), 1e-12, 40)
     assert its[0] == its_o
     assert np.linalg.norm(x.numpy()[0].reshape(-1) - xo) / np.linalg.norm(xo) < 1e-12
+
+
+class _FakeDist:
+    """Thread-simulated collectives with NCCL's tensor semantics, to exercise
+    the even-shard all_gather_into_tensor / reduce_scatter_tensor layouts of
+    parallel.py (gloo on CPU takes the padded all_gather / all_reduce paths)."""
+
+    def __init__(self, world):
+        import threading
+        self.world = world
+        self.bar = threading.Barrier(world)
+        self.slots = [None] * world
+        self.local = threading.local()
+
+    def is_initialized(self):
+        return True
+
+    def get_world_size(self, group=None):
+        return self.world
+
+    def get_rank(self, group=None):
+        return self.local.rank
+
+    def _exchange(self, t):
+        self.slots[self.local.rank] = t.clone()
+        self.bar.wait()
+        got = list(self.slots)
+        self.bar.wait()
+        return got
+
+    def all_gather_into_tensor(self, out, inp, group=None):
+        parts = self._exchange(inp)
+        out.copy_(torch.stack(parts).reshape(out.shape))
+
+    def reduce_scatter_tensor(self, out, inp, group=None):
+        parts = self._exchange(inp)
+        out.copy_(sum(p[self.local.rank] for p in parts))
+
+    def all_gather(self, outs, inp, group=None):
+        for o, p in zip(outs, self._exchange(inp)):
+            o.copy_(p)
+
+    def all_reduce(self, t, group=None):
+        t.copy_(sum(self._exchange(t)))
+
+
+@pytest.mark.parametrize("M,world", [(12, 3), (10, 4), (8, 2)])
+def test_row_collectives_nccl_layout(monkeypatch, M, world):
+    """all_gather_rows / reduce_scatter_rows with NCCL's output layouts, even
+    and uneven shards, on fake 'CUDA' tensors (is_cuda forced) -- the layout
+    ShardedSchur relies on at N > 1."""
+    import threading
+
+    from paper_1412_7466_b200 import parallel
+    fake = _FakeDist(world)
+    monkeypatch.setattr(parallel, "dist", fake)
+
+    class T(torch.Tensor):   # a CPU tensor that reports is_cuda (layout only)
+        @property
+        def is_cuda(self):
+            return True
+
+    rng = np.random.default_rng(M)
+    L, nrhs = 3, 2
+    full = torch.as_tensor(rng.standard_normal((nrhs, M, L)) + 1j * rng.standard_normal((nrhs, M, L)))
+    parts = [torch.as_tensor(rng.standard_normal((nrhs, M, L)) + 1j * rng.standard_normal((nrhs, M, L)))
+             for _ in range(world)]
+    out = [None] * world
+    err = []
+
+    def run(r):
+        try:
+            fake.local.rank = r
+            t0, t1 = parallel.shard_range(M, r, world)
+            g = parallel.all_gather_rows(full[:, t0:t1].contiguous().as_subclass(T), M)
+            s = parallel.reduce_scatter_rows(parts[r].as_subclass(T), M)
+            out[r] = (torch.Tensor(g).as_subclass(torch.Tensor), s.as_subclass(torch.Tensor))
+        except Exception as e:   # surfaced below
+            err.append(e)
+            fake.bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not err, err
+    total = sum(parts)
+    for r in range(world):
+        t0, t1 = parallel.shard_range(M, r, world)
+        assert torch.equal(out[r][0], full)
+        assert torch.allclose(out[r][1], total[:, t0:t1], rtol=0, atol=1e-13)
