@@ -52,6 +52,39 @@ class DeviceArray:
             self.ptr = ctypes.c_void_p()
 
 
+class _Curve(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("data", ctypes.c_void_p)]
+
+
+class _Iface(ctypes.Structure):
+    _fields_ = [("mean", ctypes.c_double), ("nsin", ctypes.c_int), ("ncos", ctypes.c_int),
+                ("sin_coeffs", ctypes.c_void_p), ("cos_coeffs", ctypes.c_void_p)]
+
+
+class _EmptyDesc(ctypes.Structure):           # ps_empty_desc
+    _D, _I = ctypes.c_double, ctypes.c_int
+    _fields_ = [("period", _D), ("k1", _D), ("k2", _D), ("k3", _D), ("y0", _D), ("eps", _D),
+                ("copies", _I), ("Q", _I), ("nrb", _I), ("centers", _D * 6),
+                ("g1", _Curve), ("g2", _Curve), ("wall", _Curve * 3),
+                ("lid_up", _Curve), ("lid_down", _Curve), ("top", _Iface), ("bottom", _Iface),
+                ("rule_n", _I), ("rule_skip", _I), ("rule_interp", _I),
+                ("rule_x", ctypes.c_void_p), ("rule_w", ctypes.c_void_p)]
+
+
+class _ParticleDesc(ctypes.Structure):        # ps_particle_desc
+    _D, _I = ctypes.c_double, ctypes.c_int
+    _fields_ = [("k2", _D), ("kp", _D), ("base_radius", _D), ("bump_amplitude", _D),
+                ("lobes", _I), ("n", _I), ("curve", ctypes.c_void_p),
+                ("rule_n", _I), ("rule_skip", _I), ("rule_interp", _I),
+                ("rule_x", ctypes.c_void_p), ("rule_w", ctypes.c_void_p)]
+
+
+def _curve_rows(cv):
+    """DiscretizedCurve (geometry.py:25-60) -> rows x y nx ny speed weight t arc_weight."""
+    return np.ascontiguousarray(np.column_stack([cv.nodes, cv.normals, cv.speeds, cv.weights,
+                                                 cv.t, cv.arc_weights]), dtype=float)
+
+
 class Periscat:
     """ps_ctx owner.  Mirrors the calls solver.solve_full makes."""
 
@@ -105,6 +138,78 @@ class Periscat:
                                           self._p(vh), self._p(cs),
                                           ctypes.c_double(s.config.regularization), self._p(f),
                                           s.cols["c"].start, s.cols["d"].start))
+
+    def setup_from_config(self, configs, curves, rule, centers, p, smat, rot=None):
+        """solve_full(config) without host factors: the empty grating of every
+        config (one per incidence angle) is assembled and factorised on the
+        device (ps_setup_empty).  curves = empty_grating.build_geometry(config)
+        (eg:113-119); rule = quadrature.ALPERT_RULES[config.alpert_order]."""
+        configs = list(configs) if isinstance(configs, (list, tuple)) else [configs]
+        cfg = configs[0]
+        c = np.ascontiguousarray(centers, dtype=float)
+        self.M, self.p, self.L = c.shape[0], p, 2 * p + 1
+        self._ok(self.lib.ps_set_geometry(self.ctx, self.M, p, cfg.near_field_copies,
+                                          ctypes.c_double(cfg.period), ctypes.c_double(cfg.k2),
+                                          self._p(c)))
+        bl = np.array([x.bloch_phase for x in configs], dtype=complex)
+        self.nrhs = bl.size
+        self._ok(self.lib.ps_set_rhs_bloch(self.ctx, bl.size, self._p(bl)))
+        S = np.ascontiguousarray(smat, dtype=complex)
+        r = None if rot is None else np.ascontiguousarray(rot, dtype=float)
+        self._ok(self.lib.ps_set_smatrix(self.ctx, self._p(S), 1 if S.ndim == 1 else 0,
+                                         None if r is None else self._p(r)))
+        keep = []
+
+        def arr(a):
+            a = np.ascontiguousarray(a, dtype=float)
+            keep.append(a)
+            return a.ctypes.data_as(ctypes.c_void_p)
+
+        def curve(cv):
+            rows = _curve_rows(cv)
+            return _Curve(rows.shape[0], arr(rows))
+
+        def iface(spec):
+            sc, cc = np.asarray(spec.sin_coeffs, float), np.asarray(spec.cos_coeffs, float)
+            return _Iface(spec.mean, sc.size, cc.size, arr(sc) if sc.size else None,
+                          arr(cc) if cc.size else None)
+
+        d = _EmptyDesc()
+        d.period, d.k1, d.k2, d.k3 = cfg.period, cfg.k1, cfg.k2, cfg.k3
+        d.y0, d.eps = cfg.y0, cfg.regularization
+        d.copies, d.Q, d.nrb = (cfg.near_field_copies, cfg.j_expansion_order,
+                                cfg.rb_modes_per_direction)
+        ctr = cfg.expansion_centers()
+        for i, k in enumerate((1, 2, 3)):
+            d.centers[2 * i], d.centers[2 * i + 1] = float(ctr[k][0]), float(ctr[k][1])
+        d.g1, d.g2 = curve(curves["g1"]), curve(curves["g2"])
+        for i, w in enumerate(("L1", "L2", "L3")):
+            d.wall[i] = curve(curves[w])
+        d.lid_up, d.lid_down = curve(curves["Gu"]), curve(curves["Gd"])
+        d.top, d.bottom = iface(cfg.interface_top), iface(cfg.interface_bottom)
+        d.rule_n, d.rule_skip, d.rule_interp = len(rule.nodes), rule.skip, rule.interp
+        d.rule_x, d.rule_w = arr(rule.nodes), arr(rule.weights)
+        theta = np.array([x.incident_angle for x in configs], dtype=float)
+        self._ok(self.lib.ps_setup_empty(self.ctx, ctypes.byref(d), self._p(theta)))
+        n1, n2, nw = curves["g1"].n, curves["g2"].n, curves["L2"].n
+        self.nrow_c = 2 * n1 + 2 * n2 + 2 * nw
+        self.ncol_b = 2 * n1 + 2 * n2 + 2 * cfg.j_expansion_order + 1
+        self.nrb = cfg.rb_modes_per_direction
+
+    def scattering_matrix(self, shape, k2, kp, p, curve, rule):
+        """scatmat.scattering_matrix on the device.  curve =
+        geometry.sample_particle(shape, (0, 0), 0.0, N) (geometry.py:224-256)."""
+        rows = _curve_rows(curve)
+        x = np.ascontiguousarray(rule.nodes, dtype=float)
+        w = np.ascontiguousarray(rule.weights, dtype=float)
+        d = _ParticleDesc(k2, kp, shape.base_radius, shape.bump_amplitude, shape.lobes,
+                          rows.shape[0], self._p(rows), x.size, rule.skip, rule.interp,
+                          self._p(x), self._p(w))
+        S = np.empty((2 * p + 1, 2 * p + 1), dtype=complex)
+        res = ctypes.c_double()
+        self._ok(self.lib.ps_scattering_matrix(self.ctx, ctypes.byref(d), p, self._p(S),
+                                               ctypes.byref(res)))
+        return S
 
     def apply_T(self, beta):
         """multiscat.apply_T with host arrays [nrhs][M][L]."""

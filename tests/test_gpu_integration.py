@@ -28,6 +28,54 @@ def test_ctypes_stub_apply_T_and_solve():
         ps.close()
 
 
+class _Cv:
+    """DiscretizedCurve duck type from empty_setup / scatmat rows."""
+    def __init__(self, rows):
+        self.nodes, self.normals = rows[:, 0:2], rows[:, 2:4]
+        self.speeds, self.weights, self.t, self.arc_weights = rows[:, 4], rows[:, 5], rows[:, 6], rows[:, 7]
+
+    @property
+    def n(self):
+        return self.nodes.shape[0]
+
+
+class _Rule:
+    def __init__(self, order):
+        from paper_1412_7466_b200.empty_setup import correction_rule
+        self.nodes, self.weights, self.skip, self.interp = correction_rule(order)
+
+
+def test_ctypes_stub_setup_from_config_and_bie():
+    """The stub's config path (ps_setup_empty) and Mueller-BIE call on
+    reference-shaped objects: cfg1 solve vs the oracle golden; the rotated
+    star solve vs its golden."""
+    from integration.ctypes_stub import Periscat
+    from oracle import periscat_oracle as O
+    from paper_1412_7466_b200 import empty_setup as es
+    from paper_1412_7466_b200 import grating, scatmat
+    pb = O.load_problem(1)
+    cfg = grating.fixture_config("w10")
+    cell = es.unit_cell(cfg)
+    curves = {"g1": _Cv(cell.g1), "g2": _Cv(cell.g2), "L1": _Cv(cell.walls[0]),
+              "L2": _Cv(cell.walls[1]), "L3": _Cv(cell.walls[2]), "Gu": _Cv(cell.lid_up),
+              "Gd": _Cv(cell.lid_down)}
+    z = np.load(os.path.join(O.GOLDEN, "golden_cfg1.npz"))
+    zs = np.load(os.path.join(O.GOLDEN, "golden_star.npz"))
+    ps = Periscat(0)
+    try:
+        ps.setup_from_config([cfg], curves, _Rule(16), pb.centers, pb.p, pb.smat)
+        beta, c, d, its = ps.solve()
+        assert rel(c[0], z["c"]) <= 1e-9 and rel(d[0], z["d"]) <= 1e-9
+        shape = scatmat.ParticleShape(0.03, 0.01, 3)
+        S = ps.scattering_matrix(shape, 12.0, 15.0, 20, _Cv(scatmat.particle_curve(shape, 300)),
+                                 _Rule(16))
+        ps.setup_from_config([cfg], curves, _Rule(16), pb.centers, pb.p, S, rot=zs["rot"])
+        beta, c, d, its = ps.solve()
+        assert rel(c[0], zs["c"]) <= 1e-9 and rel(d[0], zs["d"]) <= 1e-9
+    finally:
+        ps.close()
+
+
 def test_multiscat_shim_is_the_product():
     from integration.periscat_shim import multiscat
     from paper_1412_7466_b200 import multiscat as product
