@@ -89,5 +89,26 @@ def main(cfgs):
         print(json.dumps(meta), flush=True)
 
 
+def make_curved():
+    """cfg1's inclusions (M=10, r=0.04, p=20) in the grating with the
+    reference's default sinusoidal interfaces (fixture empty_curved, written
+    by oracle/make_empty.py curved): the oracle's full solve, for the device
+    assembly of curved interfaces end to end."""
+    t0 = time.perf_counter()
+    base = O.load_problem(1)
+    pb = O.Problem(O.load_empty("curved"), base.centers, base.p, base.radius)
+    rng = np.random.default_rng(1500)
+    v = pb.smat[None, :] * (rng.standard_normal((pb.M, pb.L)) + 1j * rng.standard_normal((pb.M, pb.L)))
+    sch = O.apply_schur_operator(pb, v).reshape(pb.M, pb.L)
+    sol = O.solve_full(pb)
+    np.savez_compressed(os.path.join(OUT, "golden_curved.npz"), v=v, schur=sch, beta=sol.beta,
+                        c=sol.c, d=sol.d, flux_error=sol.flux["error"],
+                        iterations=sol.iterations)
+    print("curved", sol.iterations, sol.flux, time.perf_counter() - t0, flush=True)
+
+
 if __name__ == "__main__":
-    main([int(a) for a in sys.argv[1:]] or [1, 2, 3, 4])
+    if sys.argv[1:] == ["curved"]:
+        make_curved()
+    else:
+        main([int(a) for a in sys.argv[1:]] or [1, 2, 3, 4])

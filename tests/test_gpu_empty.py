@@ -129,3 +129,25 @@ def test_setup_rejects_mixed_geometry_and_bad_angle():
     bad = grating.baseline_config(10.0, 0.3)
     with pytest.raises(ValueError):
         _setup([bad])
+
+
+@pytest.mark.parametrize("from_config", [False, True])
+def test_curved_grating_solve_matches_oracle(from_config):
+    """cfg1's inclusions in the grating with sinusoidal interfaces (the
+    reference's default InterfaceSpecs): Schur matvec and full solve, from the
+    reference's host system or from the config (device assembly of the curved
+    Nystrom blocks), vs the oracle (oracle/make_goldens.py curved)."""
+    import torch
+
+    from oracle import periscat_oracle as O
+    from paper_1412_7466_b200 import grating, solver
+    pb = O.load_problem(1)
+    z = np.load(os.path.join(O.GOLDEN, "golden_curved.npz"))
+    systems = grating.fixture_config("curved") if from_config else grating.load_fixture("curved")
+    op = solver.SchurOperator(systems, pb.centers, pb.p, smat=pb.smat, device=0)
+    got = op(torch.as_tensor(z["v"][None]).cuda()).cpu().numpy()[0]
+    assert rel(got, z["schur"]) <= MATVEC_TOL
+    sol = solver.solve_full(systems, pb.centers, pb.p, smat=pb.smat, device=0)
+    assert rel(sol.c[0], z["c"]) <= 1e-9 and rel(sol.d[0], z["d"]) <= 1e-9
+    assert abs(sol.flux[0]["error"] - float(z["flux_error"])) <= 1e-9
+    assert abs(sol.iterations[0] - int(z["iterations"])) <= 1
