@@ -151,3 +151,40 @@ def test_curved_grating_solve_matches_oracle(from_config):
     assert rel(sol.c[0], z["c"]) <= 1e-9 and rel(sol.d[0], z["d"]) <= 1e-9
     assert abs(sol.flux[0]["error"] - float(z["flux_error"])) <= 1e-9
     assert abs(sol.iterations[0] - int(z["iterations"])) <= 1
+
+
+def test_setup_argument_errors():
+    """ps_setup_empty / ps_scattering_matrix reject bad input with the
+    reference's ValueError semantics instead of computing garbage."""
+    import ctypes
+
+    from paper_1412_7466_b200 import _lib, grating
+    from paper_1412_7466_b200 import empty_setup as es
+    from paper_1412_7466_b200.engine import Engine
+    cfg = grating.fixture_config("w10")
+    eng = Engine(0)
+    try:
+        eng.set_geometry(np.array([[0.0, 0.0]]), 2, cfg.k2)
+        eng.set_bloch([cfg.bloch_phase])
+        desc, keep = es.build_desc(cfg, es.unit_cell(cfg))
+        th = np.array([cfg.incident_angle])
+        bad = _lib.EmptyDesc.from_buffer_copy(desc)
+        bad.nrb = 40                                  # even Rayleigh-Bloch count (geo:357-358)
+        rc = eng.lib.ps_setup_empty(eng.ctx, ctypes.byref(bad), th.ctypes.data_as(ctypes.c_void_p))
+        assert rc == _lib.PS_ERR_ARG
+        bad = _lib.EmptyDesc.from_buffer_copy(desc)
+        bad.k2 = -1.0
+        rc = eng.lib.ps_setup_empty(eng.ctx, ctypes.byref(bad), th.ctypes.data_as(ctypes.c_void_p))
+        assert rc == _lib.PS_ERR_ARG
+        bad = _lib.EmptyDesc.from_buffer_copy(desc)
+        bad.g1.n = 16                                 # < 4 * skip nodes (quadrature.py:127-128)
+        rc = eng.lib.ps_setup_empty(eng.ctx, ctypes.byref(bad), th.ctypes.data_as(ctypes.c_void_p))
+        assert rc == _lib.PS_ERR_ARG
+        with pytest.raises(_lib.PeriscatError):
+            eng._check(eng.lib.ps_get_empty(eng.ctx, 3, None, None, None, None))
+        # a valid call still works on the same context afterwards
+        eng._check(eng.lib.ps_setup_empty(eng.ctx, ctypes.byref(desc),
+                                          th.ctypes.data_as(ctypes.c_void_p)))
+        del keep
+    finally:
+        eng.close()
