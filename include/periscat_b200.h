@@ -236,6 +236,16 @@ typedef struct ps_empty_desc {
  * Bloch phases are the ones given to ps_set_rhs_bloch (call it first).
  * PS_ERR_NUMERICAL if an SVD does not converge. */
 int ps_setup_empty(ps_ctx* ctx, const ps_empty_desc* desc, const double* theta_host);
+/* Multi-GPU setup split ("each rank does 2 of the 16 RHS
+ * SVDs, then broadcasts"): assemble every RHS but factorise only RHS
+ * [rhs_begin, rhs_end); the other RHS get their restricted A^+ factors with
+ * ps_import_pinv from a buffer the owning rank filled with ps_export_pinv and
+ * broadcast (NCCL).  ps_pinv_bytes: size of that packed buffer (one RHS). */
+int ps_setup_empty_range(ps_ctx* ctx, const ps_empty_desc* desc, const double* theta_host,
+                         int rhs_begin, int rhs_end);
+long long ps_pinv_bytes(const ps_ctx* ctx);
+int ps_export_pinv(ps_ctx* ctx, int irhs, void* dst_dev, void* stream);
+int ps_import_pinv(ps_ctx* ctx, int irhs, const void* src_dev, void* stream);
 /* Rows/columns of the device-assembled A (856 x 781 at the BASELINE geometry). */
 int ps_empty_shape(const ps_ctx* ctx, int* nrow, int* ncol);
 /* Copy one RHS's device-assembled data back (any pointer may be NULL):

@@ -60,6 +60,10 @@ SIGNATURES = {
     "ps_empty_shape": (_I, [_P, _IP, _IP]),
     "ps_get_empty": (_I, [_P, _I, _P, _P, _P, _P]),
     "ps_set_svd_workers": (_I, [_P, _I]),
+    "ps_setup_empty_range": (_I, [_P, _P, _P, _I, _I]),
+    "ps_pinv_bytes": (ctypes.c_longlong, [_P]),
+    "ps_export_pinv": (_I, [_P, _I, _P, _P]),
+    "ps_import_pinv": (_I, [_P, _I, _P, _P]),
     "ps_setup_timings": (_I, [_P, _DP, _DP]),
     "ps_scattering_matrix": (_I, [_P, _P, _I, _P, _DP]),
 }

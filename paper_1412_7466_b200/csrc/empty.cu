@@ -559,7 +559,8 @@ int upload(Ctx* c, T** dst, const T* src, size_t n) {
 
 extern "C" {
 
-int ps_setup_empty(ps_ctx* h, const ps_empty_desc* ds, const double* theta) {
+int ps_setup_empty_range(ps_ctx* h, const ps_empty_desc* ds, const double* theta, int rb,
+                         int re) {
   using namespace ps;
   if (!h) return PS_ERR_ARG;
   Ctx* c = ps::C(h);
@@ -802,7 +803,9 @@ int ps_setup_empty(ps_ctx* h, const ps_empty_desc* ds, const double* theta) {
 
   // SVD per right-hand side, up to c->svd_workers concurrent cuSOLVER streams
   const int dev = c->device;
-  const int nwk = std::max(1, std::min(R, c->svd_workers));
+  if (rb < 0 || re > R || rb > re) return fail(c, PS_ERR_ARG, "ps_setup_empty: bad RHS range");
+  const int nown = re - rb;
+  const int nwk = std::max(1, std::min(std::max(nown, 1), c->svd_workers));
   std::vector<int> rcs(nwk, PS_OK);
   std::vector<std::string> errs(nwk);
   std::lock_guard<std::mutex> dev_lock(g_dev_mu[dev & 63]);
@@ -813,7 +816,7 @@ int ps_setup_empty(ps_ctx* h, const ps_empty_desc* ds, const double* theta) {
   auto work = [&](int wid) {
     cudaSetDevice(dev);
     SvdWorker& w = g_svd[dev][wid];
-    for (int r = wid; r < R; r += nwk) {
+    for (int r = rb + wid; r < re; r += nwk) {
       int rc = svd_run(w, e->d_A + (size_t)r * m * ncol, m, ncol, e->d_s + (size_t)r * ncol,
                        &errs[wid]);
       if (rc) {
@@ -840,7 +843,7 @@ int ps_setup_empty(ps_ctx* h, const ps_empty_desc* ds, const double* theta) {
     for (int w = 0; w < nwk; ++w) th.emplace_back(work, w);
     for (auto& t : th) t.join();
   }
-  c->launches += R;
+  c->launches += nown;
   cudaEventRecord(e2, st);
   cudaEventSynchronize(e2);
   float ms_a = 0, ms_s = 0;
@@ -854,6 +857,53 @@ int ps_setup_empty(ps_ctx* h, const ps_empty_desc* ds, const double* theta) {
   for (int w = 0; w < nwk; ++w)
     if (rcs[w]) return fail(c, rcs[w], "ps_setup_empty: " + errs[w]);
   return PS_OK;
+}
+
+int ps_setup_empty(ps_ctx* h, const ps_empty_desc* ds, const double* theta) {
+  if (!h) return PS_ERR_ARG;
+  return ps_setup_empty_range(h, ds, theta, 0, ps::C(h)->nrhs);
+}
+
+// packed restricted factors of one RHS: Uh | sinv | Vb | cscale | f
+static size_t pinv_bytes(const Ctx* c) {
+  const size_t nsv = c->nsv, nrc = c->nrow_c, nout = c->ncol_b + 2 * c->nrb;
+  return nsv * nrc * 16 + nsv * 8 + nout * nsv * 16 + nout * 8 + nrc * 16;
+}
+
+long long ps_pinv_bytes(const ps_ctx* h) {
+  if (!h) return -1;
+  const Ctx* c = reinterpret_cast<const Ctx*>(h);
+  return c->have_layers && c->nsv > 0 ? (long long)pinv_bytes(c) : -1;
+}
+
+static int pinv_copy(ps_ctx* h, int irhs, void* dev, void* stream, bool out) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = ps::C(h);
+  if (!dev || irhs < 0 || irhs >= c->nrhs) return fail(c, PS_ERR_ARG, "ps_*_pinv: bad argument");
+  auto& R = c->rhs[irhs];
+  if (!c->have_layers || c->nsv <= 0 || !R.d_Uh)
+    return fail(c, PS_ERR_STATE, "ps_*_pinv: no factors allocated (call ps_setup_empty first)");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, PS_ERR_CUDA, "cudaSetDevice");
+  const size_t nsv = c->nsv, nrc = c->nrow_c, nout = c->ncol_b + 2 * c->nrb;
+  void* parts[5] = {R.d_Uh, R.d_sinv, R.d_Vb, R.d_cscale, R.d_f};
+  const size_t sz[5] = {nsv * nrc * 16, nsv * 8, nout * nsv * 16, nout * 8, nrc * 16};
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  char* p = reinterpret_cast<char*>(dev);
+  for (int i = 0; i < 5; ++i) {
+    const cudaError_t e = out ? cudaMemcpyAsync(p, parts[i], sz[i], cudaMemcpyDeviceToDevice, st)
+                              : cudaMemcpyAsync(parts[i], p, sz[i], cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return fail(c, PS_ERR_CUDA, "ps_*_pinv: copy");
+    p += sz[i];
+  }
+  return PS_OK;
+}
+
+int ps_export_pinv(ps_ctx* h, int irhs, void* dst_dev, void* stream) {
+  return pinv_copy(h, irhs, dst_dev, stream, true);
+}
+
+int ps_import_pinv(ps_ctx* h, int irhs, const void* src_dev, void* stream) {
+  return pinv_copy(h, irhs, const_cast<void*>(src_dev), stream, false);
 }
 
 int ps_empty_shape(const ps_ctx* h, int* nrow, int* ncol) {

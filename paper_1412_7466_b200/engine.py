@@ -120,10 +120,12 @@ class Engine:
         self.nout = self.ncol_b + 2 * nrb
         self._layer_cols = system.cols
 
-    def setup_empty(self, configs, svd_workers: int | None = None):
+    def setup_empty(self, configs, svd_workers: int | None = None, rhs_range=None):
         """Device assembly + SVD of the empty-grating system of every RHS
         (ps_setup_empty; replaces set_layers + set_pinv with host factors).
-        Returns one DeviceEmptySystem per config."""
+        rhs_range=(b, e): factorise only those RHS (the multi-GPU split; the
+        others come in through import_pinv).  Returns one DeviceEmptySystem
+        per config."""
         from . import empty_setup as es
         configs = es.validate(configs)
         if len(configs) != self.nrhs:
@@ -133,7 +135,9 @@ class Engine:
         theta = _f64([c.incident_angle for c in configs])
         if svd_workers is not None:
             self._check(self.lib.ps_set_svd_workers(self.ctx, int(svd_workers)))
-        self._check(self.lib.ps_setup_empty(self.ctx, ctypes.byref(desc), _ptr(theta)))
+        b, e = (0, len(configs)) if rhs_range is None else rhs_range
+        self._check(self.lib.ps_setup_empty_range(self.ctx, ctypes.byref(desc), _ptr(theta),
+                                                  int(b), int(e)))
         del keep
         cfg = configs[0]
         n1, n2, nw = cell.g1.shape[0], cell.g2.shape[0], cell.walls[1].shape[0]
@@ -146,6 +150,19 @@ class Engine:
         self.coupled = True
         return [es.DeviceEmptySystem(c, cell.cols, cell.rows, cell.centers, self, r)
                 for r, c in enumerate(configs)]
+
+    def pinv_bytes(self) -> int:
+        """Bytes of one RHS's packed restricted A^+ factors (ps_pinv_bytes)."""
+        return int(self.lib.ps_pinv_bytes(self.ctx))
+
+    def export_pinv(self, irhs: int, buf: torch.Tensor):
+        """Pack RHS irhs's factors into a uint8 CUDA tensor of pinv_bytes()."""
+        self._check(self.lib.ps_export_pinv(self.ctx, int(irhs), ctypes.c_void_p(buf.data_ptr()),
+                                            _stream(self.device)))
+
+    def import_pinv(self, irhs: int, buf: torch.Tensor):
+        self._check(self.lib.ps_import_pinv(self.ctx, int(irhs), ctypes.c_void_p(buf.data_ptr()),
+                                            _stream(self.device)))
 
     def get_empty(self, irhs: int):
         """(A, f, col_scale, s) of a device-assembled RHS (ps_get_empty)."""

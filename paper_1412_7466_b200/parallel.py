@@ -93,6 +93,31 @@ def all_reduce_(t: torch.Tensor, group=None) -> torch.Tensor:
     return t
 
 
+def setup_empty_split(eng, configs, group=None):
+    """Multi-GPU empty-grating setup ("each rank does 2 of the
+    16 RHS SVDs, then broadcasts"): every rank assembles all RHS on its device
+    (one launch, ~1 ms) but factorises only its share shard_range(R, rank,
+    world); each RHS's packed A^+ factors (15 MB at the BASELINE geometry) are
+    then broadcast from the owning rank over NCCL."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    R = len(configs)
+    if world == 1 or R == 1:
+        return eng.setup_empty(configs)
+    rank = dist.get_rank(group)
+    systems = eng.setup_empty(configs, rhs_range=shard_range(R, rank, world))
+    buf = torch.empty(eng.pinv_bytes(), dtype=torch.uint8, device=eng.device)
+    for q in range(R):
+        owner = next(r for r in range(world) if shard_range(R, r, world)[0] <= q
+                     < shard_range(R, r, world)[1])
+        if owner == rank:
+            eng.export_pinv(q, buf)
+        dist.broadcast(buf, src=owner if group is None else dist.get_global_rank(group, owner),
+                       group=group)
+        if owner != rank:
+            eng.import_pinv(q, buf)
+    return systems
+
+
 class ShardedSchur:
     """Distributed S-preconditioned Schur operator on top of a SchurOperator
     whose engine owns targets shard_range(M, rank, world).

@@ -55,7 +55,10 @@ class SchurOperator:
         self.systems = items
         if coupled:
             if self.device_setup:
-                self.systems = eng.setup_empty(configs)
+                # under torch.distributed the per-angle SVDs are split across
+                # ranks and the factors broadcast (parallel.setup_empty_split)
+                from .parallel import setup_empty_split
+                self.systems = setup_empty_split(eng, configs)
             else:
                 eng.set_layers(items[0])
                 for r, s in enumerate(items):

@@ -18,7 +18,7 @@ CSRC = os.path.join(ROOT, "paper_1412_7466_b200", "csrc")
 
 def _declared():
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(ps_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void|long long|const char\*)\s+(ps_\w+)\s*\(", txt, re.M)))
 
 
 def test_header_declares_api():

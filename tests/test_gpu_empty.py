@@ -188,3 +188,39 @@ def test_setup_argument_errors():
         del keep
     finally:
         eng.close()
+
+
+def test_setup_split_and_factor_exchange():
+    """The multi-GPU setup split on one device: two contexts each factorise
+    half of cfg5's 16 angles (ps_setup_empty_range) and exchange the packed
+    A^+ factors (ps_export_pinv / ps_import_pinv -- what
+    parallel.setup_empty_split broadcasts over NCCL); both then apply the same
+    16-RHS Schur operator as a context that factorised everything."""
+    import torch
+
+    from oracle import periscat_oracle as O
+    from paper_1412_7466_b200 import grating, solver
+    from paper_1412_7466_b200.engine import Engine
+    pb = O.load_problem(1)
+    cfgs = [grating.fixture_config(n) for n in grating.CFG5_ANGLES]
+    ref = solver.SchurOperator(cfgs, pb.centers, pb.p, smat=pb.smat, device=0)
+    engs = [Engine(0), Engine(0)]
+    ops = []
+    for i, e in enumerate(engs):
+        e.set_geometry(pb.centers, pb.p, cfgs[0].k2, cfgs[0].period, cfgs[0].near_field_copies)
+        e.set_bloch([c.bloch_phase for c in cfgs])
+        e.set_smatrix(pb.smat)
+        e.setup_empty(cfgs, rhs_range=(8 * i, 8 * i + 8))
+    buf = torch.empty(engs[0].pinv_bytes(), dtype=torch.uint8, device="cuda")
+    for q in range(16):
+        src, dst = (engs[0], engs[1]) if q < 8 else (engs[1], engs[0])
+        src.export_pinv(q, buf)
+        dst.import_pinv(q, buf)
+    rng = np.random.default_rng(4)
+    v = torch.as_tensor(pb.smat[None, None, :] * (rng.standard_normal((16, pb.M, pb.L))
+                                                 + 1j * rng.standard_normal((16, pb.M, pb.L)))).cuda()
+    want = ref(v).cpu().numpy()
+    for e in engs:
+        got = e.apply_schur(v).cpu().numpy()
+        assert rel(got, want) <= 1e-14
+        e.close()

@@ -7,6 +7,12 @@ the GPU's beta on a target slice for RHS 0 and 15 and reports
 ||K beta - rhs|| / ||rhs|| there (a full oracle matvec would take ~1 core-hour).
 
     python tools/solve_cfg5.py [--check] [--out profiles/r01_cfg5_solve.json]
+
+Multi-GPU (one process per GPU, NCCL): target-sharded operator, the 16 SVDs
+split across ranks with their factors broadcast (parallel.setup_empty_split),
+distributed GMRES (parallel.gmres_dist):
+
+    torchrun --nproc-per-node 8 --master-addr 127.0.0.1 tools/solve_cfg5.py
 """
 import os
 
@@ -44,8 +50,23 @@ else:                                       # configs only: assembly + SVD on th
     systems = [grating.fixture_config(n) for n in grating.CFG5_ANGLES]
 t_svd = time.perf_counter() - t0
 
+world = int(os.environ.get("WORLD_SIZE", "1"))
+rank = int(os.environ.get("RANK", "0"))
+if world > 1:
+    import torch.distributed as dist
+
+    from paper_1412_7466_b200 import parallel
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    M = centers.shape[0]
+    trange = parallel.shard_range(M, rank, world)
+else:
+    local, trange = 0, None
+
 t1 = time.perf_counter()
-op = solver.SchurOperator(systems, centers, p, radius=radius)
+op = solver.SchurOperator(systems, centers, p, radius=radius, device=local, target_range=trange)
+sharded = parallel.ShardedSchur(op) if world > 1 else None
 rhs = op.rhs()
 torch.cuda.synchronize()
 t_setup = time.perf_counter() - t1
@@ -53,21 +74,32 @@ setup_dev = op.eng.setup_timings() if op.device_setup else None
 systems = op.systems
 
 t2 = time.perf_counter()
-beta, its, hist = solver.gmres(op, rhs, 1e-10, a.maxit)
-x = op.recover(beta)
+if world > 1:
+    beta, its, hist = parallel.gmres_dist(sharded, rhs, 1e-10, a.maxit, engine=op.eng)
+    x = sharded.recover(beta.contiguous())
+else:
+    beta, its, hist = solver.gmres(op, rhs, 1e-10, a.maxit)
+    x = op.recover(beta)
 c, d = op.split_cd(x)
 torch.cuda.synchronize()
 t_solve = time.perf_counter() - t2
+if world > 1:
+    tt = torch.tensor([t_setup, t_solve], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_setup, t_solve = tt.tolist()
 flux = [postproc.flux_error(c[r], d[r], s.config)["error"] for r, s in enumerate(systems)]
 res = dict(workload="cfg5: M=10000, p=20, 16 RHS, omega=10, theta_B in [-pi/3, pi/3]",
            setup_mode="host SVD of reference fixtures" if a.host_setup else
-           "device assembly + cuSOLVER SVD from configs (ps_setup_empty)",
+           "device assembly + cuSOLVER SVD from configs (ps_setup_empty)"
+           + (f", SVDs split over {world} ranks + NCCL broadcast" if world > 1 else ""),
+           n_gpus=world,
            host_prep_seconds=t_svd, setup_seconds=t_setup, setup_device_ms=setup_dev,
            solve_seconds=t_solve,
            iterations=its, flux_error=flux, max_flux_error=max(flux))
-print(json.dumps(res), flush=True)
+if rank == 0:
+    print(json.dumps(res), flush=True)
 
-if a.check:
+if a.check and world == 1:
     from oracle import periscat_oracle as O
     bh = beta.cpu().numpy()
     rh = rhs.cpu().numpy()
@@ -88,6 +120,8 @@ if a.check:
                                  seconds=time.perf_counter() - ts)
         print(r, checks[f"rhs{r}"], flush=True)
     res["oracle_slice_check"] = dict(targets=sl.tolist(), **checks)
-if a.out:
+if a.out and rank == 0:
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     json.dump(res, open(a.out, "w"), indent=1)
+if world > 1:
+    dist.destroy_process_group()
