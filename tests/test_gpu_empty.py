@@ -45,7 +45,7 @@ def _check_against_fixture(got, ref):
     assert np.all(np.diff(s) <= 0)
 
 
-@pytest.mark.parametrize("name", ["w10", "wood", "w10_a00", "w10_a15", "curved"])
+@pytest.mark.parametrize("name", ["w10", "wood", "w10_a00", "w10_a15", "curved", "w10_P0", "w10_P2"])
 def test_device_assembly_matches_reference_system(name):
     """A, f, col_scale and singular values of the device-assembled system vs
     the reference's assemble_empty_system output (fixture) for the BASELINE
