@@ -341,6 +341,12 @@ def run_ours(args):
                     "setup (S, geometry, coupling blocks), GMRES to 1e-10 and recovery; "
                     "max over ranks"}
 
+    # the other BASELINE configs that fit one step (cfg1 M=10, cfg2 M=100, cfg4
+    # Wood anomaly M=1000): one Schur matvec and solve_full(config) each
+    others = None
+    if world == 1 and not args.no_cfg5:
+        others = other_configs(local)
+
     # cfg5 (M=1e4, p=20, 16 incidence angles): the multi-RHS K1 alone, own
     # target shard, translations/s over the whole job, K1m roofline
     cfg5 = None
@@ -385,12 +391,54 @@ def run_ours(args):
                 "gpu_launches": int(stats["launches"]),
                 "clocks": clk.summary(),
                 "full_solve_m1000": full,
+                "other_configs": others,
                 "cfg5_apply_T_16rhs": cfg5}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def other_configs(local):
+    """cfg1 / cfg2 / cfg4 (BASELINE configs[0, 1, 3]): Schur matvec time and
+    warm solve_full(config) seconds with iterations and flux error."""
+    import torch
+
+    from paper_1412_7466_b200 import grating, solver
+    out = {}
+    for cfg in (1, 2, 4):
+        sysm, centers, p, radius = grating.load_config(cfg)
+        conf = sysm.config
+        M, L = centers.shape[0], 2 * p + 1
+        op = solver.SchurOperator(conf, centers, p, radius=radius, device=local)
+        rng = np.random.default_rng(cfg)
+        v = torch.as_tensor(op.smat[None, None, :] * (rng.standard_normal((1, M, L))
+                            + 1j * rng.standard_normal((1, M, L)))).cuda()
+        y = torch.empty_like(v)
+        for _ in range(3):
+            op(v, out=y)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = 20
+        e0.record()
+        for _ in range(n):
+            op(v, out=y)
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / n
+        solver.solve_full(conf, centers, p, radius=radius, device=local)     # warm
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        sol = solver.solve_full(conf, centers, p, radius=radius, device=local)
+        torch.cuda.synchronize()
+        out[f"cfg{cfg}"] = {"M": M, "p": p, "matvec_ms": ms,
+                            "translations_per_s": M * (3 * M - 1) / (ms * 1e-3),
+                            "full_solve_seconds": time.perf_counter() - t,
+                            "iterations": sol.iterations[0],
+                            "flux_error": sol.flux[0]["error"]}
+        del op
+    return out
 
 
 def cfg5_apply_T(dev, local, rank, world, dfma_peak, tensor_peak, args):
