@@ -174,6 +174,20 @@ class ClockSampler:
                 "power_w_max": max(pw) if pw else None, "samples": len(rows)}
 
 
+def _guarded(fn, world):
+    """Run an auxiliary measurement block; on one GPU a failure is recorded in
+    the JSON line instead of losing the headline (with several ranks an
+    exception must propagate: a rank leaving a collective would hang the rest)."""
+    if world > 1:
+        return fn()
+    try:
+        return fn()
+    except Exception as e:   # noqa: BLE001 -- reported, not swallowed
+        import traceback
+        traceback.print_exc(file=sys.stderr)
+        return {"error": f"{type(e).__name__}: {e}"}
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def run_ours(args):
     import torch
@@ -321,31 +335,34 @@ def run_ours(args):
         return solver.Solution(None, c, d, its, hist, [fl],
                                dict(assemble_ms=a_ms, svd_ms=s_ms))
 
-    full_solve()                                 # warm
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ts = time.perf_counter()
-    sol = full_solve()
-    torch.cuda.synchronize()
-    tsol = torch.tensor([time.perf_counter() - ts], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tsol, op=dist.ReduceOp.MAX)
-    full = {"seconds": float(tsol.item()), "iterations": sol.iterations[0],
-            "flux_error": sol.flux[0]["error"],
-            "driver": "ps_gmres (device)" if world == 1 else "parallel.gmres_dist (NCCL)",
-            "setup_device_ms": {"empty_assembly": sol.timings.get("assemble_ms"),
-                                "svd_and_pinv_factors": sol.timings.get("svd_ms")},
-            "note": "wall clock from the grating config and the inclusion centres: device "
-                    "assembly of the 856x781 empty-grating matrix, cuSOLVER SVD, operator "
-                    "setup (S, geometry, coupling blocks), GMRES to 1e-10 and recovery; "
-                    "max over ranks"}
+    def timed_full_solve():
+        full_solve()                                 # warm
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ts = time.perf_counter()
+        sol = full_solve()
+        torch.cuda.synchronize()
+        tsol = torch.tensor([time.perf_counter() - ts], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tsol, op=dist.ReduceOp.MAX)
+        return {"seconds": float(tsol.item()), "iterations": sol.iterations[0],
+                "flux_error": sol.flux[0]["error"],
+                "driver": "ps_gmres (device)" if world == 1 else "parallel.gmres_dist (NCCL)",
+                "setup_device_ms": {"empty_assembly": sol.timings.get("assemble_ms"),
+                                    "svd_and_pinv_factors": sol.timings.get("svd_ms")},
+                "note": "wall clock from the grating config and the inclusion centres: device "
+                        "assembly of the 856x781 empty-grating matrix, cuSOLVER SVD, operator "
+                        "setup (S, geometry, coupling blocks), GMRES to 1e-10 and recovery; "
+                        "max over ranks"}
+
+    full = _guarded(timed_full_solve, world)
 
     # the other BASELINE configs that fit one step (cfg1 M=10, cfg2 M=100, cfg4
     # Wood anomaly M=1000): one Schur matvec and solve_full(config) each
     others = None
     if world == 1 and not args.no_cfg5:
-        others = other_configs(local)
+        others = _guarded(lambda: other_configs(local), world)
 
     # cfg5 (M=1e4, p=20, 16 incidence angles): the multi-RHS K1 alone, own
     # target shard, translations/s over the whole job, K1m roofline
@@ -353,12 +370,16 @@ def run_ours(args):
     if not args.no_cfg5:
         sus = ctypes.c_double()
         _lib.check(None, lib.ps_dfma_sustained(local, 3.0, ctypes.byref(sus)))
-        cfg5 = cfg5_apply_T(dev, local, rank, world, sus.value, tpeak.value, args)
+        cfg5 = _guarded(lambda: cfg5_apply_T(dev, local, rank, world, sus.value, tpeak.value,
+                                             args), world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, cores, sample, _ = cpu_oracle_rate(3, 1)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        def cpu_leg():
+            rate, cores, sample, _ = cpu_oracle_rate(3, 1)
+            return {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                    "sample": sample}
+        cpu = _guarded(cpu_leg, world)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
