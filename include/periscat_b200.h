@@ -258,6 +258,30 @@ int ps_set_svd_workers(ps_ctx* ctx, int workers);
 /* Device time of the last ps_setup_empty: assembly and SVD + factor restriction. */
 int ps_setup_timings(const ps_ctx* ctx, double* assemble_ms, double* svd_ms);
 
+/* ---- empty-grating fields at points --------------- */
+
+/* Number of empty-grating unknowns (columns of A, 781 at the BASELINE
+ * geometry) ps_recover_full returns; -1 if the factors carry no field rows. */
+int ps_full_columns(const ps_ctx* ctx);
+/* x = A^+ (f - g) over ALL columns, in the reference order mu1, sigma1, mu2,
+ * sigma2, a2, a1, a3, c, d (empty_grating.py:154-156; the recovery of
+ * solve_full), g = C beta reduced over ranks.  x [nrhs][ncol]. */
+int ps_recover_full(ps_ctx* ctx, const void* g_dev, void* x_dev, void* stream);
+/* Layer-field data for ps_layer_field when the factors came from ps_set_pinv
+ * (ps_setup_empty sets them itself): k1, k3, expansion centres 1 and 3
+ * (geometry.py:398-406) and the incident wave vector per RHS,
+ * inc [nrhs][2] = k1 (cos theta, sin theta) (empty_grating.py:32-42). */
+int ps_set_field_params(ps_ctx* ctx, double k1, double k3, const double* c1_host,
+                        const double* c3_host, const double* inc_host);
+/* Total empty-grating layer field at points (empty_grating.eval_empty_field,
+ * eg:352-393, total=True: phased layer potentials of the bounding interfaces
+ * + the layer's regular expansion + the incident wave in layer 1) from x of
+ * ps_recover_full.  pts [npts][2] f64 and layer [npts] int (1, 2, 3; other
+ * values give 0) on the device; out [nrhs][npts] complex.  Plain smooth
+ * quadrature: keep points ~5 node spacings off the interfaces (lp:244-246). */
+int ps_layer_field(ps_ctx* ctx, const void* x_dev, int npts, const double* pts_dev,
+                   const int* layer_dev, void* out_dev, void* stream);
+
 /* ---- particle scattering matrix ------------------- */
 
 /* Star-shaped particle r(t) = a1 + a2 cos(a3 t) (ParticleShape,

@@ -1,11 +1,12 @@
 """Drop-in ``periscat.postproc`` on top of the reference's
 own ``empty_grating`` module.
 
-``eval_total_field_grid`` evaluates the total field on a grid: the particle
-phased multipole sums on the B200 (``ps_particle_field``), and the empty-grating
-layer fields + u_inc with the reference's ``eval_empty_field`` (eg:352-393) on
-the recovered empty-grating unknowns x = A^+ (f - C beta) (
-``apply_pinv``, eg:264-273).
+``eval_total_field_grid`` evaluates the total field on a grid on the B200:
+the particle phased multipole sums (``ps_particle_field``) and the
+empty-grating layer fields + u_inc (``ps_layer_field`` on x = A^+ (f - C beta),
+``ps_recover_full``; the device restatement of eval_empty_field, eg:352-393).
+``reference=True`` evaluates the layer fields with the reference's own
+``eval_empty_field`` on the host instead.
 """
 from __future__ import annotations
 
@@ -27,7 +28,10 @@ def empty_solution(op, beta, system, irhs: int = 0):
     return EmptySolution(system, x, residual=float("nan"))
 
 
-def eval_total_field_grid(op, beta, systems, centers, radius, nx=128, ny=128, y_plot=None):
+def eval_total_field_grid(op, beta, systems, centers, radius, nx=128, ny=128, y_plot=None,
+                          reference: bool = False):
+    if not reference:
+        return _grid(op, beta, centers, radius, nx=nx, ny=ny, y_plot=y_plot, layer_field="device")
     from periscat.empty_grating import eval_empty_field
     systems = systems if isinstance(systems, (list, tuple)) else [systems]
     sols = [empty_solution(op, beta, s, r) for r, s in enumerate(systems)]

@@ -66,6 +66,10 @@ SIGNATURES = {
     "ps_import_pinv": (_I, [_P, _I, _P, _P]),
     "ps_setup_timings": (_I, [_P, _DP, _DP]),
     "ps_scattering_matrix": (_I, [_P, _P, _I, _P, _DP]),
+    "ps_full_columns": (_I, [_P]),
+    "ps_recover_full": (_I, [_P, _P, _P, _P]),
+    "ps_set_field_params": (_I, [_P, _D, _D, _P, _P, _P]),
+    "ps_layer_field": (_I, [_P, _P, _I, _P, _P, _P, _P]),
 }
 
 

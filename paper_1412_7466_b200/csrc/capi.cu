@@ -78,7 +78,7 @@ void ps_destroy(ps_ctx* h) {
   Ctx* c = C(h);
   cudaSetDevice(c->device);
   void* ptrs[] = {c->d_centers, c->d_S, c->d_rot, c->d_g1, c->d_g2, c->d_w2, c->d_blochpow,
-                  c->d_partial, c->d_work};
+                  c->d_partial, c->d_work, c->d_inc};
   for (void* p : ptrs)
     if (p) ps::dev_free(p);
   for (auto& r : c->rhs) {
@@ -245,7 +245,11 @@ int ps_set_pinv(ps_ctx* h, int irhs, int nrow, int ncol, const double* U, const 
   const int nsv = ncol;   // reduced SVD of an nrow x ncol matrix, nrow >= ncol
   c->nsv = nsv;
   const int nrc = c->nrow_c;
-  const int nout = c->ncol_b + 2 * c->nrb;
+  const int nj = 2 * c->Q + 1;
+  const int nout0 = c->ncol_b + 2 * c->nrb;
+  // field rows: the a1 / a3 columns (eg:154-156: right after a2) when present
+  c->nfield = (c->ncol_b + 2 * nj <= ncol) ? 2 * nj : 0;
+  const int nout = nout0 + c->nfield;
   // Uh[k][i] = conj(U[i][k]) for the C rows i < nrow_c
   std::vector<double2> uh((size_t)nsv * nrc);
   for (int k = 0; k < nsv; ++k)
@@ -255,13 +259,14 @@ int ps_set_pinv(ps_ctx* h, int irhs, int nrow, int ncol, const double* U, const 
     }
   std::vector<double> sinv(nsv);
   for (int k = 0; k < nsv; ++k) sinv[k] = std::fmin(1.0 / s[k], 1.0 / eps);
-  // Vb[o][k] = conj(Vh[k][col(o)]) for the output columns (B cols, c, d)
+  // Vb[o][k] = conj(Vh[k][col(o)]) for the output columns (B cols, c, d, then a1, a3)
   std::vector<int> outcol(nout);
   for (int o = 0; o < c->ncol_b; ++o) outcol[o] = o;
   for (int o = 0; o < c->nrb; ++o) {
     outcol[c->ncol_b + o] = col_c + o;
     outcol[c->ncol_b + c->nrb + o] = col_d + o;
   }
+  for (int o = 0; o < c->nfield; ++o) outcol[nout0 + o] = c->ncol_b + o;
   std::vector<double2> vb((size_t)nout * nsv);
   std::vector<double> cs(nout);
   for (int o = 0; o < nout; ++o) {
@@ -324,6 +329,62 @@ int ps_particle_field(ps_ctx* h, const void* beta, int npts, const double* pts, 
   if (int rc = set_device(c)) return rc;
   return ps::particle_field(c, reinterpret_cast<const double2*>(beta), pts, npts,
                             reinterpret_cast<double2*>(out), reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_set_field_params(ps_ctx* h, double k1, double k3, const double* c1, const double* c3,
+                        const double* inc) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (!c1 || !c3 || !inc || !(k1 > 0) || !(k3 > 0)) {
+    c->err = "ps_set_field_params: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  if (int rc = dev_upload(c, &c->d_inc, inc, 2 * (size_t)c->nrhs)) return rc;
+  c->f_k1 = k1;
+  c->f_k3 = k3;
+  c->f_c1[0] = c1[0];
+  c->f_c1[1] = c1[1];
+  c->f_c3[0] = c3[0];
+  c->f_c3[1] = c3[1];
+  c->have_field = 1;
+  return PS_OK;
+}
+
+int ps_full_columns(const ps_ctx* h) {
+  if (!h) return -1;
+  const Ctx* c = reinterpret_cast<const Ctx*>(h);
+  if (!c->have_layers || c->nfield == 0) return -1;
+  return c->ncol_b + 2 * c->nrb + c->nfield;
+}
+
+int ps_recover_full(ps_ctx* h, const void* g, void* x, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (!g || !x) {
+    c->err = "ps_recover_full: null pointer";
+    return PS_ERR_ARG;
+  }
+  if (!c->have_layers || c->nsv <= 0) {
+    c->err = "ps_recover_full: no empty-grating factors";
+    return PS_ERR_STATE;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::recover_full(c, reinterpret_cast<const double2*>(g), reinterpret_cast<double2*>(x),
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_layer_field(ps_ctx* h, const void* x, int npts, const double* pts, const int* layer,
+                   void* out, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (npts < 0 || (npts > 0 && (!x || !pts || !layer || !out))) {
+    c->err = "ps_layer_field: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::layer_field(c, reinterpret_cast<const double2*>(x), pts, layer, npts,
+                         reinterpret_cast<double2*>(out), reinterpret_cast<cudaStream_t>(stream));
 }
 
 int ps_apply_T_blocks(ps_ctx* h, int part, int nparts, const void* beta, void* out, void* stream) {

@@ -561,7 +561,7 @@ struct Work {
 
 size_t work_stride(const Ctx* c) {
   const size_t nrc = c->nrow_c, nsv = c->nsv > 0 ? c->nsv : 1;
-  const size_t nout = c->ncol_b + 2 * c->nrb;
+  const size_t nout = c->ncol_b + 2 * c->nrb + c->nfield;
   const size_t mtl = (size_t)(c->t_end - c->t_begin) * c->L;
   const size_t nch = c->have_layers ? (size_t)b_chunks(c) : 0;
   return nrc + nsv + nout + 2 * mtl + 512 * nrc + nch * mtl + 8;
@@ -569,7 +569,7 @@ size_t work_stride(const Ctx* c) {
 
 int work(Ctx* c, int r, Work* w) {
   const size_t nrc = c->nrow_c, nsv = c->nsv > 0 ? c->nsv : 1;
-  const size_t nout = c->ncol_b + 2 * c->nrb;
+  const size_t nout = c->ncol_b + 2 * c->nrb + c->nfield;
   const size_t mtl = (size_t)(c->t_end - c->t_begin) * c->L;
   const size_t per = work_stride(c);
   const size_t need = per * c->nrhs;
@@ -837,6 +837,43 @@ int schur_rhs(Ctx* c, double2* rhs, cudaStream_t st) {
     } else {
       if (int rc = s_apply(c, nullptr, w.bsub, rhs + r * out_stride, st, 1.0)) return rc;
     }
+  }
+  return PS_OK;
+}
+
+// restricted output row o -> column of the empty-grating unknown vector
+// (eg:154-156): B columns (mu1..a2) as is, then c, d, then the field rows a1, a3
+__global__ void scatter_full(const double2* __restrict__ xr, int ncol_b, int nrb, int nj,
+                             int nout, int nfield, double2* __restrict__ x) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= nout + nfield) return;
+  int col;
+  if (o < ncol_b) col = o;
+  else if (o < ncol_b + nrb) col = ncol_b + 2 * nj + (o - ncol_b);                // c
+  else if (o < nout) col = ncol_b + 2 * nj + nrb + (o - ncol_b - nrb);             // d
+  else col = ncol_b + (o - nout);                                                  // a1, a3
+  x[col] = xr[o];
+}
+
+int recover_full(Ctx* c, const double2* g, double2* x, cudaStream_t st) {
+  const int nout = c->ncol_b + 2 * c->nrb;
+  const int nj = 2 * c->Q + 1;
+  if (c->nfield != 2 * nj) {
+    c->err = "recover_full: factors without the a1 / a3 field rows";
+    return PS_ERR_STATE;
+  }
+  const int ncol = nout + c->nfield;
+  for (int r = 0; r < c->nrhs; ++r) {
+    Work w;
+    if (int rc = work(c, r, &w)) return rc;
+    f_minus<<<(c->nrow_c + 255) / 256, 256, 0, st>>>(c->rhs[r].d_f, g + (size_t)r * c->nrow_c,
+                                                     c->nrow_c, w.g);
+    PS_CUDA_TRY(c, cudaGetLastError());
+    if (int rc = pinv(c, r, w.g, w.x, ncol, st)) return rc;
+    scatter_full<<<(ncol + 255) / 256, 256, 0, st>>>(w.x, c->ncol_b, c->nrb, nj, nout, c->nfield,
+                                                      x + (size_t)r * ncol);
+    PS_CUDA_TRY(c, cudaGetLastError());
+    c->launches += 2;
   }
   return PS_OK;
 }

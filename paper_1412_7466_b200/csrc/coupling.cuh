@@ -11,6 +11,8 @@ int schur_finish(Ctx* c, const double2* v_own, const double2* a_own, const doubl
                  double2* y, cudaStream_t st);
 int schur_rhs(Ctx* c, double2* rhs, cudaStream_t st);
 int recover(Ctx* c, const double2* g, double2* x, cudaStream_t st);
+// all empty-grating unknowns x [nrhs][ncol] in the reference column order
+int recover_full(Ctx* c, const double2* g, double2* x, cudaStream_t st);
 // coupling_dense.cu
 int precompute_coupling(Ctx* c, double max_bytes);
 void release_dense_coupling(Ctx* c);

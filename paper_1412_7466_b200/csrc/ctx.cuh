@@ -58,6 +58,12 @@ struct Ctx {
   int ncol_b = 0;           // 2*n1 + 2*n2 + (2Q+1)
   int nrb = 0;              // Rayleigh-Bloch orders per direction (c, d)
   int nsv = 0;              // number of singular values
+  int nfield = 0;           // extra restricted-V rows kept for field evaluation (a1, a3 columns)
+  // layer-field evaluation (ps_layer_field): k1, k3, expansion centres 1 / 3,
+  // incident wave vector per RHS k1 (cos theta, sin theta)
+  int have_field = 0;
+  double f_k1 = 0, f_k3 = 0, f_c1[2] = {0, 0}, f_c3[2] = {0, 0};
+  double* d_inc = nullptr;  // [nrhs][2]
   int k1_variant = 0;       // 0 auto (K1s when all targets owned), 1 tiled K1, 2 symmetric K1s
   int mrhs_variant = 0;     // 0 auto (K1d DMMA for >= 12 RHS), 1 DFMA K1m, 2 DMMA K1d
   int dense = 0;            // 1: apply C and B from the pre-assembled matrices

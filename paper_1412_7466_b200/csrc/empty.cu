@@ -382,10 +382,11 @@ __global__ void pinv_extract_kernel(const double2* __restrict__ U, const double*
                                     const double2* __restrict__ VT,
                                     const double* __restrict__ cs_full,
                                     const double2* __restrict__ f_full, int m, int ncol, int nrc,
-                                    int ncol_b, int nrb, int col_c, int col_d, double eps,
-                                    double2* Uh, double* sinv, double2* Vb, double* cs,
+                                    int ncol_b, int nrb, int col_c, int col_d, int nfield,
+                                    double eps, double2* Uh, double* sinv, double2* Vb, double* cs,
                                     double2* f) {
-  const int nout = ncol_b + 2 * nrb;
+  const int nout0 = ncol_b + 2 * nrb;
+  const int nout = nout0 + nfield;   // + the a1 / a3 field rows
   const long long nu = (long long)ncol * nrc, nv = (long long)nout * ncol;
   const long long tot = nu + nv + ncol + nout + nrc;
   for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x; id < tot;
@@ -397,7 +398,8 @@ __global__ void pinv_extract_kernel(const double2* __restrict__ U, const double*
     } else if (id < nu + nv) {
       const long long q = id - nu;
       const int o = (int)(q / ncol), k = (int)(q % ncol);
-      const int col = o < ncol_b ? o : (o < ncol_b + nrb ? col_c + o - ncol_b : col_d + o - ncol_b - nrb);
+      const int col = o < ncol_b ? o : (o < ncol_b + nrb ? col_c + o - ncol_b
+                                       : (o < nout0 ? col_d + o - ncol_b - nrb : ncol_b + o - nout0));
       const double2 v = VT[(size_t)col * ncol + k];
       Vb[q] = c2(v.x, -v.y);
     } else if (id < nu + nv + ncol) {
@@ -405,7 +407,8 @@ __global__ void pinv_extract_kernel(const double2* __restrict__ U, const double*
       sinv[k] = fmin(1.0 / s[k], 1.0 / eps);
     } else if (id < nu + nv + ncol + nout) {
       const int o = (int)(id - nu - nv - ncol);
-      const int col = o < ncol_b ? o : (o < ncol_b + nrb ? col_c + o - ncol_b : col_d + o - ncol_b - nrb);
+      const int col = o < ncol_b ? o : (o < ncol_b + nrb ? col_c + o - ncol_b
+                                       : (o < nout0 ? col_d + o - ncol_b - nrb : ncol_b + o - nout0));
       cs[o] = cs_full[col];
     } else {
       const int i = (int)(id - nu - nv - ncol - nout);
@@ -790,8 +793,26 @@ int ps_setup_empty_range(ps_ctx* h, const ps_empty_desc* ds, const double* theta
     if (int rc = upload(c, &c->d_w2, w2.data(), w2.size())) return rc;
     c->have_layers = 1;
   }
-  const int nsv = ncol, nrc = c->nrow_c, nout = c->ncol_b + 2 * nrb;
+  const int nsv = ncol, nrc = c->nrow_c;
   c->nsv = nsv;
+  c->nfield = 2 * nj;                    // keep the a1 / a3 rows for field evaluation
+  const int nout = c->ncol_b + 2 * nrb + c->nfield;
+  // layer-field parameters (ps_layer_field)
+  {
+    std::vector<double> inc(2 * (size_t)R);
+    for (int r = 0; r < R; ++r) {
+      inc[2 * r] = ds->k1 * std::cos(theta[r]);
+      inc[2 * r + 1] = ds->k1 * std::sin(theta[r]);
+    }
+    if (int rc = upload(c, &c->d_inc, inc.data(), inc.size())) return rc;
+    c->f_k1 = ds->k1;
+    c->f_k3 = ds->k3;
+    c->f_c1[0] = ctr[0];
+    c->f_c1[1] = ctr[1];
+    c->f_c3[0] = ctr[4];
+    c->f_c3[1] = ctr[5];
+    c->have_field = 1;
+  }
   for (int r = 0; r < R; ++r) {
     auto& Rd = c->rhs[r];
     if (int rc = upload<double2>(c, &Rd.d_Uh, nullptr, (size_t)nsv * nrc)) return rc;
@@ -827,7 +848,7 @@ int ps_setup_empty_range(ps_ctx* h, const ps_empty_desc* ds, const double* theta
       const long long totx = (long long)nsv * nrc + (long long)nout * nsv + nsv + nout + nrc;
       pinv_extract_kernel<<<(int)std::min<long long>((totx + 255) / 256, 4096), 256, 0, w.st>>>(
           w.U, e->d_s + (size_t)r * ncol, w.VT, e->d_cs + (size_t)r * ncol,
-          e->d_f + (size_t)r * m, m, ncol, nrc, c->ncol_b, nrb, c_c, c_d, ds->eps, Rd.d_Uh,
+          e->d_f + (size_t)r * m, m, ncol, nrc, c->ncol_b, nrb, c_c, c_d, c->nfield, ds->eps, Rd.d_Uh,
           Rd.d_sinv, Rd.d_Vb, Rd.d_cscale, Rd.d_f);
       if (cudaStreamSynchronize(w.st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
         rcs[wid] = PS_ERR_CUDA;
@@ -866,7 +887,7 @@ int ps_setup_empty(ps_ctx* h, const ps_empty_desc* ds, const double* theta) {
 
 // packed restricted factors of one RHS: Uh | sinv | Vb | cscale | f
 static size_t pinv_bytes(const Ctx* c) {
-  const size_t nsv = c->nsv, nrc = c->nrow_c, nout = c->ncol_b + 2 * c->nrb;
+  const size_t nsv = c->nsv, nrc = c->nrow_c, nout = c->ncol_b + 2 * c->nrb + c->nfield;
   return nsv * nrc * 16 + nsv * 8 + nout * nsv * 16 + nout * 8 + nrc * 16;
 }
 
@@ -884,7 +905,7 @@ static int pinv_copy(ps_ctx* h, int irhs, void* dev, void* stream, bool out) {
   if (!c->have_layers || c->nsv <= 0 || !R.d_Uh)
     return fail(c, PS_ERR_STATE, "ps_*_pinv: no factors allocated (call ps_setup_empty first)");
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, PS_ERR_CUDA, "cudaSetDevice");
-  const size_t nsv = c->nsv, nrc = c->nrow_c, nout = c->ncol_b + 2 * c->nrb;
+  const size_t nsv = c->nsv, nrc = c->nrow_c, nout = c->ncol_b + 2 * c->nrb + c->nfield;
   void* parts[5] = {R.d_Uh, R.d_sinv, R.d_Vb, R.d_cscale, R.d_f};
   const size_t sz[5] = {nsv * nrc * 16, nsv * 8, nout * nsv * 16, nout * 8, nrc * 16};
   auto st = reinterpret_cast<cudaStream_t>(stream);

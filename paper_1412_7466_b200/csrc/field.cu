@@ -152,4 +152,173 @@ int particle_field(Ctx* c, const double2* beta, const double* pts, int npts, dou
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Empty-grating layer fields at points (empty_grating.eval_empty_field,
+// empty_grating.py:352-393, total=True): per point, the representation of the
+// layer it lies in -- the phased single + double layers of the bounding
+// interfaces (phased_layer_field, eg:319-338, smooth quadrature as
+// layerpot.eval_layer_potentials, lp:240-263), the layer's regular expansion
+// (specialfn.regular_wave_block, sf:86-125) and, in layer 1, the incident
+// wave (incident_field, eg:32-42) -- from the full unknown vector
+// x = A^+ (f - C beta) (ps_recover_full).  Thread per (point, RHS).
+namespace {
+
+__device__ __forceinline__ double2 fcmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+struct LayerArgs {
+  const double2* x;        // [nrhs][ncol]
+  const double* pts;       // [npts][2]
+  const int* layer;        // [npts]: 1, 2, 3 (anything else -> 0)
+  const double* g1;        // [n1][5] x y nx ny aw
+  const double* g2;        // [n2][5]
+  const double2* bpow;     // [nrhs][2P+3]
+  const double* inc;       // [nrhs][2]
+  double2* out;            // [nrhs][npts]
+  int npts, ncol, n1, n2, Q, copies, np;
+  int c_mu1, c_s1, c_mu2, c_s2, c_a2, c_a1, c_a3;
+  double k1, k2, k3, period;
+  double c1x, c1y, c2x, c2y, c3x, c3y;
+};
+
+// sum_l alpha^l sum_j aw_j [S_k(x, y_j + l d) sigma_j + D_k(x, y_j + l d) mu_j]
+__device__ double2 layer_potential(const LayerArgs& a, const double* cv, int n, const double2* mu,
+                                   const double2* sg, double k, const double2* bp, double px,
+                                   double py) {
+  double2 tot = make_double2(0.0, 0.0);
+  for (int l = -a.copies; l <= a.copies; ++l) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int j = 0; j < n; ++j) {
+      const double* y = cv + (size_t)j * 5;
+      const double u0 = px - (y[0] + l * a.period), u1 = py - y[1];
+      const double r = hypot(u0, u1);
+      double j0, j1, y0, y1;
+      bessel_jy01(k * r, miller_start_j01(k * r), &j0, &j1, &y0, &y1);
+      const double udn = (u0 * y[2] + u1 * y[3]) / r;
+      // S = (i/4) H0, D = (i/4) k H1 (u . n_y) / r  (layerpot.py:69-91)
+      const double2 sv = make_double2(-0.25 * y0, 0.25 * j0);
+      const double2 dv = make_double2(-0.25 * k * udn * y1, 0.25 * k * udn * j1);
+      const double2 s = sg[j], m = mu[j];
+      const double aw = y[4];
+      acc.x += aw * (sv.x * s.x - sv.y * s.y + dv.x * m.x - dv.y * m.y);
+      acc.y += aw * (sv.x * s.y + sv.y * s.x + dv.x * m.y + dv.y * m.x);
+    }
+    const double2 w = bp[l + a.copies + 1];
+    const double2 t = fcmul(w, acc);
+    tot.x += t.x;
+    tot.y += t.y;
+  }
+  return tot;
+}
+
+// sum_{n=-Q}^{Q} a_n J_n(k r) e^{i n theta} about (cx, cy)
+__device__ double2 regular_sum(const double2* an, int Q, double k, double cx, double cy, double px,
+                               double py) {
+  const double dx = px - cx, dy = py - cy;
+  const double r = hypot(dx, dy);
+  if (r == 0.0) return an[Q];
+  double J[80];
+  double inv, y0, y1;
+  bessel_jy_sweep(k * r, Q, [&](int nu, double v) { J[nu] = v; }, &inv, &y0, &y1);
+  const double c = dx / r, s = dy / r;
+  double2 acc = make_double2(an[Q].x * J[0] * inv, an[Q].y * J[0] * inv);
+  double pr = 1.0, pi = 0.0;   // e^{i n theta}
+  for (int n = 1; n <= Q; ++n) {
+    const double qr = pr * c - pi * s, qi = pr * s + pi * c;
+    pr = qr;
+    pi = qi;
+    const double jn = J[n] * inv;
+    const double jm = (n & 1) ? -jn : jn;               // J_{-n} = (-1)^n J_n
+    const double2 ap = an[Q + n], am = an[Q - n];
+    // a_n J_n e^{in th} + a_{-n} J_{-n} e^{-in th}
+    acc.x += jn * (ap.x * pr - ap.y * pi) + jm * (am.x * pr + am.y * pi);
+    acc.y += jn * (ap.x * pi + ap.y * pr) + jm * (am.y * pr - am.x * pi);
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(128) layer_field_kernel(LayerArgs a) {
+  const int pt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (pt >= a.npts) return;
+  const int ly = a.layer[pt];
+  double2 u = make_double2(0.0, 0.0);
+  const double px = a.pts[2 * pt], py = a.pts[2 * pt + 1];
+  const double2* x = a.x + (size_t)r * a.ncol;
+  const double2* bp = a.bpow + (size_t)r * a.np;
+  if (ly == 1) {
+    u = layer_potential(a, a.g1, a.n1, x + a.c_mu1, x + a.c_s1, a.k1, bp, px, py);
+    const double2 e = regular_sum(x + a.c_a1, a.Q, a.k1, a.c1x, a.c1y, px, py);
+    double sn, cs;
+    sincos(px * a.inc[2 * r] + py * a.inc[2 * r + 1], &sn, &cs);
+    u = make_double2(u.x + e.x + cs, u.y + e.y + sn);
+  } else if (ly == 2) {
+    const double2 u1 = layer_potential(a, a.g1, a.n1, x + a.c_mu1, x + a.c_s1, a.k2, bp, px, py);
+    const double2 u2 = layer_potential(a, a.g2, a.n2, x + a.c_mu2, x + a.c_s2, a.k2, bp, px, py);
+    const double2 e = regular_sum(x + a.c_a2, a.Q, a.k2, a.c2x, a.c2y, px, py);
+    u = make_double2(u1.x + u2.x + e.x, u1.y + u2.y + e.y);
+  } else if (ly == 3) {
+    u = layer_potential(a, a.g2, a.n2, x + a.c_mu2, x + a.c_s2, a.k3, bp, px, py);
+    const double2 e = regular_sum(x + a.c_a3, a.Q, a.k3, a.c3x, a.c3y, px, py);
+    u = make_double2(u.x + e.x, u.y + e.y);
+  }
+  a.out[(size_t)r * a.npts + pt] = u;
+}
+
+}  // namespace
+
+int layer_field(Ctx* c, const double2* x, const double* pts, const int* layer, int npts,
+                double2* out, cudaStream_t st) {
+  if (!c->have_layers || !c->have_field || c->nfield == 0) {
+    c->err = "ps_layer_field: no empty-grating setup with field data (ps_setup_empty, or "
+             "ps_set_pinv + ps_set_field_params)";
+    return PS_ERR_STATE;
+  }
+  if (c->Q + 1 > 79) {
+    c->err = "ps_layer_field: j_expansion_order > 78 unsupported";
+    return PS_ERR_UNSUPPORTED;
+  }
+  if (npts == 0) return PS_OK;
+  const int nj = 2 * c->Q + 1;
+  LayerArgs a;
+  a.x = x;
+  a.pts = pts;
+  a.layer = layer;
+  a.g1 = c->d_g1;
+  a.g2 = c->d_g2;
+  a.bpow = c->d_blochpow;
+  a.inc = c->d_inc;
+  a.out = out;
+  a.npts = npts;
+  a.ncol = c->ncol_b + 2 * nj + 2 * c->nrb;
+  a.n1 = c->n1;
+  a.n2 = c->n2;
+  a.Q = c->Q;
+  a.copies = c->copies;
+  a.np = 2 * c->copies + 3;
+  a.c_mu1 = 0;
+  a.c_s1 = c->n1;
+  a.c_mu2 = 2 * c->n1;
+  a.c_s2 = 2 * c->n1 + c->n2;
+  a.c_a2 = 2 * c->n1 + 2 * c->n2;
+  a.c_a1 = a.c_a2 + nj;
+  a.c_a3 = a.c_a1 + nj;
+  a.k1 = c->f_k1;
+  a.k2 = c->k2;
+  a.k3 = c->f_k3;
+  a.period = c->period;
+  a.c1x = c->f_c1[0];
+  a.c1y = c->f_c1[1];
+  a.c2x = c->x2[0];
+  a.c2y = c->x2[1];
+  a.c3x = c->f_c3[0];
+  a.c3y = c->f_c3[1];
+  layer_field_kernel<<<dim3((npts + 127) / 128, c->nrhs), 128, 0, st>>>(a);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  c->launches += 1;
+  return PS_OK;
+}
+
 }  // namespace ps

@@ -306,6 +306,46 @@ class Engine:
         self._check(self.lib.ps_recover(self.ctx, gp, o, _stream(self.device)))
         return out
 
+    def recover_full(self, g: torch.Tensor) -> torch.Tensor:
+        """x = A^+ (f - g) over all empty-grating columns (ps_recover_full),
+        [nrhs][ncol] in the reference column order."""
+        ncol = int(self.lib.ps_full_columns(self.ctx))
+        if ncol <= 0:
+            raise RuntimeError("factors without field rows (set up the empty grating first)")
+        out = torch.empty((self.nrhs, ncol), dtype=torch.complex128, device=self.device)
+        gp = self._dev(g, (self.nrhs, self.nrow_c))
+        self._check(self.lib.ps_recover_full(self.ctx, gp, ctypes.c_void_p(out.data_ptr()),
+                                             _stream(self.device)))
+        return out
+
+    def set_field_params(self, configs):
+        """k1, k3, expansion centres and incident wave vectors for
+        layer_field when the factors came from set_pinv (host SVD)."""
+        cfg = configs[0]
+        ctr = cfg.expansion_centers()
+        inc = _f64([[c.k1 * np.cos(c.incident_angle), c.k1 * np.sin(c.incident_angle)]
+                    for c in configs])
+        c1, c3 = _f64(ctr[1]), _f64(ctr[3])
+        self._check(self.lib.ps_set_field_params(self.ctx, float(cfg.k1), float(cfg.k3), _ptr(c1),
+                                                 _ptr(c3), _ptr(inc)))
+
+    def layer_field(self, x: torch.Tensor, points, layer) -> torch.Tensor:
+        """[nrhs][npts] empty-grating layer field (+ incident in layer 1) at
+        points of the given layers (ps_layer_field)."""
+        pts = torch.as_tensor(np.ascontiguousarray(np.asarray(points, dtype=float).reshape(-1, 2)),
+                              device=self.device)
+        lay = torch.as_tensor(np.ascontiguousarray(np.asarray(layer, dtype=np.int32).ravel()),
+                              device=self.device)
+        out = torch.empty((self.nrhs, pts.shape[0]), dtype=torch.complex128, device=self.device)
+        if pts.shape[0] == 0:
+            return out
+        xp = x.to(device=self.device, dtype=torch.complex128).contiguous()
+        self._check(self.lib.ps_layer_field(self.ctx, ctypes.c_void_p(xp.data_ptr()),
+                                            int(pts.shape[0]), ctypes.c_void_p(pts.data_ptr()),
+                                            ctypes.c_void_p(lay.data_ptr()),
+                                            ctypes.c_void_p(out.data_ptr()), _stream(self.device)))
+        return out
+
     def gmres(self, rhs: torch.Tensor, tol: float = 1e-10, maxit: int = 150):
         x = torch.empty_like(rhs)
         r = self._dev(rhs, (self.nrhs, self.M, self.L))

@@ -48,6 +48,21 @@ def particle_field(op, beta, points) -> np.ndarray:
     return eng.particle_field(b, points).cpu().numpy()
 
 
+def empty_field(op, beta, points, layer) -> np.ndarray:
+    """[nrhs][npts] total empty-grating layer field (empty_grating.eval_empty_field,
+    eg:352-393, total=True) of the coupled solution at points of the given
+    layers (1 / 2 / 3), on the device: x = A^+ (f - C beta) over all columns
+    (ps_recover_full), then the layer potentials + regular expansions +
+    incident wave (ps_layer_field)."""
+    import torch
+    eng = op.eng if hasattr(op, "eng") else op
+    b = torch.as_tensor(np.asarray(beta, dtype=complex)) if not isinstance(beta, torch.Tensor) \
+        else beta
+    b = b.to(device=eng.device, dtype=torch.complex128).reshape(eng.nrhs, eng.M, eng.L).contiguous()
+    x = eng.recover_full(eng.apply_C(b))
+    return eng.layer_field(x, points, layer).cpu().numpy()
+
+
 def _interface_heights(config, system, x):
     if hasattr(config, "interface_top"):                      # reference ProblemConfig
         return (config.interface_top.height(x, config.period),
@@ -83,14 +98,15 @@ def classify_points(config, points, centers, radius: float, system=None,
 
 
 def eval_total_field_grid(op, beta, centers, radius: float, nx: int = 128, ny: int = 128,
-                          y_plot: float | None = None, layer_field=None) -> dict:
+                          y_plot: float | None = None, layer_field="device") -> dict:
     """SPEC.md:619-627 on a uniform grid over [-d/2, d/2] x [-y_plot, y_plot].
 
-    Particle phased multipole sums come from the device (layer-2 points);
-    ``layer_field(points) -> [nrhs][npts]`` supplies the empty-grating layer
-    fields + u_inc (the reference's ``empty_grating.eval_empty_field`` on the
-    solution x_empty = A^+(f - C beta), eg:352-393); without it the result is
-    the particle part only.  Masked points (inside particles, near interfaces)
+    Particle phased multipole sums come from the device (layer-2 points).
+    The empty-grating layer fields + u_inc (eval_empty_field on x_empty =
+    A^+(f - C beta), eg:352-393) are evaluated on the device too
+    (``layer_field="device"``), or by a callable ``layer_field(points) ->
+    [nrhs][npts]`` (e.g. the reference's own evaluator); ``None`` gives the
+    particle part only.  Masked points (inside particles, near interfaces)
     are NaN and flagged in ``mask``."""
     cfg = op.config
     d = cfg.period
@@ -122,7 +138,11 @@ def eval_total_field_grid(op, beta, centers, radius: float, nx: int = 128, ny: i
     in2 = (layer == 2) & ~masked
     if np.any(in2):
         u[:, in2] = particle_field(op, beta, pts[in2])
-    if layer_field is not None:
+    if isinstance(layer_field, str) and layer_field == "device":
+        ok = ~masked
+        lay = np.where(ok, layer, 0)
+        u += empty_field(op, beta, pts, lay)
+    elif layer_field is not None:
         u += np.asarray(layer_field(pts), dtype=complex).reshape(op.nrhs, -1)
     u[:, masked] = np.nan
     return dict(x=xs, y=ys, field=u.reshape(op.nrhs, ny, nx), layer=layer.reshape(ny, nx),

@@ -63,6 +63,8 @@ class SchurOperator:
                 eng.set_layers(items[0])
                 for r, s in enumerate(items):
                     eng.set_pinv(r, s)
+                if hasattr(cfg, "expansion_centers"):     # layer fields (ps_layer_field)
+                    eng.set_field_params(configs)
         elif self.device_setup:
             self.systems = [_ConfigOnly(c) for c in configs]
         if target_range is not None:

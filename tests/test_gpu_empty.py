@@ -224,3 +224,23 @@ def test_setup_split_and_factor_exchange():
         got = e.apply_schur(v).cpu().numpy()
         assert rel(got, want) <= 1e-14
         e.close()
+
+
+@pytest.mark.parametrize("name,golden", [("w10", "golden_cfg1.npz"), ("curved", "golden_curved.npz")])
+@pytest.mark.parametrize("from_config", [False, True])
+def test_layer_fields_match_reference_evaluator(name, golden, from_config):
+    """Device layer fields (ps_recover_full + ps_layer_field) of the golden
+    coupled solution vs the reference's own empty_grating.eval_empty_field
+    (eg:352-393, total=True) at grid points of all three layers
+    (oracle/make_fields.py), from host reference factors and from the config."""
+    from oracle import periscat_oracle as O
+    from paper_1412_7466_b200 import grating, postproc, solver
+    pb = O.load_problem(1)
+    z = np.load(os.path.join(O.GOLDEN, f"field_{name}.npz"))
+    systems = grating.fixture_config(name) if from_config else grating.load_fixture(name)
+    op = solver.SchurOperator(systems, pb.centers, pb.p, smat=pb.smat, device=0)
+    got = postproc.empty_field(op, z["beta"][None], z["pts"], z["layer"])[0]
+    ref = z["field"]
+    for ly in (1, 2, 3):
+        sel = z["layer"] == ly
+        assert rel(got[sel], ref[sel]) <= 1e-10, (ly, rel(got[sel], ref[sel]))

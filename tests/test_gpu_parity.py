@@ -494,7 +494,8 @@ def test_eval_total_field_grid_cfg2(O):
     op = solver.SchurOperator(sysm, pb.centers, pb.p, smat=pb.smat)
     rng = np.random.default_rng(4)
     beta = pb.smat[None, None, :] * _cplx(rng, (1, pb.M, pb.L))
-    res = postproc.eval_total_field_grid(op, beta, pb.centers, 0.04, nx=60, ny=50, y_plot=0.7)
+    res = postproc.eval_total_field_grid(op, beta, pb.centers, 0.04, nx=60, ny=50, y_plot=0.7,
+                                         layer_field=None)
     xx, yy = np.meshgrid(res["x"], res["y"])
     pts = np.column_stack([xx.ravel(), yy.ravel()])
     layer, masked = postproc.classify_points(op.config, pts, pb.centers, 0.04, system=sysm)

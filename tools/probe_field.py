@@ -19,9 +19,16 @@ op = solver.SchurOperator(sysm, centers, p, radius=radius)
 beta = sol.beta
 M, L = centers.shape[0], 2 * p + 1
 for n in (128, 256, 512):
+    postproc.eval_total_field_grid(op, beta, centers, radius, nx=n, ny=n, y_plot=0.7)   # warm
+    torch.cuda.synchronize()
     t = time.perf_counter()
-    res = postproc.eval_total_field_grid(op, beta, centers, radius, nx=n, ny=n, y_plot=0.5)
+    res = postproc.eval_total_field_grid(op, beta, centers, radius, nx=n, ny=n, y_plot=0.7)
+    torch.cuda.synchronize()
     dt = time.perf_counter() - t
+    t = time.perf_counter()
+    postproc.eval_total_field_grid(op, beta, centers, radius, nx=n, ny=n, y_plot=0.7,
+                                   layer_field=None)
+    dpo = time.perf_counter() - t
     npts = int((~res["mask"] & (res["layer"] == 2)).sum())
     pts = np.column_stack([np.repeat(res["y"], n) * 0, np.repeat(res["y"], n)])
     xx, yy = np.meshgrid(res["x"], res["y"])
@@ -31,7 +38,8 @@ for n in (128, 256, 512):
     u = postproc.particle_field(op, beta, P2)
     dk = time.perf_counter() - t
     pairs = npts * M * 3
-    print(f"grid {n}x{n}: {npts} layer-2 points, eval_total_field_grid {dt*1e3:.1f} ms, "
+    print(f"grid {n}x{n}: {npts} layer-2 points, eval_total_field_grid (layer fields + "
+          f"particles, all on the device) {dt*1e3:.1f} ms (particles only {dpo*1e3:.1f} ms), "
           f"particle_field {dk*1e3:.1f} ms = {pairs/dk:.3e} point-source pairs/s", flush=True)
 sl = P2[:: max(1, P2.shape[0] // 200)][:200]
 t = time.perf_counter()
