@@ -510,11 +510,10 @@ int launch_b(Ctx* c, const double2* x, const double2* bpow, double2* bpart, doub
   a.x2x = c->x2[0];
   a.x2y = c->x2[1];
   if (a.nt <= 0) return PS_OK;
-  static bool attr = false;
-  if (!attr && S::SMEM > 48 * 1024) {
+  static unsigned long long attr_mask = 0;
+  if (S::SMEM > 48 * 1024 && first_on_device(&attr_mask, c->device)) {
     PS_CUDA_TRY(c, cudaFuncSetAttribute(b_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)S::SMEM));
-    attr = true;
   }
   b_kernel<P><<<dim3(a.nt, a.nchunk), kBT, S::SMEM, st>>>(a);
   PS_CUDA_TRY(c, cudaGetLastError());

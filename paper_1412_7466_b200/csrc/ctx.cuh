@@ -105,6 +105,15 @@ struct Ctx {
 
 inline Ctx* C(ps_ctx* h) { return reinterpret_cast<Ctx*>(h); }
 
+// cudaFuncSetAttribute is per device: a launcher keeps one bit per device it
+// has configured (a repeated call from racing threads is harmless)
+inline bool first_on_device(unsigned long long* mask, int device) {
+  const unsigned long long bit = 1ull << (device & 63);
+  if (*mask & bit) return false;
+  *mask |= bit;
+  return true;
+}
+
 // Device memory of every context comes from the device's stream-ordered
 // default pool with a 4 GiB release threshold: freed blocks stay cached, so a
 // new context (e.g. each solve_full) reuses the previous one's coupling

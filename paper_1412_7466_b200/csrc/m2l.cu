@@ -366,11 +366,10 @@ int launch_p(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
     ctx->partial_elems = need;
   }
   a.partial = ctx->d_partial;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static unsigned long long attr_mask = 0;
+  if (first_on_device(&attr_mask, ctx->device)) {
     PS_CUDA_TRY(ctx, cudaFuncSetAttribute(m2l_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)S::SMEM));
-    attr_done = true;
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (ctx->profile) {

@@ -396,11 +396,10 @@ int launch_m(Ctx* ctx, const double2* beta, double2* out, int mode, const double
                                                   total, bw);
   PS_CUDA_TRY(ctx, cudaGetLastError());
   ctx->launches += 1;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static unsigned long long attr_mask = 0;
+  if (first_on_device(&attr_mask, ctx->device)) {
     PS_CUDA_TRY(ctx, cudaFuncSetAttribute(m2l_mrhs_kernel<P>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
-    attr_done = true;
   }
   const long long in_stride = (long long)ctx->M * S::L, out_stride = (long long)nt * S::L;
   for (a.rg0 = 0; a.rg0 < ctx->nrhs; a.rg0 += kRG) {

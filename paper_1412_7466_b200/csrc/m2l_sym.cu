@@ -510,11 +510,10 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   bloch_weight_1<<<2 * ctx->sm_count, 256, 0, ks>>>(beta, bpow - 1, ctx->M, S::L, a.ncp, bw, bws,
                                                     bwr, bwsr);
   PS_CUDA_TRY(ctx, cudaGetLastError());
-  static bool attr_done = false;
-  if (!attr_done) {
+  static unsigned long long attr_mask = 0;
+  if (first_on_device(&attr_mask, ctx->device)) {
     PS_CUDA_TRY(ctx, cudaFuncSetAttribute(m2l_sym_kernel<P>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
-    attr_done = true;
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (ctx->profile) {
