@@ -70,7 +70,8 @@ class SchurOperator:
         if target_range is not None:
             eng.set_target_range(*target_range)
         # pre-assembled B / C blocks when they fit (else matrix-free K3/K5)
-        self.dense = bool(coupled and dense_gb > 0 and eng.precompute_coupling(dense_gb))
+        self.dense = bool(coupled and dense_gb > 0 and eng.M > 0
+                          and eng.precompute_coupling(dense_gb))
         self.M, self.p, self.L, self.nrhs = eng.M, p, eng.L, eng.nrhs
         self.device = eng.device
 
@@ -149,9 +150,17 @@ def solve_full(systems, centers, p: int, radius: float | None = None, smat=None,
     cfg = op.config
     tol = cfg.gmres_tol if tol is None else tol
     maxit = cfg.gmres_maxit if maxit is None else maxit
-    rhs = op.rhs()
-    beta, its, hist = gmres(op, rhs, tol, maxit)
-    x = op.recover(beta)
+    if op.M == 0:
+        # no inclusions: the empty grating's own solution
+        # x = A^+ f (empty_grating.solve_empty, eg:276-290)
+        beta = torch.zeros(op.shape, dtype=torch.complex128, device=op.device)
+        its, hist = [0] * op.nrhs, [[0.0] for _ in range(op.nrhs)]
+        g = torch.zeros((op.nrhs, op.eng.nrow_c), dtype=torch.complex128, device=op.device)
+        x = op.eng.recover(g)
+    else:
+        rhs = op.rhs()
+        beta, its, hist = gmres(op, rhs, tol, maxit)
+        x = op.recover(beta)
     c, d = op.split_cd(x)
     torch.cuda.synchronize(op.device)
     t2 = time.perf_counter()

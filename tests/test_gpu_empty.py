@@ -244,3 +244,21 @@ def test_layer_fields_match_reference_evaluator(name, golden, from_config):
     for ly in (1, 2, 3):
         sel = z["layer"] == ly
         assert rel(got[sel], ref[sel]) <= 1e-10, (ly, rel(got[sel], ref[sel]))
+
+
+@pytest.mark.parametrize("from_config", [False, True])
+def test_no_inclusions_reduces_to_empty_grating(from_config):
+    """M = 0 (SPEC.md:545-547 degeneracy): solve_full returns the empty
+    grating's own solution x = A^+ f (empty_grating.solve_empty, eg:276-290)
+    and its flux balance."""
+    from paper_1412_7466_b200 import grating, postproc, solver
+    ref = grating.load_fixture("w10")
+    u, s, vh = np.linalg.svd(ref.matrix, full_matrices=False)
+    x = ref.col_scale * (vh.conj().T @ (np.minimum(1 / s, 1e10) * (u.conj().T @ ref.rhs)))
+    c_ref, d_ref = x[ref.cols["c"]], x[ref.cols["d"]]
+    systems = grating.fixture_config("w10") if from_config else ref
+    sol = solver.solve_full(systems, np.zeros((0, 2)), 20, radius=0.04, device=0)
+    assert sol.iterations[0] == 0
+    assert rel(sol.c[0], c_ref) <= 1e-12 and rel(sol.d[0], d_ref) <= 1e-12
+    fl = postproc.flux_error(c_ref, d_ref, ref.config)["error"]
+    assert abs(sol.flux[0]["error"] - fl) <= 1e-12 and fl < 1e-12
