@@ -509,3 +509,25 @@ def test_eval_total_field_grid_cfg2(O):
               for l in (-1, 0, 1))
     assert rel(f[sel], ref) <= 1e-12
     assert np.all(f[(layer != 2) & ~masked] == 0)
+
+
+@pytest.mark.parametrize("cfg,nrhs", [(3, 1), (2, 16)])
+def test_matvec_and_solve_are_bit_reproducible(O, cfg, nrhs):
+    """SPEC.md:507 / 576: apply_T has a deterministic order -- every device
+    reduction (M2L partials, coupling splits, GMRES dots) runs in a fixed
+    order, so repeated Schur matvecs and GMRES solves are bitwise identical
+    (K1s + SM-partitioned coupling for cfg3, K1d for 16 RHS)."""
+    from paper_1412_7466_b200 import grating, solver
+    pb = O.load_problem(cfg)
+    sysm = grating.load_fixture(O.CONFIGS[cfg]["empty"])
+    systems = [sysm] * nrhs
+    op = solver.SchurOperator(systems, pb.centers, pb.p, smat=pb.smat)
+    rng = np.random.default_rng(99)
+    v = _dev(pb.smat[None, None, :] * _cplx(rng, (nrhs, pb.M, pb.L)))
+    y0 = op(v).cpu().numpy()
+    for _ in range(3):
+        assert np.array_equal(op(v).cpu().numpy(), y0)
+    if nrhs == 1:
+        x1, _, _ = solver.gmres(op, op.rhs(), 1e-10, 150)
+        x2, _, _ = solver.gmres(op, op.rhs(), 1e-10, 150)
+        assert torch.equal(x1, x2)
