@@ -33,6 +33,8 @@ from paper_1412_7466_b200 import grating, postproc, solver
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--check", action="store_true")
+ap.add_argument("--check-full", action="store_true",
+                help="oracle Schur residual of RHS 0 over ALL targets (one process per core)")
 ap.add_argument("--out", default=None)
 ap.add_argument("--maxit", type=int, default=150)
 ap.add_argument("--host-setup", action="store_true",
@@ -120,6 +122,50 @@ if a.check and world == 1:
                                  seconds=time.perf_counter() - ts)
         print(r, checks[f"rhs{r}"], flush=True)
     res["oracle_slice_check"] = dict(targets=sl.tolist(), **checks)
+def _full_worker(args):
+    """Oracle (T beta - B A^+ C beta) on a target chunk of cfg5 RHS 0."""
+    chunk, xg = args
+    from oracle import periscat_oracle as O
+    st = _FULL
+    u = O.apply_T(st["beta"], st["centers"], st["es"].k2, st["p"], st["es"].bloch, st["es"].period,
+                  st["es"].copies, targets=chunk)
+    return u, O.apply_B_phys(st["es"], xg, st["centers"][chunk], st["p"])
+
+
+_FULL = {}
+
+if a.check_full and world == 1:
+    import multiprocessing as mp
+
+    from oracle import periscat_oracle as O
+    ts = time.perf_counter()
+    bh = beta.cpu().numpy()[0]
+    rh = rhs.cpu().numpy()[0]
+    es = O.load_empty(grating.CFG5_ANGLES[0])
+    pb = O.Problem(es, centers, p, radius)
+    xg = es.apply_pinv(O.apply_C(es, bh, centers))
+    _FULL.update(beta=bh, centers=centers, es=es, p=p)
+    ncores = len(os.sched_getaffinity(0))
+    chunks = [c for c in np.array_split(np.arange(centers.shape[0]), 8 * ncores) if c.size]
+    with mp.get_context("fork").Pool(ncores) as pool:
+        parts = pool.map(_full_worker, [(c, xg) for c in chunks])
+    uT = np.concatenate([q[0] for q in parts], axis=0)
+    uB = np.concatenate([q[1] for q in parts], axis=0)
+    y = bh - pb.smat[None, :] * (uT - uB)
+    # the GPU's own pieces on the same beta (RHS 0): M2L and the whole operator
+    gT = op.apply_T(beta).cpu().numpy()[0]
+    gK = op(beta).cpu().numpy()[0]
+    res["oracle_full_check"] = dict(
+        rhs=0, targets=int(centers.shape[0]), processes=ncores,
+        residual=float(np.linalg.norm(y - rh) / np.linalg.norm(rh)),
+        gpu_residual=float(np.linalg.norm(gK - rh) / np.linalg.norm(rh)),
+        operator_diff=float(np.linalg.norm(gK - y) / np.linalg.norm(y)),
+        apply_T_diff=float(np.linalg.norm(gT - uT) / np.linalg.norm(uT)),
+        apply_T_diff_S=float(np.linalg.norm(pb.smat * (gT - uT)) / np.linalg.norm(pb.smat * uT)),
+        seconds=time.perf_counter() - ts)
+    print(res["oracle_full_check"], flush=True)
+    np.savez_compressed(os.path.join(os.path.dirname(a.out) if a.out else ".", "cfg5_full_check.npz"),
+                        beta=bh, rhs=rh, y_cpu=y, y_gpu=gK, uT_cpu=uT, uB_cpu=uB, uT_gpu=gT)
 if a.out and rank == 0:
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     json.dump(res, open(a.out, "w"), indent=1)
