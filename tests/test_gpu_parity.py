@@ -531,3 +531,41 @@ def test_matvec_and_solve_are_bit_reproducible(O, cfg, nrhs):
         x1, _, _ = solver.gmres(op, op.rhs(), 1e-10, 150)
         x2, _, _ = solver.gmres(op, op.rhs(), 1e-10, 150)
         assert torch.equal(x1, x2)
+
+
+_FULL3 = {}
+
+
+def _cfg3_chunk(args):
+    chunk, v, xg = args
+    pb = _FULL3["pb"]
+    from oracle import periscat_oracle as Ox
+    u = Ox.apply_T(v, pb.centers, pb.es.k2, pb.p, pb.es.bloch, pb.es.period, pb.es.copies,
+                   targets=chunk)
+    return u - Ox.apply_B_phys(pb.es, xg, pb.centers[chunk], pb.p)
+
+
+def test_schur_cfg3_full_vector(O):
+    """cfg3 (M=1000, p=25): the whole Schur matvec K v against the oracle over
+    ALL targets (the goldens hold a 24-target slice), oracle M2L spread over
+    the host cores."""
+    import multiprocessing as mp
+    import os as _os
+    from paper_1412_7466_b200 import grating, solver
+    pb = O.load_problem(3)
+    _FULL3["pb"] = pb
+    rng = np.random.default_rng(303)
+    v = pb.smat[None, :] * _cplx(rng, (pb.M, pb.L))
+    xg = pb.es.apply_pinv(O.apply_C(pb.es, v, pb.centers))
+    n = len(_os.sched_getaffinity(0))
+    chunks = [c for c in np.array_split(np.arange(pb.M), 4 * n) if c.size]
+    with mp.get_context("fork").Pool(n) as pool:
+        u = np.concatenate(pool.map(_cfg3_chunk, [(c, v, xg) for c in chunks]), axis=0)
+    ref = v - pb.smat[None, :] * u
+    op = solver.SchurOperator(grating.load_fixture("w10"), pb.centers, pb.p, smat=pb.smat)
+    got = op(_dev(v[None])).cpu().numpy()[0]
+    assert rel(got, ref) <= MATVEC_TOL
+    aT = op.apply_T(_dev(v[None])).cpu().numpy()[0]
+    uT = np.concatenate([O.apply_T(v, pb.centers, pb.es.k2, pb.p, pb.es.bloch, targets=c)
+                         for c in (np.arange(0, 40), np.arange(960, 1000))], axis=0)
+    assert rel(aT[np.r_[0:40, 960:1000]], uT) <= MATVEC_TOL
