@@ -80,7 +80,8 @@ def cpu_oracle_rate(steps: int, warmup: int, per_worker: int = 12):
     ntarget = cores * per_worker
     tids = np.arange(ntarget) % pb.M
     chunks = [tids[i::cores] for i in range(cores)]
-    ctx = mp.get_context("fork")
+    # spawn, not fork: on the GPU arm this runs after CUDA / NCCL threads exist
+    ctx = mp.get_context("spawn")
     times = []
     with ctx.Pool(cores, initializer=_pool_init,
                   initargs=(beta, pb.centers, pb.es.k2, pb.p, pb.es.bloch)) as pool:

@@ -536,8 +536,15 @@ def test_matvec_and_solve_are_bit_reproducible(O, cfg, nrhs):
 _FULL3 = {}
 
 
+def _cfg3_init():
+    from oracle import periscat_oracle as Ox
+    _FULL3["pb"] = Ox.load_problem(3)
+
+
 def _cfg3_chunk(args):
     chunk, v, xg = args
+    if "pb" not in _FULL3:
+        _cfg3_init()
     pb = _FULL3["pb"]
     from oracle import periscat_oracle as Ox
     u = Ox.apply_T(v, pb.centers, pb.es.k2, pb.p, pb.es.bloch, pb.es.period, pb.es.copies,
@@ -559,7 +566,8 @@ def test_schur_cfg3_full_vector(O):
     xg = pb.es.apply_pinv(O.apply_C(pb.es, v, pb.centers))
     n = len(_os.sched_getaffinity(0))
     chunks = [c for c in np.array_split(np.arange(pb.M), 4 * n) if c.size]
-    with mp.get_context("fork").Pool(n) as pool:
+    # spawn, not fork: this process already runs CUDA threads
+    with mp.get_context("spawn").Pool(n, initializer=_cfg3_init) as pool:
         u = np.concatenate(pool.map(_cfg3_chunk, [(c, v, xg) for c in chunks]), axis=0)
     ref = v - pb.smat[None, :] * u
     op = solver.SchurOperator(grating.load_fixture("w10"), pb.centers, pb.p, smat=pb.smat)
