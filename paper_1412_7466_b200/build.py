@@ -50,9 +50,12 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
         fh.write("\n".join(log))
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs,
            "-L/usr/local/cuda/lib64", "-lcusolver", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
-    subprocess.run(cmd, check=True)
-    for o in objs:
-        os.remove(o)
+    try:
+        subprocess.run(cmd, check=True)
+    finally:                       # no stale objects left behind on a failed link
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     if verbose:
         print(f"built {out} in {time.time() - t0:.1f}s")
     return out
