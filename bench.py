@@ -325,7 +325,7 @@ def run_ours(args):
         if world == 1:
             return solver.solve_full(conf, centers, p, radius=radius, device=local)
         opd = solver.SchurOperator(conf, centers, p, radius=radius, device=local,
-                                   target_range=(t0, t1))
+                                   target_range=(t0, t1), split_setup=True)
         sh = parallel.ShardedSchur(opd)
         x, its, hist = parallel.gmres_dist(sh, sh.rhs(), 1e-10, 150, engine=opd.eng)
         xe = sh.recover(x.contiguous())

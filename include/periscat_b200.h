@@ -172,15 +172,37 @@ int ps_recover(ps_ctx* ctx, const void* g_dev, void* x_dev, void* stream);
 
 /* ---- GMRES building blocks (device-resident Arnoldi) --- */
 
-/* h[r][i] = <V_i^r, w^r> for i < k, over this rank's n entries:
- * V [kmax][nrhs][n] (Krylov-index major), w [nrhs][n], h [nrhs][k] (complex). */
-int ps_block_dot(ps_ctx* ctx, int nrhs, int n, int k, int kmax, const void* V_dev,
-                 const void* w_dev, void* h_dev, void* stream);
-/* w^r -= sum_i h[r][i] V_i^r */
-int ps_block_axpy(ps_ctx* ctx, int nrhs, int n, int k, int kmax, const void* V_dev,
-                  const void* h_dev, void* w_dev, void* stream);
-/* nrm2[r] = sum |w^r|^2 (partial over this rank) */
-int ps_norm2(ps_ctx* ctx, int nrhs, int n, const void* w_dev, double* nrm2_dev, void* stream);
+/* Arnoldi pieces for drivers that apply the operator themselves and, on
+ * several ranks, all-reduce the partial results between the calls
+ * (krylov.gmres_device for any device operator, parallel.gmres_dist; they
+ * replace the reference-SPEC GMRES loop SPEC.md:549-557).  The per-RHS
+ * Hessenberg / Givens / residual state stays in the context on the device;
+ * the caller owns the Krylov basis V [maxit+1][nrhs][n] (Krylov-index major)
+ * and the vectors.  Only ps_krylov_begin synchronises (NaN/Inf RHS check).
+ *   begin : state from the (all-reduced) squared RHS norms, V_0 = b / ||b||
+ *   dot   : h [nrhs][k] = <V_i^r, w^r>, i < k, this rank's n entries (frozen
+ *           RHS give 0)
+ *   axpy  : w^r -= sum_i h[r][i] V_i^r (active RHS)
+ *   norm2 : nrm2 [nrhs] = sum |w^r|^2 over this rank's entries
+ *   step  : column k = h1 + h2 (the two CGS2 passes, [nrhs][k+1] each) and
+ *           ||w||^2 -> Givens update, V_{k+1} = w / ||w||; status [nrhs+1]
+ *           (device) = relative residual per RHS, then a NaN/Inf flag
+ *   freeze: active_host [nrhs] (0 = converged RHS, no further updates)
+ *   solve : x = sum_i y_i V_i with R y = g, iters_host [nrhs] columns each */
+int ps_krylov_begin(ps_ctx* ctx, int nrhs, long long n, int maxit, const void* b_dev,
+                    const double* bnorm2_dev, void* V_dev, void* stream);
+int ps_krylov_dot(ps_ctx* ctx, int k, const void* V_dev, const void* w_dev, void* h_dev,
+                  void* stream);
+int ps_krylov_axpy(ps_ctx* ctx, int k, const void* V_dev, const void* h_dev, void* w_dev,
+                   void* stream);
+int ps_krylov_norm2(ps_ctx* ctx, int nrhs, long long n, const void* w_dev, double* nrm2_dev,
+                    void* stream);
+int ps_krylov_step(ps_ctx* ctx, int k, const void* h1_dev, const void* h2_dev,
+                   const double* wnorm2_dev, const void* w_dev, void* V_dev, double* status_dev,
+                   void* stream);
+int ps_krylov_freeze(ps_ctx* ctx, const int* active_host, void* stream);
+int ps_krylov_solve(ps_ctx* ctx, const int* iters_host, const void* V_dev, void* x_dev,
+                    void* stream);
 
 /* Whole unrestarted GMRES on one device (single rank): zero initial guess,
  * CGS2 Arnoldi, Givens least squares on the device; stops per RHS at

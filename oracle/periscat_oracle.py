@@ -382,16 +382,21 @@ class Problem:
         return 2 * self.p + 1
 
 
-def apply_schur_operator(pb: Problem, v, with_coupling: bool = True) -> np.ndarray:
+def apply_schur_operator(pb: Problem, v, with_coupling: bool = True, targets=None) -> np.ndarray:
     """K v = v - S T v - S B A^+ C v  (paper B = -B_phys).
-    SPEC.md:539-547; PAPER.md final preconditioned system."""
+    SPEC.md:539-547; PAPER.md final preconditioned system.  ``targets``
+    restricts the output rows to those inclusions (C v still sums over all
+    sources; T and B are per target)."""
     v = np.asarray(v, dtype=complex).reshape(pb.M, pb.L)
     es = pb.es
-    u = apply_T(v, pb.centers, es.k2, pb.p, es.bloch, es.period, es.copies)
+    tidx = np.arange(pb.M) if targets is None else np.arange(pb.M)[targets]
+    u = apply_T(v, pb.centers, es.k2, pb.p, es.bloch, es.period, es.copies, targets=tidx)
     if with_coupling:
         x = es.apply_pinv(apply_C(es, v, pb.centers))
-        u = u - apply_B_phys(es, x, pb.centers, pb.p)
-    return (v - pb.apply_S(u)).reshape(-1)
+        u = u - apply_B_phys(es, x, pb.centers[tidx], pb.p)
+    sub = pb if targets is None else Problem(es, pb.centers[tidx], pb.p, pb.radius, pb.smat,
+                                             None if pb.rot is None else pb.rot[tidx])
+    return (v[tidx] - sub.apply_S(u)).reshape(-1)
 
 
 def schur_rhs(pb: Problem) -> np.ndarray:

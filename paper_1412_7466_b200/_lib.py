@@ -37,9 +37,13 @@ SIGNATURES = {
     "ps_apply_schur": (_I, [_P, _P, _P, _P]),
     "ps_schur_rhs": (_I, [_P, _P, _P]),
     "ps_recover": (_I, [_P, _P, _P, _P]),
-    "ps_block_dot": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P]),
-    "ps_block_axpy": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P]),
-    "ps_norm2": (_I, [_P, _I, _I, _P, _P, _P]),
+    "ps_krylov_begin": (_I, [_P, _I, ctypes.c_longlong, _I, _P, _P, _P, _P]),
+    "ps_krylov_dot": (_I, [_P, _I, _P, _P, _P, _P]),
+    "ps_krylov_axpy": (_I, [_P, _I, _P, _P, _P, _P]),
+    "ps_krylov_norm2": (_I, [_P, _I, ctypes.c_longlong, _P, _P, _P]),
+    "ps_krylov_step": (_I, [_P, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "ps_krylov_freeze": (_I, [_P, _IP, _P]),
+    "ps_krylov_solve": (_I, [_P, _IP, _P, _P, _P]),
     "ps_gmres": (_I, [_P, _P, _P, _D, _I, _IP, _DP, _P]),
     "ps_dfma_peak": (_I, [_I, _DP, _DP]),
     "ps_dfma_sustained": (_I, [_I, _D, _DP]),

@@ -166,13 +166,22 @@ int ps_set_rhs_bloch(ps_ctx* h, int nrhs, const double* bloch) {
     return PS_ERR_ARG;
   }
   if (int rc = set_device(c)) return rc;
-  if ((int)c->rhs.size() > nrhs) {
-    for (size_t r = nrhs; r < c->rhs.size(); ++r) {
-      auto& d = c->rhs[r];
+  if ((int)c->rhs.size() != nrhs) {
+    // a different RHS count invalidates every per-RHS factor set (and the
+    // per-RHS layer-field data): the coupled entry points then report
+    // PS_ERR_STATE until the factors are installed again (ps_set_pinv /
+    // ps_setup_empty), instead of reading null factors of the new RHS
+    for (auto& d : c->rhs) {
       void* rp[] = {d.d_Uh, d.d_sinv, d.d_Vb, d.d_cscale, d.d_f};
       for (void* q : rp)
         if (q) ps::dev_free(q);
+      d = ps::RhsData{};
     }
+    c->nsv = 0;
+    c->nfield = 0;
+    if (c->d_inc) ps::dev_free(c->d_inc);
+    c->d_inc = nullptr;
+    c->have_field = 0;
   }
   c->rhs.resize(nrhs);
   c->nrhs = nrhs;
@@ -489,7 +498,7 @@ int ps_apply_schur(ps_ctx* h, const void* v, void* y, void* stream) {
 int ps_schur_rhs(ps_ctx* h, void* rhs, void* stream) {
   if (!h) return PS_ERR_ARG;
   Ctx* c = C(h);
-  if (c->p < 0 || !c->d_S || !c->have_layers || !c->rhs[0].d_Uh) {
+  if (c->p < 0 || !c->d_S || !ps::factors_ready(c)) {
     c->err = "ps_schur_rhs: geometry / S / layers / pinv not set";
     return PS_ERR_STATE;
   }
@@ -504,7 +513,7 @@ int ps_schur_rhs(ps_ctx* h, void* rhs, void* stream) {
 int ps_recover(ps_ctx* h, const void* g, void* x, void* stream) {
   if (!h) return PS_ERR_ARG;
   Ctx* c = C(h);
-  if (!c->have_layers || !c->rhs[0].d_Uh) {
+  if (!ps::factors_ready(c)) {
     c->err = "ps_recover: layers / pinv not set";
     return PS_ERR_STATE;
   }
@@ -517,50 +526,99 @@ int ps_recover(ps_ctx* h, const void* g, void* x, void* stream) {
                      reinterpret_cast<cudaStream_t>(stream));
 }
 
-int ps_block_dot(ps_ctx* h, int nrhs, int n, int k, int kmax, const void* V, const void* w,
-                 void* hout, void* stream) {
+int ps_krylov_begin(ps_ctx* h, int nrhs, long long n, int maxit, const void* b,
+                    const double* bnorm2, void* V, void* stream) {
   if (!h) return PS_ERR_ARG;
   Ctx* c = C(h);
-  if (nrhs < 1 || n < 0 || k < 0 || k > kmax || !V || !w || !hout) {
-    c->err = "ps_block_dot: bad argument";
+  if (nrhs < 1 || n < 1 || maxit < 1 || !b || !bnorm2 || !V) {
+    c->err = "ps_krylov_begin: bad argument";
     return PS_ERR_ARG;
   }
   if (int rc = set_device(c)) return rc;
-  return ps::block_dot(c, nrhs, n, k, kmax, reinterpret_cast<const double2*>(V),
-                       reinterpret_cast<const double2*>(w), reinterpret_cast<double2*>(hout),
-                       reinterpret_cast<cudaStream_t>(stream));
+  return ps::krylov_begin(c, nrhs, n, maxit, reinterpret_cast<const double2*>(b), bnorm2,
+                          reinterpret_cast<double2*>(V), reinterpret_cast<cudaStream_t>(stream));
 }
 
-int ps_block_axpy(ps_ctx* h, int nrhs, int n, int k, int kmax, const void* V, const void* hin,
-                  void* w, void* stream) {
+int ps_krylov_dot(ps_ctx* h, int k, const void* V, const void* w, void* hout, void* stream) {
   if (!h) return PS_ERR_ARG;
   Ctx* c = C(h);
-  if (nrhs < 1 || n < 0 || k < 0 || k > kmax || !V || !w || !hin) {
-    c->err = "ps_block_axpy: bad argument";
+  if (!V || !w || !hout) {
+    c->err = "ps_krylov_dot: null pointer";
     return PS_ERR_ARG;
   }
   if (int rc = set_device(c)) return rc;
-  return ps::block_axpy(c, nrhs, n, k, kmax, reinterpret_cast<const double2*>(V),
-                        reinterpret_cast<const double2*>(hin), reinterpret_cast<double2*>(w),
+  return ps::krylov_dot(c, k, reinterpret_cast<const double2*>(V),
+                        reinterpret_cast<const double2*>(w), reinterpret_cast<double2*>(hout),
                         reinterpret_cast<cudaStream_t>(stream));
 }
 
-int ps_norm2(ps_ctx* h, int nrhs, int n, const void* w, double* nrm2, void* stream) {
+int ps_krylov_axpy(ps_ctx* h, int k, const void* V, const void* hin, void* w, void* stream) {
   if (!h) return PS_ERR_ARG;
   Ctx* c = C(h);
-  if (nrhs < 1 || n < 0 || !w || !nrm2) {
-    c->err = "ps_norm2: bad argument";
+  if (!V || !w || !hin) {
+    c->err = "ps_krylov_axpy: null pointer";
     return PS_ERR_ARG;
   }
   if (int rc = set_device(c)) return rc;
-  return ps::norm2(c, nrhs, n, reinterpret_cast<const double2*>(w), nrm2,
-                   reinterpret_cast<cudaStream_t>(stream));
+  return ps::krylov_axpy(c, k, reinterpret_cast<const double2*>(V),
+                         reinterpret_cast<const double2*>(hin), reinterpret_cast<double2*>(w),
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_krylov_norm2(ps_ctx* h, int nrhs, long long n, const void* w, double* nrm2, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (nrhs < 1 || n < 1 || !w || !nrm2) {
+    c->err = "ps_krylov_norm2: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::krylov_norm2(c, nrhs, n, reinterpret_cast<const double2*>(w), nrm2,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_krylov_step(ps_ctx* h, int k, const void* h1, const void* h2, const double* wnorm2,
+                   const void* w, void* V, double* status, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (!h1 || !h2 || !wnorm2 || !w || !V || !status) {
+    c->err = "ps_krylov_step: null pointer";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::krylov_step(c, k, reinterpret_cast<const double2*>(h1),
+                         reinterpret_cast<const double2*>(h2), wnorm2,
+                         reinterpret_cast<const double2*>(w), reinterpret_cast<double2*>(V), status,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_krylov_freeze(ps_ctx* h, const int* active_host, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (!active_host) {
+    c->err = "ps_krylov_freeze: null pointer";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::krylov_freeze(c, active_host, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_krylov_solve(ps_ctx* h, const int* iters_host, const void* V, void* x, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (!iters_host || !V || !x) {
+    c->err = "ps_krylov_solve: null pointer";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::krylov_solve(c, iters_host, reinterpret_cast<const double2*>(V),
+                          reinterpret_cast<double2*>(x), reinterpret_cast<cudaStream_t>(stream));
 }
 
 int ps_precompute_coupling(ps_ctx* h, double max_gb) {
   if (!h) return PS_ERR_ARG;
   Ctx* c = C(h);
-  if (c->p < 0 || !c->have_layers || !c->rhs[0].d_Uh) {
+  if (c->p < 0 || !ps::factors_ready(c)) {
     c->err = "ps_precompute_coupling: geometry / layers / pinv not set";
     return PS_ERR_STATE;
   }

@@ -22,6 +22,7 @@
 // symbol orders of the same row.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <string>
 
 #include "coupling.cuh"
@@ -553,17 +554,24 @@ int dispatch_b(Ctx* c, const double2* x, const double2* bpow, double2* bpart, do
 }
 
 // workspace layout per RHS:
-//   g [nrc] | h [nsv] | x [nout] | bsub [Mt*L] | u [Mt*L] | gpart [512*nrc] | bpart [nchunk*Mt*L]
+//   g [nrc] | h [nsv] | x [nout] | bsub [Mt*L] | u [Mt*L] | gpart [gpart_elems] | bpart [nchunk*Mt*L]
 struct Work {
   double2 *g, *h, *x, *bsub, *u, *gpart, *bpart;
 };
+
+// gpart holds the split partial sums of C beta: at most 512 splits in the
+// matrix-free K3 (c_splits) and at most 4*sm_count+1 ct_gemv blocks in the
+// dense path (dense_apply_C); size for whichever is larger.
+size_t gpart_elems(const Ctx* c) {
+  return std::max((size_t)512 * c->nrow_c, dense_gpart_elems(c));
+}
 
 size_t work_stride(const Ctx* c) {
   const size_t nrc = c->nrow_c, nsv = c->nsv > 0 ? c->nsv : 1;
   const size_t nout = c->ncol_b + 2 * c->nrb + c->nfield;
   const size_t mtl = (size_t)(c->t_end - c->t_begin) * c->L;
   const size_t nch = c->have_layers ? (size_t)b_chunks(c) : 0;
-  return nrc + nsv + nout + 2 * mtl + 512 * nrc + nch * mtl + 8;
+  return nrc + nsv + nout + 2 * mtl + gpart_elems(c) + nch * mtl + 8;
 }
 
 int work(Ctx* c, int r, Work* w) {
@@ -586,7 +594,7 @@ int work(Ctx* c, int r, Work* w) {
   w->bsub = w->x + nout;
   w->u = w->bsub + mtl;
   w->gpart = w->u + mtl;
-  w->bpart = w->gpart + 512 * nrc;
+  w->bpart = w->gpart + gpart_elems(c);
   return PS_OK;
 }
 
@@ -663,7 +671,7 @@ static int schur_mrhs(Ctx* c, const double2* v, double2* y, bool coupled, cudaSt
 int apply_schur_g(Ctx* c, const double2* v, const double2* g, double2* y, cudaStream_t st) {
   const size_t in_stride = (size_t)c->M * c->L;
   const size_t out_stride = (size_t)(c->t_end - c->t_begin) * c->L;
-  const bool coupled = c->have_layers && c->rhs[0].d_Uh && g;
+  const bool coupled = ps::factors_ready(c) && g;
   if (c->nrhs > 1) {
     if (coupled)
       for (int r = 0; r < c->nrhs; ++r) {
@@ -720,7 +728,7 @@ __global__ void sub_rows(const double2* __restrict__ a, const double2* __restric
 // reduce-scattered): y = v_own - S (a_own - B A^+ g), one RHS.
 int schur_finish(Ctx* c, const double2* v_own, const double2* a_own, const double2* g,
                  double2* y, cudaStream_t st) {
-  const bool coupled = c->have_layers && c->rhs[0].d_Uh && g;
+  const bool coupled = ps::factors_ready(c) && g;
   Work w;
   if (int rc = work(c, 0, &w)) return rc;
   const double2* bsub = nullptr;
@@ -771,7 +779,7 @@ static int schur_overlapped(Ctx* c, const double2* v, double2* y, cudaStream_t s
 }
 
 int apply_schur(Ctx* c, const double2* v, double2* y, cudaStream_t st) {
-  const bool coupled = c->have_layers && c->rhs[0].d_Uh;
+  const bool coupled = ps::factors_ready(c);
   if (!coupled) return apply_schur_g(c, v, nullptr, y, st);
   if (c->overlap_sms >= 0 && c->overlap_sms < c->sm_count && c->nrhs == 1 && c->s_diag &&
       c->dense && c->dcs0 == 0 && c->dcs1 == c->M && m2l_sym_selected(c))

@@ -16,6 +16,7 @@ struct Dev2 {  // tiny RAII-free device buffer record (freed in ps_destroy)
 };
 
 struct EmptyState;   // device empty-grating setup (empty.cu)
+struct Krylov;       // device Arnoldi / Givens state (gmres.cu)
 
 struct RhsData {          // per right-hand side (incidence angle)
   double2 bloch{1.0, 0.0};
@@ -90,6 +91,7 @@ struct Ctx {
 
   // device empty-grating assembly + SVD (ps_setup_empty, empty.cu)
   EmptyState* empty = nullptr;
+  Krylov* krylov = nullptr;        // GMRES state + scratch (gmres.cu)
   int svd_workers = 4;             // concurrent cuSOLVER streams for multi-RHS setup
 
   std::vector<void*> owned;        // everything cudaMalloc'ed
@@ -104,6 +106,15 @@ struct Ctx {
 };
 
 inline Ctx* C(ps_ctx* h) { return reinterpret_cast<Ctx*>(h); }
+
+// the coupled (layer) entry points need the A^+ factors of EVERY right-hand
+// side; ps_set_rhs_bloch drops them all when the RHS count changes
+inline bool factors_ready(const Ctx* c) {
+  if (!c->have_layers || c->nsv <= 0 || c->rhs.empty()) return false;
+  for (const auto& r : c->rhs)
+    if (!r.d_Uh || !r.d_sinv || !r.d_Vb || !r.d_cscale || !r.d_f) return false;
+  return true;
+}
 
 // cudaFuncSetAttribute is per device: a launcher keeps one bit per device it
 // has configured (a repeated call from racing threads is harmless)

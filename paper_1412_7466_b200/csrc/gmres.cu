@@ -10,6 +10,7 @@
 // [nrhs][n] block the Schur operator consumes directly).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -263,62 +264,110 @@ __global__ void cadd_rows(double2* __restrict__ a, const double2* __restrict__ b
 
 int nchunks(long long n) { return (int)((n + kChunk - 1) / kChunk); }
 
-struct Scratch {
-  void* p = nullptr;
-  size_t bytes = 0;
-};
+// hcol[r][i] = h1[r][i] + h2[r][i]  (i <= k; h1/h2 packed [nrhs][k+1], hcol ld)
+__global__ void combine_cols(const double2* __restrict__ h1, const double2* __restrict__ h2,
+                             int nrhs, int kp1, double2* __restrict__ hcol, int ld) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nrhs * kp1) return;
+  const int r = idx / kp1, i = idx % kp1;
+  const double2 a = h1[idx], b = h2[idx];
+  hcol[(long long)r * ld + i] = make_double2(a.x + b.x, a.y + b.y);
+}
+
+// status[r] = relative residual of RHS r, status[nrhs] = non-finite flag
+__global__ void write_status(const double* __restrict__ res, const int* __restrict__ nonfinite,
+                             int nrhs, double* __restrict__ status) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < nrhs) status[r] = res[r];
+  if (r == nrhs) status[r] = nonfinite[0] ? 1.0 : 0.0;
+}
 
 }  // namespace
 
-// persistent scratch per context (released by gmres_release)
-static std::vector<std::pair<Ctx*, Scratch>> g_scratch;
+// Device state of one Arnoldi process batch (per context): the Hessenberg
+// columns, Givens rotations and residual vector of every RHS, the CGS2
+// coefficient scratch and the chunked dot-product partials.  Owned by the
+// context (no process-global state), grown on demand, freed by gmres_release.
+struct Krylov {
+  void* base = nullptr;
+  size_t bytes = 0;
+  int nrhs = 0, maxit = 0;
+  long long n = 0;
+  GState s{};
+  double2* hcol = nullptr;   // [nrhs][maxit+1]
+  double2* y = nullptr;      // [nrhs][maxit+1]
+  double2* part = nullptr;   // [nrhs][maxit+1][nchunks]
+  double* nrm2 = nullptr;    // [nrhs]
+  int* kk = nullptr;         // [nrhs]
+  int* flags = nullptr;      // [nrhs]
+};
 
-static int scratch(Ctx* c, size_t bytes, void** out) {
-  for (auto& e : g_scratch)
-    if (e.first == c) {
-      if (e.second.bytes < bytes) {
-        ps::dev_free(e.second.p);
-        e.second.p = nullptr;
-        e.second.bytes = 0;
-        PS_CUDA_TRY(c, ps::dev_malloc(&e.second.p, bytes));
-        e.second.bytes = bytes;
-      }
-      *out = e.second.p;
-      return PS_OK;
-    }
-  Scratch s;
-  PS_CUDA_TRY(c, ps::dev_malloc(&s.p, bytes));
-  s.bytes = bytes;
-  g_scratch.push_back({c, s});
-  *out = s.p;
+namespace {
+
+// Sizes the Krylov state for (nrhs, n, maxit) plus `extra` bytes of caller
+// scratch at the front (the single-rank driver's basis V and w); reuses the
+// previous allocation when it is large enough.
+int krylov_state(Ctx* c, int nrhs, long long n, int maxit, size_t extra, Krylov** out,
+                 void** extra_out) {
+  if (!c->krylov) c->krylov = new Krylov();
+  Krylov* K = c->krylov;
+  const int nc = nchunks(n);
+  const size_t szH = (size_t)nrhs * maxit * (maxit + 1);
+  const size_t szCS = (size_t)nrhs * maxit;
+  const size_t szG = (size_t)nrhs * (maxit + 1);
+  const size_t szPart = (size_t)nrhs * (maxit + 1) * nc;
+  const size_t pre = (extra + 255) / 256 * 256;
+  const size_t elems = szH + 2 * szCS + 3 * szG + szPart;
+  const size_t need = pre + elems * sizeof(double2) + (4 * (size_t)nrhs + 8) * sizeof(double) +
+                      (5 * (size_t)nrhs + 8) * sizeof(int) + 256;
+  if (K->bytes < need) {
+    if (K->base) ps::dev_free(K->base);
+    K->base = nullptr;
+    K->bytes = 0;
+    PS_CUDA_TRY(c, ps::dev_malloc(&K->base, need));
+    K->bytes = need;
+  }
+  K->nrhs = nrhs;
+  K->n = n;
+  K->maxit = maxit;
+  char* b = (char*)K->base;
+  if (extra_out) *extra_out = b;
+  double2* p = (double2*)(b + pre);
+  K->s.H = p; p += szH;
+  K->s.cs = p; p += szCS;
+  K->s.sn = p; p += szCS;
+  K->s.g = p; p += szG;
+  K->hcol = p; p += szG;
+  K->y = p; p += szG;
+  K->part = p; p += szPart;
+  double* d = (double*)p;
+  K->s.bnorm = d; d += nrhs;
+  K->s.res = d; d += nrhs;
+  K->nrm2 = d; d += 2 * nrhs;
+  int* q = (int*)d;
+  K->s.active = q; q += nrhs;
+  K->kk = q; q += nrhs;
+  K->flags = q; q += nrhs;
+  K->s.nonfinite = q;                   // [1 + nrhs]
+  *out = K;
   return PS_OK;
 }
 
-void gmres_release(Ctx* c) {
-  for (size_t i = 0; i < g_scratch.size(); ++i)
-    if (g_scratch[i].first == c) {
-      ps::dev_free(g_scratch[i].second.p);
-      g_scratch.erase(g_scratch.begin() + i);
-      return;
-    }
-}
-
-static int dot_impl(Ctx* c, int nrhs, long long n, int k, const double2* V, const double2* w,
-                    double2* h, int ldh, int accumulate, const int* active, double2* part,
-                    cudaStream_t st) {
+int dot_impl(Ctx* c, int nrhs, long long n, int k, const double2* V, const double2* w,
+             double2* h, int ldh, const int* active, double2* part, cudaStream_t st) {
   if (k == 0) return PS_OK;
   const int nc = nchunks(n);
   dim3 grid(nc, k, nrhs);
   c->launches += 2;
   dot_partial<<<grid, kDotThreads, 0, st>>>(V, w, nrhs, n, k, nc, active, part);
   PS_CUDA_TRY(c, cudaGetLastError());
-  dot_final<<<(nrhs * k + 127) / 128, 128, 0, st>>>(part, nrhs, k, nc, h, ldh, accumulate);
+  dot_final<<<(nrhs * k + 127) / 128, 128, 0, st>>>(part, nrhs, k, nc, h, ldh, 0);
   PS_CUDA_TRY(c, cudaGetLastError());
   return PS_OK;
 }
 
-static int axpy_impl(Ctx* c, int nrhs, long long n, int k, const double2* V, const double2* h,
-                     int ldh, double sgn, const int* active, double2* w, cudaStream_t st) {
+int axpy_impl(Ctx* c, int nrhs, long long n, int k, const double2* V, const double2* h, int ldh,
+              double sgn, const int* active, double2* w, cudaStream_t st) {
   if (k == 0) return PS_OK;
   int bx = (int)((n + 255) / 256);
   if (bx > 4 * c->sm_count) bx = 4 * c->sm_count;
@@ -329,8 +378,8 @@ static int axpy_impl(Ctx* c, int nrhs, long long n, int k, const double2* V, con
   return PS_OK;
 }
 
-static int norm_impl(Ctx* c, int nrhs, long long n, const double2* w, double* out,
-                     double2* part, cudaStream_t st) {
+int norm_impl(Ctx* c, int nrhs, long long n, const double2* w, double* out, double2* part,
+              cudaStream_t st) {
   const int nc = nchunks(n);
   c->launches += 2;
   norm2_partial<<<dim3(nc, nrhs), kDotThreads, 0, st>>>(w, n, nc, part);
@@ -340,27 +389,168 @@ static int norm_impl(Ctx* c, int nrhs, long long n, const double2* w, double* ou
   return PS_OK;
 }
 
-int block_dot(Ctx* c, int nrhs, int n, int k, int kmax, const double2* V, const double2* w,
-              double2* h, cudaStream_t st) {
-  (void)kmax;
-  void* sp;
-  if (int rc = scratch(c, (size_t)nrhs * (k + 1) * nchunks(n) * sizeof(double2) + 64, &sp))
+int grid_x(const Ctx* c, long long n) {
+  return (int)std::min<long long>(std::max<long long>((n + 255) / 256, 1), 4LL * c->sm_count);
+}
+
+// state init from the (global) squared RHS norms, V_0 = b / ||b||
+int begin_impl(Ctx* c, Krylov* K, const double2* b, const double* b2, double2* V, cudaStream_t st) {
+  const int nrhs = K->nrhs;
+  PS_CUDA_TRY(c, cudaMemsetAsync(K->s.nonfinite, 0, (1 + nrhs) * sizeof(int), st));
+  c->launches += 2;
+  init_state<<<(nrhs + 127) / 128, 128, 0, st>>>(K->s, nrhs, K->maxit, b2);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  scale_into<<<dim3(grid_x(c, K->n), nrhs), 256, 0, st>>>(b, b2, K->n, nullptr, V);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  return PS_OK;
+}
+
+// Givens update of column k from the CGS2 coefficients (hcol, ld maxit+1) and
+// the squared norm of the orthogonalised w; V_{k+1} = w / ||w||
+int step_impl(Ctx* c, Krylov* K, int k, const double* wn2, const double2* w, double2* V,
+              cudaStream_t st) {
+  const int nrhs = K->nrhs;
+  c->launches += 2;
+  givens_step<<<(nrhs + 127) / 128, 128, 0, st>>>(K->s, nrhs, k, K->maxit, K->hcol, K->maxit + 1,
+                                                  wn2);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  scale_into<<<dim3(grid_x(c, K->n), nrhs), 256, 0, st>>>(
+      w, wn2, K->n, K->s.active, V + (size_t)(k + 1) * nrhs * K->n);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  return PS_OK;
+}
+
+int freeze_impl(Ctx* c, Krylov* K, const int* active_host, cudaStream_t st) {
+  PS_CUDA_TRY(c, cudaMemcpyAsync(K->flags, active_host, K->nrhs * sizeof(int),
+                                 cudaMemcpyHostToDevice, st));
+  c->launches += 1;
+  set_flags<<<(K->nrhs + 127) / 128, 128, 0, st>>>(K->s.active, K->flags, K->nrhs);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  return PS_OK;
+}
+
+// x = sum_i y_i V_i with R y = g per RHS (kk_host[r] columns)
+int solve_impl(Ctx* c, Krylov* K, const int* kk_host, const double2* V, double2* x,
+               cudaStream_t st) {
+  const int nrhs = K->nrhs;
+  PS_CUDA_TRY(c, cudaMemcpyAsync(K->kk, kk_host, nrhs * sizeof(int), cudaMemcpyHostToDevice, st));
+  c->launches += 1;
+  back_solve<<<(nrhs + 127) / 128, 128, 0, st>>>(K->s, nrhs, K->kk, K->maxit, K->y, K->maxit + 1);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  PS_CUDA_TRY(c, cudaMemsetAsync(x, 0, (size_t)nrhs * K->n * sizeof(double2), st));
+  int kmax = 0;
+  for (int r = 0; r < nrhs; ++r) kmax = std::max(kmax, kk_host[r]);
+  return axpy_impl(c, nrhs, K->n, kmax, V, K->y, K->maxit + 1, 1.0, nullptr, x, st);
+}
+
+int need_state(Ctx* c, const char* fn) {
+  if (!c->krylov || !c->krylov->base || c->krylov->nrhs < 1) {
+    c->err = std::string(fn) + ": call ps_krylov_begin first";
+    return PS_ERR_STATE;
+  }
+  return PS_OK;
+}
+
+}  // namespace
+
+void gmres_release(Ctx* c) {
+  if (!c->krylov) return;
+  if (c->krylov->base) ps::dev_free(c->krylov->base);
+  delete c->krylov;
+  c->krylov = nullptr;
+}
+
+// ---------------------------------------------------------------- building
+// blocks for drivers that apply the operator (and reduce over ranks)
+// themselves: krylov.gmres_device (any device operator) and the multi-rank
+// parallel.gmres_dist.  h tensors are packed [nrhs][k].
+int krylov_begin(Ctx* c, int nrhs, long long n, int maxit, const double2* b, const double* b2,
+                 double2* V, cudaStream_t st) {
+  Krylov* K;
+  if (int rc = krylov_state(c, nrhs, n, maxit, 0, &K, nullptr)) return rc;
+  if (int rc = begin_impl(c, K, b, b2, V, st)) return rc;
+  std::vector<int> bad(nrhs + 1, 0);
+  PS_CUDA_TRY(c, cudaMemcpyAsync(bad.data(), K->s.nonfinite, (nrhs + 1) * sizeof(int),
+                                 cudaMemcpyDeviceToHost, st));
+  PS_CUDA_TRY(c, cudaStreamSynchronize(st));
+  for (int r = 0; r < nrhs; ++r)
+    if (bad[1 + r]) {
+      c->err = "ps_krylov_begin: NaN/Inf in the right-hand side " + std::to_string(r) +
+               " (SPEC.md:553)";
+      return PS_ERR_NUMERICAL;
+    }
+  return PS_OK;
+}
+
+int krylov_dot(Ctx* c, int k, const double2* V, const double2* w, double2* h, cudaStream_t st) {
+  if (int rc = need_state(c, "ps_krylov_dot")) return rc;
+  Krylov* K = c->krylov;
+  if (k < 1 || k > K->maxit + 1) {
+    c->err = "ps_krylov_dot: k out of range";
+    return PS_ERR_ARG;
+  }
+  return dot_impl(c, K->nrhs, K->n, k, V, w, h, k, K->s.active, K->part, st);
+}
+
+int krylov_axpy(Ctx* c, int k, const double2* V, const double2* h, double2* w, cudaStream_t st) {
+  if (int rc = need_state(c, "ps_krylov_axpy")) return rc;
+  Krylov* K = c->krylov;
+  if (k < 1 || k > K->maxit + 1) {
+    c->err = "ps_krylov_axpy: k out of range";
+    return PS_ERR_ARG;
+  }
+  return axpy_impl(c, K->nrhs, K->n, k, V, h, k, -1.0, K->s.active, w, st);
+}
+
+int krylov_norm2(Ctx* c, int nrhs, long long n, const double2* w, double* out, cudaStream_t st) {
+  // usable before ps_krylov_begin (the RHS norm): own partial scratch
+  Krylov* K;
+  const bool have = c->krylov && c->krylov->base && c->krylov->nrhs == nrhs && c->krylov->n == n;
+  if (have) {
+    K = c->krylov;
+  } else if (int rc = krylov_state(c, nrhs, n, 1, 0, &K, nullptr)) {
     return rc;
-  return dot_impl(c, nrhs, n, k, V, w, h, k, 0, nullptr, (double2*)sp, st);
+  }
+  return norm_impl(c, nrhs, n, w, out, K->part, st);
 }
 
-int block_axpy(Ctx* c, int nrhs, int n, int k, int kmax, const double2* V, const double2* h,
-               double2* w, cudaStream_t st) {
-  (void)kmax;
-  return axpy_impl(c, nrhs, n, k, V, h, k, -1.0, nullptr, w, st);
+int krylov_step(Ctx* c, int k, const double2* h1, const double2* h2, const double* wn2,
+                const double2* w, double2* V, double* status, cudaStream_t st) {
+  if (int rc = need_state(c, "ps_krylov_step")) return rc;
+  Krylov* K = c->krylov;
+  if (k < 0 || k >= K->maxit) {
+    c->err = "ps_krylov_step: k out of range";
+    return PS_ERR_ARG;
+  }
+  const int nrhs = K->nrhs;
+  c->launches += 2;
+  combine_cols<<<(nrhs * (k + 1) + 127) / 128, 128, 0, st>>>(h1, h2, nrhs, k + 1, K->hcol,
+                                                             K->maxit + 1);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  if (int rc = step_impl(c, K, k, wn2, w, V, st)) return rc;
+  write_status<<<(nrhs + 1 + 127) / 128, 128, 0, st>>>(K->s.res, K->s.nonfinite, nrhs, status);
+  PS_CUDA_TRY(c, cudaGetLastError());
+  return PS_OK;
 }
 
-int norm2(Ctx* c, int nrhs, int n, const double2* w, double* out, cudaStream_t st) {
-  void* sp;
-  if (int rc = scratch(c, (size_t)nrhs * nchunks(n) * sizeof(double2) + 64, &sp)) return rc;
-  return norm_impl(c, nrhs, n, w, out, (double2*)sp, st);
+int krylov_freeze(Ctx* c, const int* active_host, cudaStream_t st) {
+  if (int rc = need_state(c, "ps_krylov_freeze")) return rc;
+  return freeze_impl(c, c->krylov, active_host, st);
 }
 
+int krylov_solve(Ctx* c, const int* iters_host, const double2* V, double2* x, cudaStream_t st) {
+  if (int rc = need_state(c, "ps_krylov_solve")) return rc;
+  Krylov* K = c->krylov;
+  for (int r = 0; r < K->nrhs; ++r)
+    if (iters_host[r] < 0 || iters_host[r] > K->maxit) {
+      c->err = "ps_krylov_solve: iteration count out of range";
+      return PS_ERR_ARG;
+    }
+  return solve_impl(c, K, iters_host, V, x, st);
+}
+
+// ---------------------------------------------------------------- whole
+// single-rank GMRES with the Schur operator of the context
 int gmres(Ctx* c, const double2* rhs, double2* x, double tol, int maxit, int* iters,
           double* hist, cudaStream_t st) {
   if (c->t_begin != 0 || c->t_end != c->M) {
@@ -369,51 +559,23 @@ int gmres(Ctx* c, const double2* rhs, double2* x, double tol, int maxit, int* it
   }
   const int nrhs = c->nrhs;
   const long long n = (long long)c->M * c->L;
-  const int nc = nchunks(n);
-  // device memory: V, w, H, cs, sn, g, hcol, part, small vectors
   const size_t szV = (size_t)(maxit + 1) * nrhs * n;
-  const size_t szH = (size_t)nrhs * maxit * (maxit + 1);
-  const size_t szCS = (size_t)nrhs * maxit;
-  const size_t szG = (size_t)nrhs * (maxit + 1);
-  const size_t szHc = (size_t)nrhs * (maxit + 1);
-  const size_t szPart = (size_t)nrhs * (maxit + 1) * nc;
   const size_t n2 = (size_t)nrhs * n;
-  const size_t total2 = szV + n2 + szH + 2 * szCS + szG + 2 * szHc + szPart + 8 * nrhs + 128;
-  void* base;
-  if (int rc = scratch(c, total2 * sizeof(double2), &base)) return rc;
-  double2* p = (double2*)base;
-  double2* V = p; p += szV;
-  double2* w = p; p += n2;
-  GState s;
-  s.H = p; p += szH;
-  s.cs = p; p += szCS;
-  s.sn = p; p += szCS;
-  s.g = p; p += szG;
-  double2* hcol = p; p += szHc;
-  double2* y = p; p += szHc;
-  double2* part = p; p += szPart;
-  double* dsmall = (double*)p;
-  s.bnorm = dsmall;
-  s.res = dsmall + nrhs;
-  double* nrm2 = dsmall + 2 * nrhs;
-  s.active = (int*)(dsmall + 3 * nrhs);
-  int* kk_dev = s.active + nrhs;
-  int* flags_dev = kk_dev + nrhs;
-  s.nonfinite = flags_dev + nrhs;          // [1 + nrhs]
-  PS_CUDA_TRY(c, cudaMemsetAsync(s.nonfinite, 0, (1 + nrhs) * sizeof(int), st));
+  Krylov* K;
+  void* front;
+  if (int rc = krylov_state(c, nrhs, n, maxit, (szV + n2) * sizeof(double2), &K, &front)) return rc;
+  double2* V = (double2*)front;
+  double2* w = V + szV;
+  double* nrm2 = K->nrm2;
 
-  // init: V_0 = b / ||b||
-  if (int rc = norm_impl(c, nrhs, n, rhs, nrm2, part, st)) return rc;
-  c->launches += 2;   // init_state, scale_into
-  init_state<<<(nrhs + 127) / 128, 128, 0, st>>>(s, nrhs, maxit, nrm2);
-  scale_into<<<dim3((int)std::min<long long>((n + 255) / 256, 4LL * c->sm_count), nrhs), 256, 0,
-               st>>>(rhs, nrm2, n, nullptr, V);
-  PS_CUDA_TRY(c, cudaGetLastError());
+  if (int rc = norm_impl(c, nrhs, n, rhs, nrm2, K->part, st)) return rc;
+  if (int rc = begin_impl(c, K, rhs, nrm2, V, st)) return rc;
 
   std::vector<double> res(nrhs), bn(nrhs);
   std::vector<int> active(nrhs), kk(nrhs, 0), badrhs(nrhs + 1, 0);
-  PS_CUDA_TRY(c, cudaMemcpyAsync(bn.data(), s.bnorm, nrhs * sizeof(double), cudaMemcpyDeviceToHost, st));
-  PS_CUDA_TRY(c, cudaMemcpyAsync(badrhs.data(), s.nonfinite, (nrhs + 1) * sizeof(int),
+  PS_CUDA_TRY(c, cudaMemcpyAsync(bn.data(), K->s.bnorm, nrhs * sizeof(double),
+                                 cudaMemcpyDeviceToHost, st));
+  PS_CUDA_TRY(c, cudaMemcpyAsync(badrhs.data(), K->s.nonfinite, (nrhs + 1) * sizeof(int),
                                  cudaMemcpyDeviceToHost, st));
   PS_CUDA_TRY(c, cudaStreamSynchronize(st));
   for (int r = 0; r < nrhs; ++r)
@@ -431,30 +593,26 @@ int gmres(Ctx* c, const double2* rhs, double2* x, double tol, int maxit, int* it
   }
   int nactive = 0;
   for (int r = 0; r < nrhs; ++r) nactive += active[r];
-  const int bx = (int)std::min<long long>((n + 255) / 256, 4LL * c->sm_count);
-  int k = 0;
-  for (k = 0; k < maxit && nactive > 0; ++k) {
+  const int ld = maxit + 1;
+  for (int k = 0; k < maxit && nactive > 0; ++k) {
     double2* Vk = V + (size_t)k * nrhs * n;
-    double2* Vk1 = V + (size_t)(k + 1) * nrhs * n;
     // w = K V_k
     if (int rc = apply_schur(c, Vk, w, st)) return rc;
-    // CGS2
-    if (int rc = dot_impl(c, nrhs, n, k + 1, V, w, hcol, maxit + 1, 0, s.active, part, st)) return rc;
-    if (int rc = axpy_impl(c, nrhs, n, k + 1, V, hcol, maxit + 1, -1.0, s.active, w, st)) return rc;
-    if (int rc = dot_impl(c, nrhs, n, k + 1, V, w, y, maxit + 1, 0, s.active, part, st)) return rc;
-    if (int rc = axpy_impl(c, nrhs, n, k + 1, V, y, maxit + 1, -1.0, s.active, w, st)) return rc;
-    // hcol += y  (second-pass coefficients)
-    cadd_rows<<<(nrhs * (k + 1) + 127) / 128, 128, 0, st>>>(hcol, y, nrhs, k + 1, maxit + 1);
+    // CGS2: hcol = first-pass coefficients, y = second-pass ones
+    if (int rc = dot_impl(c, nrhs, n, k + 1, V, w, K->hcol, ld, K->s.active, K->part, st)) return rc;
+    if (int rc = axpy_impl(c, nrhs, n, k + 1, V, K->hcol, ld, -1.0, K->s.active, w, st)) return rc;
+    if (int rc = dot_impl(c, nrhs, n, k + 1, V, w, K->y, ld, K->s.active, K->part, st)) return rc;
+    if (int rc = axpy_impl(c, nrhs, n, k + 1, V, K->y, ld, -1.0, K->s.active, w, st)) return rc;
+    c->launches += 1;
+    cadd_rows<<<(nrhs * (k + 1) + 127) / 128, 128, 0, st>>>(K->hcol, K->y, nrhs, k + 1, ld);
     PS_CUDA_TRY(c, cudaGetLastError());
-    if (int rc = norm_impl(c, nrhs, n, w, nrm2, part, st)) return rc;
-    c->launches += 3;   // cadd_rows, givens_step, scale_into
-    givens_step<<<(nrhs + 127) / 128, 128, 0, st>>>(s, nrhs, k, maxit, hcol, maxit + 1, nrm2);
-    PS_CUDA_TRY(c, cudaGetLastError());
-    scale_into<<<dim3(bx, nrhs), 256, 0, st>>>(w, nrm2, n, s.active, Vk1);
-    PS_CUDA_TRY(c, cudaGetLastError());
+    if (int rc = norm_impl(c, nrhs, n, w, nrm2, K->part, st)) return rc;
+    if (int rc = step_impl(c, K, k, nrm2, w, V, st)) return rc;
     int nonfinite = 0;
-    PS_CUDA_TRY(c, cudaMemcpyAsync(res.data(), s.res, nrhs * sizeof(double), cudaMemcpyDeviceToHost, st));
-    PS_CUDA_TRY(c, cudaMemcpyAsync(&nonfinite, s.nonfinite, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PS_CUDA_TRY(c, cudaMemcpyAsync(res.data(), K->s.res, nrhs * sizeof(double),
+                                   cudaMemcpyDeviceToHost, st));
+    PS_CUDA_TRY(c, cudaMemcpyAsync(&nonfinite, K->s.nonfinite, sizeof(int), cudaMemcpyDeviceToHost,
+                                   st));
     PS_CUDA_TRY(c, cudaStreamSynchronize(st));
     if (nonfinite) {
       c->err = "ps_gmres: NaN/Inf in Krylov vector (SPEC.md:553)";
@@ -472,23 +630,10 @@ int gmres(Ctx* c, const double2* rhs, double2* x, double tol, int maxit, int* it
         changed = true;
       }
     }
-    if (changed) {
-      PS_CUDA_TRY(c, cudaMemcpyAsync(flags_dev, active.data(), nrhs * sizeof(int),
-                                     cudaMemcpyHostToDevice, st));
-      c->launches += 1;
-      set_flags<<<(nrhs + 127) / 128, 128, 0, st>>>(s.active, flags_dev, nrhs);
-      PS_CUDA_TRY(c, cudaGetLastError());
-    }
+    if (changed)
+      if (int rc = freeze_impl(c, K, active.data(), st)) return rc;
   }
-  // x = sum_i y_i V_i
-  PS_CUDA_TRY(c, cudaMemcpyAsync(kk_dev, kk.data(), nrhs * sizeof(int), cudaMemcpyHostToDevice, st));
-  c->launches += 1;
-  back_solve<<<(nrhs + 127) / 128, 128, 0, st>>>(s, nrhs, kk_dev, maxit, y, maxit + 1);
-  PS_CUDA_TRY(c, cudaGetLastError());
-  PS_CUDA_TRY(c, cudaMemsetAsync(x, 0, n2 * sizeof(double2), st));
-  int kmax_used = 0;
-  for (int r = 0; r < nrhs; ++r) kmax_used = std::max(kmax_used, kk[r]);
-  if (int rc = axpy_impl(c, nrhs, n, kmax_used, V, y, maxit + 1, 1.0, nullptr, x, st)) return rc;
+  if (int rc = solve_impl(c, K, kk.data(), V, x, st)) return rc;
   PS_CUDA_TRY(c, cudaStreamSynchronize(st));
   return PS_OK;
 }

@@ -369,25 +369,47 @@ class Engine:
     def stats_reset(self):
         self._check(self.lib.ps_stats_reset(self.ctx))
 
-    # GMRES building blocks for the multi-rank driver
-    def block_dot(self, V: torch.Tensor, w: torch.Tensor, k: int, h: torch.Tensor):
-        kmax, nrhs, n = V.shape
-        self._check(self.lib.ps_block_dot(self.ctx, nrhs, n, int(k), kmax,
-                                          ctypes.c_void_p(V.data_ptr()),
-                                          ctypes.c_void_p(w.data_ptr()),
-                                          ctypes.c_void_p(h.data_ptr()), _stream(self.device)))
+    # Arnoldi building blocks (krylov.gmres_device / parallel.gmres_dist)
+    def _vp(self, t: torch.Tensor):
+        if t.device != self.device or not t.is_contiguous():
+            raise TypeError(f"expected a contiguous tensor on {self.device}")
+        return ctypes.c_void_p(t.data_ptr())
+
+    def krylov_begin(self, b: torch.Tensor, bnorm2: torch.Tensor, V: torch.Tensor):
+        """State from the squared RHS norms, V[0] = b / ||b|| (b [nrhs][n])."""
+        kmax1, nrhs, n = V.shape
+        self._check(self.lib.ps_krylov_begin(self.ctx, nrhs, n, kmax1 - 1, self._vp(b),
+                                             self._vp(bnorm2), self._vp(V),
+                                             _stream(self.device)))
+
+    def krylov_dot(self, k: int, V: torch.Tensor, w: torch.Tensor, h: torch.Tensor):
+        self._check(self.lib.ps_krylov_dot(self.ctx, int(k), self._vp(V), self._vp(w), self._vp(h),
+                                           _stream(self.device)))
         return h
 
-    def block_axpy(self, V: torch.Tensor, h: torch.Tensor, k: int, w: torch.Tensor):
-        kmax, nrhs, n = V.shape
-        self._check(self.lib.ps_block_axpy(self.ctx, nrhs, n, int(k), kmax,
-                                           ctypes.c_void_p(V.data_ptr()),
-                                           ctypes.c_void_p(h.data_ptr()),
-                                           ctypes.c_void_p(w.data_ptr()), _stream(self.device)))
+    def krylov_axpy(self, k: int, V: torch.Tensor, h: torch.Tensor, w: torch.Tensor):
+        self._check(self.lib.ps_krylov_axpy(self.ctx, int(k), self._vp(V), self._vp(h),
+                                            self._vp(w), _stream(self.device)))
         return w
 
-    def norm2(self, w: torch.Tensor, out: torch.Tensor):
+    def krylov_norm2(self, w: torch.Tensor, out: torch.Tensor):
         nrhs, n = w.shape
-        self._check(self.lib.ps_norm2(self.ctx, nrhs, n, ctypes.c_void_p(w.data_ptr()),
-                                      ctypes.c_void_p(out.data_ptr()), _stream(self.device)))
+        self._check(self.lib.ps_krylov_norm2(self.ctx, nrhs, n, self._vp(w), self._vp(out),
+                                             _stream(self.device)))
         return out
+
+    def krylov_step(self, k: int, h1, h2, wn2, w, V, status):
+        self._check(self.lib.ps_krylov_step(self.ctx, int(k), self._vp(h1), self._vp(h2),
+                                            self._vp(wn2), self._vp(w), self._vp(V),
+                                            self._vp(status), _stream(self.device)))
+        return status
+
+    def krylov_freeze(self, active):
+        a = (ctypes.c_int * len(active))(*[int(x) for x in active])
+        self._check(self.lib.ps_krylov_freeze(self.ctx, a, _stream(self.device)))
+
+    def krylov_solve(self, iters, V: torch.Tensor, x: torch.Tensor):
+        it = (ctypes.c_int * len(iters))(*[int(x) for x in iters])
+        self._check(self.lib.ps_krylov_solve(self.ctx, it, self._vp(V), self._vp(x),
+                                             _stream(self.device)))
+        return x

@@ -9,17 +9,15 @@ Per Schur matvec:
      own targets, or (one RHS) the symmetric K1s over 1/world of the tile
      pairs for all targets followed by a reduce-scatter (ShardedSchur).
 GMRES dot products are local partial sums followed by an all-reduce; the
-Hessenberg least-squares bookkeeping (O(k) scalars) is replicated.
+Hessenberg / Givens update (O(k) scalars per RHS) is replicated on every
+rank's device (krylov.gmres_device).
 
-The same driver runs on CPU tensors with the gloo backend (tests) and on
-CUDA tensors with NCCL (bench / solve), where the orthogonalisation uses the
-C-ABI block kernels.
+Collectives run on the device with NCCL; with any other backend (gloo: the
+multi-process tests, including several ranks sharing one GPU) they stage
+through host copies.
 """
 from __future__ import annotations
 
-import math
-
-import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -32,42 +30,58 @@ def shard_sizes(M: int, world: int) -> list[int]:
     return [shard_range(M, r, world)[1] - shard_range(M, r, world)[0] for r in range(world)]
 
 
+def _world(group) -> int:
+    return dist.get_world_size(group) if dist.is_initialized() else 1
+
+
+def _device_collectives(t: torch.Tensor, group) -> bool:
+    """NCCL moves CUDA tensors itself; any other backend (gloo: the
+    multi-process tests, several ranks sharing one GPU) gets host copies."""
+    return t.is_cuda and dist.get_backend(group) == "nccl"
+
+
 def all_gather_rows(v_own: torch.Tensor, M: int, group=None) -> torch.Tensor:
     """[nrhs][M_own][L] on every rank -> [nrhs][M][L] (rows in rank order)."""
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    world = _world(group)
     if world == 1:
         return v_own
     sizes = shard_sizes(M, world)
+    dev = v_own.device
     vr = torch.view_as_real(v_own.contiguous())          # complex -> (..., 2) float64
-    if len(set(sizes)) == 1 and v_own.is_cuda:
+    on_dev = _device_collectives(vr, group)
+    if not on_dev:
+        vr = vr.cpu()
+    if len(set(sizes)) == 1 and on_dev:
         buf = torch.empty((world,) + tuple(vr.shape), dtype=vr.dtype, device=vr.device)
         dist.all_gather_into_tensor(buf, vr, group=group)
         full = buf.permute(1, 0, 2, 3, 4).reshape(v_own.shape[0], M, v_own.shape[2], 2)
         return torch.view_as_complex(full.contiguous())
-    # uneven shards: pad every rank's rows to the largest shard, gather, trim
+    # uneven shards (or host staging): pad every rank's rows to the largest
+    # shard, gather, trim
     mx = max(sizes)
     pad = torch.zeros((v_own.shape[0], mx, v_own.shape[2], 2), dtype=vr.dtype, device=vr.device)
     pad[:, :vr.shape[1]] = vr
     parts = [torch.empty_like(pad) for _ in sizes]
     dist.all_gather(parts, pad, group=group)
     full = torch.cat([p[:, :s] for p, s in zip(parts, sizes)], dim=1)
-    return torch.view_as_complex(full.contiguous())
+    return torch.view_as_complex(full.contiguous()).to(dev)
 
 
 def reduce_scatter_rows(x_full: torch.Tensor, M: int, group=None) -> torch.Tensor:
     """[nrhs][M][L] partial sums on every rank -> this rank's rows
     shard_range(M, rank, world) of the sum over ranks (NCCL reduce-scatter;
-    uneven shards are padded; gloo, which has no reduce-scatter here, sums
-    with an all-reduce and slices)."""
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    uneven shards are padded; other backends sum with an all-reduce of host
+    copies and slice)."""
+    world = _world(group)
     if world == 1:
         return x_full
     rank = dist.get_rank(group)
     t0, t1 = shard_range(M, rank, world)
     xr = torch.view_as_real(x_full.contiguous())
-    if not x_full.is_cuda:
-        dist.all_reduce(xr, group=group)
-        return torch.view_as_complex(xr)[:, t0:t1].contiguous()
+    if not _device_collectives(xr, group):
+        h = xr.cpu()
+        dist.all_reduce(h, group=group)
+        return torch.view_as_complex(h)[:, t0:t1].contiguous().to(x_full.device)
     sizes = shard_sizes(M, world)
     mx = max(sizes)
     if len(set(sizes)) == 1:
@@ -84,12 +98,30 @@ def reduce_scatter_rows(x_full: torch.Tensor, M: int, group=None) -> torch.Tenso
 
 
 def all_reduce_(t: torch.Tensor, group=None) -> torch.Tensor:
-    if dist.is_initialized() and dist.get_world_size(group) > 1:
-        if t.is_complex():
-            tr = torch.view_as_real(t)
-            dist.all_reduce(tr, group=group)
-        else:
-            dist.all_reduce(t, group=group)
+    """In-place sum over ranks (complex tensors as their real view)."""
+    if _world(group) == 1:
+        return t
+    tr = torch.view_as_real(t) if t.is_complex() else t
+    if _device_collectives(tr, group):
+        dist.all_reduce(tr, group=group)
+    else:
+        h = tr.cpu()
+        dist.all_reduce(h, group=group)
+        tr.copy_(h)
+    return t
+
+
+def broadcast_(t: torch.Tensor, src: int, group=None) -> torch.Tensor:
+    """In-place broadcast from group rank ``src``."""
+    if _world(group) == 1:
+        return t
+    gsrc = src if group is None else dist.get_global_rank(group, src)
+    if _device_collectives(t, group):
+        dist.broadcast(t, src=gsrc, group=group)
+    else:
+        h = t.cpu()
+        dist.broadcast(h, src=gsrc, group=group)
+        t.copy_(h)
     return t
 
 
@@ -99,7 +131,7 @@ def setup_empty_split(eng, configs, group=None):
     (one launch, ~1 ms) but factorises only its share shard_range(R, rank,
     world); each RHS's packed A^+ factors (15 MB at the BASELINE geometry) are
     then broadcast from the owning rank over NCCL."""
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    world = _world(group)
     R = len(configs)
     if world == 1 or R == 1:
         return eng.setup_empty(configs)
@@ -111,8 +143,7 @@ def setup_empty_split(eng, configs, group=None):
                      < shard_range(R, r, world)[1])
         if owner == rank:
             eng.export_pinv(q, buf)
-        dist.broadcast(buf, src=owner if group is None else dist.get_global_rank(group, owner),
-                       group=group)
+        broadcast_(buf, owner, group)
         if owner != rank:
             eng.import_pinv(q, buf)
     return systems
@@ -137,7 +168,7 @@ class ShardedSchur:
     def __init__(self, op, group=None, mode: str = "auto", overlap="auto", reserve: int = 4):
         self.op = op
         self.group = group
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.world = _world(group)
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.t0, self.t1 = shard_range(op.M, self.rank, self.world)
         self.s_range = (self.t0, self.t1)     # own sources for the C partial sum
@@ -217,113 +248,15 @@ class ShardedSchur:
         return self.op.eng.recover(g)
 
 
-class _TorchOps:
-    """Vector kernels for the distributed GMRES: the C-ABI block kernels on
-    CUDA, plain torch on CPU (gloo tests)."""
-
-    def __init__(self, engine=None):
-        self.eng = engine
-
-    def dot(self, V, w, k, h):                 # h[r][i] = <V_i^r, w^r>
-        if self.eng is not None and w.is_cuda:
-            return self.eng.block_dot(V, w, k, h)
-        h[:, :k] = torch.einsum("krn,rn->rk", V[:k].conj(), w)
-        return h
-
-    def axpy(self, V, h, k, w):                # w -= sum_i h_i V_i
-        if self.eng is not None and w.is_cuda:
-            return self.eng.block_axpy(V, h, k, w)
-        w -= torch.einsum("rk,krn->rn", h[:, :k], V[:k])
-        return w
-
-    def norm2(self, w, out):
-        if self.eng is not None and w.is_cuda:
-            return self.eng.norm2(w, out)
-        out.copy_((w.real ** 2 + w.imag ** 2).sum(dim=1))
-        return out
-
-
 def gmres_dist(apply, rhs_own: torch.Tensor, tol: float = 1e-10, maxit: int = 150,
-               group=None, engine=None):
-    """Unrestarted GMRES over target-sharded vectors, CGS2
-    Arnoldi, zero initial guess, per-RHS stopping.  ``apply(v_own) -> y_own``
-    must do its own communication.  Returns (x_own, iterations, histories)."""
-    nrhs = rhs_own.shape[0]
-    shape = rhs_own.shape
-    n = rhs_own[0].numel()
-    dev = rhs_own.device
-    ops = _TorchOps(engine)
-    V = torch.zeros((maxit + 1, nrhs, n), dtype=torch.complex128, device=dev)
-    b = rhs_own.reshape(nrhs, n)
-    nb = torch.empty(nrhs, dtype=torch.float64, device=dev)
-    ops.norm2(b, nb)
-    all_reduce_(nb, group)
-    bnorm = np.sqrt(nb.cpu().numpy())
-    active = bnorm > 0
-    V[0] = b / torch.as_tensor(np.where(active, bnorm, 1.0), device=dev)[:, None]
-    H = np.zeros((nrhs, maxit + 1, maxit), dtype=complex)
-    cs = np.zeros((nrhs, maxit), dtype=complex)
-    sn = np.zeros((nrhs, maxit), dtype=complex)
-    g = np.zeros((nrhs, maxit + 1), dtype=complex)
-    g[:, 0] = bnorm
-    hist = [[1.0 if a else 0.0] for a in active]
-    iters = [0] * nrhs
-    h1 = torch.zeros((nrhs, maxit + 1), dtype=torch.complex128, device=dev)
-    h2 = torch.zeros_like(h1)
-    w2 = torch.empty(nrhs, dtype=torch.float64, device=dev)
-    k = 0
-    for k in range(maxit):
-        if not active.any():
-            break
-        w = apply(V[k].reshape(shape)).reshape(nrhs, n).clone()
-        amask = torch.as_tensor(active, device=dev)
-        w[~amask] = 0
-        ops.dot(V, w, k + 1, h1)
-        hk = h1[:, :k + 1].contiguous()
-        all_reduce_(hk, group)
-        ops.axpy(V, hk, k + 1, w)
-        ops.dot(V, w, k + 1, h2)
-        hk2 = h2[:, :k + 1].contiguous()
-        all_reduce_(hk2, group)
-        ops.axpy(V, hk2, k + 1, w)
-        ops.norm2(w, w2)
-        all_reduce_(w2, group)
-        hcol = (hk + hk2).cpu().numpy()
-        wn = np.sqrt(w2.cpu().numpy())
-        if not np.all(np.isfinite(hcol)) or not np.all(np.isfinite(wn)):
-            raise FloatingPointError("gmres_dist: NaN/Inf in Krylov vector (SPEC.md:553)")
-        scale = np.where(active & (wn > 0), wn, 1.0)
-        V[k + 1] = w / torch.as_tensor(scale, device=dev)[:, None]
-        for r in range(nrhs):
-            if not active[r]:
-                continue
-            col = H[r, :, k]
-            col[:k + 1] = hcol[r]
-            col[k + 1] = wn[r]
-            for i in range(k):
-                t = np.conj(cs[r, i]) * col[i] + np.conj(sn[r, i]) * col[i + 1]
-                col[i + 1] = -sn[r, i] * col[i] + cs[r, i] * col[i + 1]
-                col[i] = t
-            a_, b_ = col[k], col[k + 1]
-            rr = math.hypot(abs(a_), abs(b_))
-            cs[r, k] = a_ / rr if rr else 1.0
-            sn[r, k] = b_ / rr if rr else 0.0
-            col[k] = rr
-            col[k + 1] = 0.0
-            g[r, k + 1] = -sn[r, k] * g[r, k]
-            g[r, k] = np.conj(cs[r, k]) * g[r, k]
-            res = abs(g[r, k + 1]) / bnorm[r]
-            hist[r].append(res)
-            iters[r] = k + 1
-            if res <= tol:
-                active[r] = False
-    x = torch.zeros((nrhs, n), dtype=torch.complex128, device=dev)
-    kmax = max(iters) if iters else 0
-    ny = np.zeros((nrhs, kmax), dtype=complex)
-    for r in range(nrhs):
-        kk = iters[r]
-        if kk:
-            ny[r, :kk] = -np.linalg.solve(np.triu(H[r, :kk, :kk]), g[r, :kk])
-    if kmax:
-        ops.axpy(V, torch.as_tensor(ny, device=dev).contiguous(), kmax, x)   # x = sum_i y_i V_i
-    return x.reshape(shape), iters, hist
+               group=None, engine=None, ops=None):
+    """Unrestarted GMRES over target-sharded vectors: CGS2
+    Arnoldi, zero initial guess, per-RHS stopping, with the Arnoldi vectors,
+    the Hessenberg / Givens state and the least-squares solve all on the
+    device (krylov.gmres_device).  Per iteration: two all-reduces of the
+    [nrhs][k+1] CGS2 columns, one of the [nrhs] squared norms, one
+    device->host read of the residuals.  ``apply(v_own) -> y_own`` does its
+    own communication.  Returns (x_own, iterations, histories)."""
+    from .krylov import gmres_device
+    return gmres_device(apply, rhs_own, tol, maxit, engine=engine,
+                        reduce=lambda t: all_reduce_(t, group), ops=ops)

@@ -26,7 +26,14 @@ class _ConfigOnly:
 class SchurOperator:
     def __init__(self, systems, centers, p: int, smat=None, radius: float | None = None,
                  rot=None, device=None, target_range=None, coupled: bool = True,
-                 engine: Engine | None = None, dense_gb: float = 40.0):
+                 engine: Engine | None = None, dense_gb: float = 40.0, group=None,
+                 split_setup: bool = False):
+        """``split_setup`` (opt-in, collective): with configs and several
+        RHS, every rank of ``group`` factorises only its share of the
+        per-angle SVDs and the factors are broadcast
+        (parallel.setup_empty_split); all ranks of the group must construct
+        the operator together.  Without it the constructor never
+        communicates."""
         if not isinstance(systems, (list, tuple)):
             systems = [systems]
         items = list(systems)
@@ -54,11 +61,11 @@ class SchurOperator:
         self.coupled = coupled
         self.systems = items
         if coupled:
-            if self.device_setup:
-                # under torch.distributed the per-angle SVDs are split across
-                # ranks and the factors broadcast (parallel.setup_empty_split)
+            if self.device_setup and split_setup:
                 from .parallel import setup_empty_split
-                self.systems = setup_empty_split(eng, configs)
+                self.systems = setup_empty_split(eng, configs, group)
+            elif self.device_setup:
+                self.systems = eng.setup_empty(configs)
             else:
                 eng.set_layers(items[0])
                 for r, s in enumerate(items):
@@ -111,15 +118,33 @@ def apply_schur_operator(op: SchurOperator, beta):
     return y.cpu().numpy() if on_host else y
 
 
-def gmres(op: SchurOperator, rhs, tol: float = 1e-10, maxit: int = 150):
+def gmres(op, rhs, tol: float = 1e-10, maxit: int = 150, engine: Engine | None = None):
     """Unrestarted device GMRES.  Returns (x, iterations per
-    RHS, residual history per RHS)."""
+    RHS, residual history per RHS).
+
+    ``op`` is a SchurOperator owning all targets (the all-in-C driver
+    ps_gmres) or any callable ``op(v) -> y`` on complex128 CUDA tensors of
+    rhs's shape (krylov.gmres_device: the Arnoldi step still runs in the
+    library kernels, on ``engine`` or op.eng or a fresh context).  Host
+    arrays round-trip through the device."""
     on_host = not isinstance(rhs, torch.Tensor)
-    r = torch.as_tensor(np.asarray(rhs, dtype=complex).reshape(op.shape) if on_host else rhs)
-    r = r.to(device=op.device, dtype=torch.complex128).contiguous()
-    x, its, hist = op.eng.gmres(r, tol, maxit)
-    hist_l = [h[~np.isnan(h)].tolist() for h in hist]
-    return (x.cpu().numpy() if on_host else x), its, hist_l
+    if isinstance(op, SchurOperator) and op.eng.t_range == (0, op.M):
+        r = torch.as_tensor(np.asarray(rhs, dtype=complex).reshape(op.shape) if on_host else rhs)
+        r = r.to(device=op.device, dtype=torch.complex128).contiguous()
+        x, its, hist = op.eng.gmres(r, tol, maxit)
+        hist_l = [h[~np.isnan(h)].tolist() for h in hist]
+        return (x.cpu().numpy() if on_host else x), its, hist_l
+    from .krylov import gmres_device
+    eng = engine or getattr(op, "eng", None)
+    if on_host:
+        dev = eng.device if eng is not None else torch.device("cuda", torch.cuda.current_device())
+        r = torch.as_tensor(np.ascontiguousarray(np.asarray(rhs, dtype=complex))).to(dev)
+    else:
+        r = rhs.to(torch.complex128).contiguous()
+    if eng is None:
+        eng = Engine(r.device)
+    x, its, hist = gmres_device(op, r, tol, maxit, engine=eng)
+    return (x.cpu().numpy() if on_host else x), its, hist
 
 
 @dataclass

@@ -64,7 +64,8 @@ def _body(rank, world, q):
         y = np.stack([(A[r] @ vf[r].reshape(-1)).reshape(M, L) for r in range(nrhs)])
         return torch.as_tensor(y[:, t0:t1]).contiguous()
 
-    x, its, hist = parallel.gmres_dist(apply, own, tol=1e-12, maxit=60)
+    from host_krylov import HostKrylov
+    x, its, hist = parallel.gmres_dist(apply, own, tol=1e-12, maxit=60, ops=HostKrylov())
     xf = parallel.all_gather_rows(x.contiguous(), M).numpy()
     q.put((rank, xf, its))
 
@@ -106,12 +107,22 @@ def test_gmres_dist_single_process_matches_oracle_gmres():
     from oracle import periscat_oracle as O
     from paper_1412_7466_b200 import parallel
     A, b = _dense_problem(5, 3, 1, seed=3)
+    from host_krylov import HostKrylov
     x, its, hist = parallel.gmres_dist(
         lambda v: torch.as_tensor((A[0] @ v.numpy()[0].reshape(-1)).reshape(1, 5, 3)),
-        torch.as_tensor(b), tol=1e-12, maxit=40)
+        torch.as_tensor(b), tol=1e-12, maxit=40, ops=HostKrylov())
     xo, its_o, _ = O.gmres(lambda v: A[0] @ v, b[0].reshape(-1), 1e-12, 40)
     assert its[0] == its_o
     assert np.linalg.norm(x.numpy()[0].reshape(-1) - xo) / np.linalg.norm(xo) < 1e-12
+
+
+def test_gmres_dist_has_no_cpu_fallback():
+    """The product driver runs the Arnoldi step in the CUDA kernels only:
+    host tensors without a test double are rejected, not computed on CPU."""
+    from paper_1412_7466_b200 import parallel
+    A, b = _dense_problem(5, 3, 1, seed=3)
+    with pytest.raises((TypeError, ValueError)):
+        parallel.gmres_dist(lambda v: v, torch.as_tensor(b), tol=1e-12, maxit=5)
 
 
 class _FakeDist:
@@ -128,6 +139,9 @@ class _FakeDist:
 
     def is_initialized(self):
         return True
+
+    def get_backend(self, group=None):
+        return "nccl"
 
     def get_world_size(self, group=None):
         return self.world

@@ -577,3 +577,23 @@ def test_schur_cfg3_full_vector(O):
     uT = np.concatenate([O.apply_T(v, pb.centers, pb.es.k2, pb.p, pb.es.bloch, targets=c)
                          for c in (np.arange(0, 40), np.arange(960, 1000))], axis=0)
     assert rel(aT[np.r_[0:40, 960:1000]], uT) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("M,p", [(11, 25), (14, 20), (22, 25)])
+def test_dense_coupling_many_ct_blocks(O, M, p):
+    """Dense coupling where the C^T GEMV launches more than 512 split blocks
+    (K = M L in 524..592 on 148 SMs): the workspace holds every block's
+    partial sums (gpart sizing) and the matvec matches the oracle."""
+    from paper_1412_7466_b200 import grating, solver
+    rng = np.random.default_rng(M * 100 + p)
+    xs = (np.arange(M) + 0.5) / M - 0.5
+    centers = np.column_stack([xs, rng.uniform(-0.3, 0.3, M)])
+    sysm = grating.load_fixture("w10")
+    pr = O.Problem(O.load_empty("w10"), centers, p, 0.012)
+    op = solver.SchurOperator(sysm, centers, p, smat=pr.smat, dense_gb=40.0)
+    assert op.dense
+    v = pr.smat[None, :] * _cplx(rng, (M, 2 * p + 1))
+    for _ in range(2):
+        got = op(_dev(v[None])).cpu().numpy()[0]
+    ref = O.apply_schur_operator(pr, v).reshape(M, 2 * p + 1)
+    assert rel(got, ref) <= MATVEC_TOL

@@ -67,7 +67,8 @@ else:
     local, trange = 0, None
 
 t1 = time.perf_counter()
-op = solver.SchurOperator(systems, centers, p, radius=radius, device=local, target_range=trange)
+op = solver.SchurOperator(systems, centers, p, radius=radius, device=local, target_range=trange,
+                          split_setup=world > 1)
 sharded = parallel.ShardedSchur(op) if world > 1 else None
 rhs = op.rhs()
 torch.cuda.synchronize()
