@@ -57,6 +57,12 @@ int ps_max_order(void);
 int ps_set_geometry(ps_ctx* ctx, int M, int p, int copies, double period, double k2,
                     const double* centers_host /* [M][2] */);
 
+/* Disk-overlap domain check with the reference's
+ * ParticleSet.min_gap semantics (geometry.py:131-144): smallest centre
+ * distance over all pairs and their +-d copies minus 2 radius (+inf for
+ * fewer than two inclusions), computed on the device.  PS_ERR_DOMAIN when
+ * negative (overlapping enclosing disks); *min_gap (may be NULL) gets it. */
+int ps_check_overlap(ps_ctx* ctx, double radius, double* min_gap);
 /* Owned target inclusions [t_begin, t_end) for target sharding across ranks
  * ("apply_T parallel over target particles"). */
 int ps_set_target_range(ps_ctx* ctx, int t_begin, int t_end);
@@ -139,6 +145,12 @@ int ps_apply_T(ps_ctx* ctx, const void* beta_dev, void* out_dev, void* stream);
  * mask them. */
 int ps_particle_field(ps_ctx* ctx, const void* beta, int npts, const double* pts, void* out,
                       void* stream);
+/* ps_particle_field plus the derivative along the unit vector dirs[pt]
+ * (dirs [npts][2] f64 device; out_dn [nrhs][npts]): the particle part of
+ * the wall-discrepancy check (empty_grating.wall_discrepancy_residual's
+ * extra_field, eg:396-433). */
+int ps_particle_field_grad(ps_ctx* ctx, const void* beta, int npts, const double* pts,
+                           const double* dirs, void* out, void* out_dn, void* stream);
 int ps_apply_T_blocks(ps_ctx* ctx, int part, int nparts, const void* beta, void* out,
                       void* stream);
 /* Epilogue of the split: y_own = v_own - S (a_own - B A^+ g) for the owned
@@ -303,6 +315,26 @@ int ps_set_field_params(ps_ctx* ctx, double k1, double k3, const double* c1_host
  * quadrature: keep points ~5 node spacings off the interfaces (lp:244-246). */
 int ps_layer_field(ps_ctx* ctx, const void* x_dev, int npts, const double* pts_dev,
                    const int* layer_dev, void* out_dev, void* stream);
+/* Values and derivatives along dirs[pt] of the layer field (incident wave in
+ * layer 1 only if incident != 0: eval_empty_field total=True/False) -- the
+ * empty-grating part of wall_discrepancy_residual (eg:396-433), with the
+ * derivative kernels N / T of layerpot._kernel_values_diff (lp:67-91) and
+ * the regular-wave gradients (sf:86-125). */
+int ps_layer_field_grad(ps_ctx* ctx, const void* x_dev, int npts, const double* pts_dev,
+                        const int* layer_dev, const double* dirs_dev, int incident,
+                        void* out_dev, void* out_dn_dev, void* stream);
+/* The empty-grating matrix of one RHS when the factors came from host SVDs
+ * (ps_setup_empty keeps its own): A_host the COLUMN-SCALED matrix
+ * (EmptyGratingSystem.matrix, row-major complex [m][ncol]), f_host [m],
+ * col_scale_host [ncol] (empty_grating.py:246-255). */
+int ps_set_empty_system(ps_ctx* ctx, int irhs, int m, int ncol, const double* A_host,
+                        const double* f_host, const double* col_scale_host);
+/* Empty-grating rows of the coupled residual (solve_empty's
+ * residual, eg:289-290): per RHS out_dev[2r] = ||A (x / cs) + C beta - f||^2
+ * and out_dev[2r+1] = ||f||^2, x [nrhs][ncol] all unknowns (ps_recover_full),
+ * g_dev [nrhs][nrow_c] = C beta (NULL: zero). */
+int ps_empty_residual(ps_ctx* ctx, const void* x_dev, const void* g_dev, double* out_dev,
+                      void* stream);
 
 /* ---- particle scattering matrix ------------------- */
 

@@ -27,6 +27,7 @@ SIGNATURES = {
     "ps_last_error": (ctypes.c_char_p, [_P]),
     "ps_set_geometry": (_I, [_P, _I, _I, _I, _D, _D, _P]),
     "ps_set_target_range": (_I, [_P, _I, _I]),
+    "ps_check_overlap": (_I, [_P, _D, _DP]),
     "ps_set_rhs_bloch": (_I, [_P, _I, _P]),
     "ps_set_smatrix": (_I, [_P, _P, _I, _P]),
     "ps_set_layers": (_I, [_P, _I, _P, _I, _P, _I, _P, _P, _I, _I]),
@@ -74,6 +75,10 @@ SIGNATURES = {
     "ps_recover_full": (_I, [_P, _P, _P, _P]),
     "ps_set_field_params": (_I, [_P, _D, _D, _P, _P, _P]),
     "ps_layer_field": (_I, [_P, _P, _I, _P, _P, _P, _P]),
+    "ps_layer_field_grad": (_I, [_P, _P, _I, _P, _P, _P, _I, _P, _P, _P]),
+    "ps_particle_field_grad": (_I, [_P, _P, _I, _P, _P, _P, _P, _P]),
+    "ps_set_empty_system": (_I, [_P, _I, _I, _I, _P, _P, _P]),
+    "ps_empty_residual": (_I, [_P, _P, _P, _P, _P]),
 }
 
 

@@ -52,6 +52,64 @@ int upload_blochpow(Ctx* c) {
   return dev_upload(c, &c->d_blochpow, h.data(), h.size());
 }
 
+// Closest pair of centres over the phased copies l = -lmax..lmax (j >= i;
+// the self term j == i, l == 0 excluded): thread per i, per-thread result;
+// the host reduces the M records (deterministic: smallest distance, then
+// smallest i).  Replaces an O(M^2) host scan (1.5e8 pairs at M = 1e4).
+__global__ void pair_min_dist(const double2* __restrict__ c, int M, int lmax, double period,
+                              double* __restrict__ best, int* __restrict__ bj,
+                              int* __restrict__ bl) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const double2 ci = c[i];
+  double m = INFINITY;
+  int mj = -1, ml = 0;
+  for (int j = i; j < M; ++j) {
+    const double2 cj = c[j];
+    for (int l = -lmax; l <= lmax; ++l) {
+      if (j == i && l == 0) continue;
+      const double d = hypot(ci.x - cj.x - l * period, ci.y - cj.y);
+      if (d < m) {
+        m = d;
+        mj = j;
+        ml = l;
+      }
+    }
+  }
+  best[i] = m;
+  bj[i] = mj;
+  bl[i] = ml;
+}
+
+struct Closest {
+  double dist = INFINITY;
+  int i = -1, j = -1, l = 0;
+};
+
+int closest_pair(Ctx* c, int lmax, Closest* out) {
+  *out = Closest{};
+  const int M = c->M;
+  if (M < 1) return PS_OK;
+  double* d = nullptr;
+  PS_CUDA_TRY(c, ps::dev_malloc(&d, (size_t)M * (sizeof(double) + 2 * sizeof(int))));
+  int* dj = reinterpret_cast<int*>(d + M);
+  int* dl = dj + M;
+  pair_min_dist<<<(M + 127) / 128, 128>>>(reinterpret_cast<const double2*>(c->d_centers), M, lmax,
+                                          c->period, d, dj, dl);
+  c->launches += 1;
+  std::vector<double> hd(M);
+  std::vector<int> hj(M), hl(M);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(hd.data(), d, M * sizeof(double), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(hj.data(), dj, M * sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(hl.data(), dl, M * sizeof(int), cudaMemcpyDeviceToHost);
+  ps::dev_free(d);
+  PS_CUDA_TRY(c, e);
+  for (int i = 0; i < M; ++i)
+    if (hj[i] >= 0 && hd[i] < out->dist) *out = Closest{hd[i], i, hj[i], hl[i]};
+  return PS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -115,21 +173,6 @@ int ps_set_geometry(ps_ctx* h, int M, int p, int copies, double period, double k
              std::to_string(ps::m2l_max_order());
     return PS_ERR_UNSUPPORTED;
   }
-  // coincident centres (incl. phased copies) make the translation singular
-  // (SPEC.md:458, 506).  Disk overlap itself is the caller's geometry
-  // contract (ParticleSet.min_gap, geometry.py:131-144).
-  for (int i = 0; i < M; ++i)
-    for (int j = i; j < M; ++j)
-      for (int l = -copies; l <= copies; ++l) {
-        if (i == j && l == 0) continue;
-        const double dx = centers[2 * i] - centers[2 * j] - l * period;
-        const double dy = centers[2 * i + 1] - centers[2 * j + 1];
-        if (dx == 0.0 && dy == 0.0) {
-          c->err = "ps_set_geometry: coincident centres " + std::to_string(i) + ", " +
-                   std::to_string(j) + " (copy " + std::to_string(l) + ")";
-          return PS_ERR_DOMAIN;
-        }
-      }
   if (int rc = set_device(c)) return rc;
   c->M = M;
   c->p = p;
@@ -141,7 +184,47 @@ int ps_set_geometry(ps_ctx* h, int M, int p, int copies, double period, double k
   c->t_end = M;
   c->h_centers.assign(centers, centers + 2 * (size_t)M);
   if (int rc = dev_upload(c, &c->d_centers, centers, 2 * (size_t)M)) return rc;
+  // coincident centres (incl. phased copies) make the translation singular
+  // (SPEC.md:458, 506); disk overlap needs the radius (ps_check_overlap)
+  Closest cp;
+  if (int rc = closest_pair(c, copies, &cp)) return rc;
+  if (cp.i >= 0 && cp.dist == 0.0) {
+    c->err = "ps_set_geometry: coincident centres " + std::to_string(cp.i) + ", " +
+             std::to_string(cp.j) + " (copy " + std::to_string(cp.l) + ")";
+    c->M = 0;
+    return PS_ERR_DOMAIN;
+  }
   return upload_blochpow(c);
+}
+
+int ps_check_overlap(ps_ctx* h, double radius, double* min_gap) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (!(radius >= 0.0)) {
+    c->err = "ps_check_overlap: bad radius";
+    return PS_ERR_ARG;
+  }
+  if (c->p < 0) {
+    c->err = "ps_check_overlap: geometry not set";
+    return PS_ERR_STATE;
+  }
+  if (int rc = set_device(c)) return rc;
+  // ParticleSet.min_gap (geometry.py:131-144): all pairs and their +-d
+  // copies; fewer than two inclusions -> +inf
+  double gap = INFINITY;
+  Closest cp;
+  if (c->M >= 2) {
+    if (int rc = closest_pair(c, 1, &cp)) return rc;
+    gap = cp.dist - 2.0 * radius;
+  }
+  if (min_gap) *min_gap = gap;
+  if (gap < 0.0) {
+    c->err = "overlapping inclusions " + std::to_string(cp.i) + ", " + std::to_string(cp.j) +
+             " (copy " + std::to_string(cp.l) + "): centre distance " + std::to_string(cp.dist) +
+             " < 2R = " + std::to_string(2.0 * radius) + " (SPEC.md:458, 506)";
+    return PS_ERR_DOMAIN;
+  }
+  return PS_OK;
 }
 
 int ps_set_target_range(ps_ctx* h, int t_begin, int t_end) {
@@ -336,8 +419,27 @@ int ps_particle_field(ps_ctx* h, const void* beta, int npts, const double* pts, 
     return PS_ERR_ARG;
   }
   if (int rc = set_device(c)) return rc;
-  return ps::particle_field(c, reinterpret_cast<const double2*>(beta), pts, npts,
-                            reinterpret_cast<double2*>(out), reinterpret_cast<cudaStream_t>(stream));
+  return ps::particle_field(c, reinterpret_cast<const double2*>(beta), pts, nullptr, npts,
+                            reinterpret_cast<double2*>(out), nullptr,
+                            reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_particle_field_grad(ps_ctx* h, const void* beta, int npts, const double* pts,
+                           const double* dirs, void* out, void* out_dn, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (c->p < 0) {
+    c->err = "ps_particle_field_grad: geometry not set";
+    return PS_ERR_STATE;
+  }
+  if (npts < 0 || (npts > 0 && (!beta || !pts || !dirs || !out || !out_dn))) {
+    c->err = "ps_particle_field_grad: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::particle_field(c, reinterpret_cast<const double2*>(beta), pts, dirs, npts,
+                            reinterpret_cast<double2*>(out), reinterpret_cast<double2*>(out_dn),
+                            reinterpret_cast<cudaStream_t>(stream));
 }
 
 int ps_set_field_params(ps_ctx* h, double k1, double k3, const double* c1, const double* c3,
@@ -392,8 +494,23 @@ int ps_layer_field(ps_ctx* h, const void* x, int npts, const double* pts, const 
     return PS_ERR_ARG;
   }
   if (int rc = set_device(c)) return rc;
-  return ps::layer_field(c, reinterpret_cast<const double2*>(x), pts, layer, npts,
-                         reinterpret_cast<double2*>(out), reinterpret_cast<cudaStream_t>(stream));
+  return ps::layer_field(c, reinterpret_cast<const double2*>(x), pts, layer, nullptr, npts, 1,
+                         reinterpret_cast<double2*>(out), nullptr,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ps_layer_field_grad(ps_ctx* h, const void* x, int npts, const double* pts, const int* layer,
+                        const double* dirs, int incident, void* out, void* out_dn, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (npts < 0 || (npts > 0 && (!x || !pts || !layer || !dirs || !out || !out_dn))) {
+    c->err = "ps_layer_field_grad: bad argument";
+    return PS_ERR_ARG;
+  }
+  if (int rc = set_device(c)) return rc;
+  return ps::layer_field(c, reinterpret_cast<const double2*>(x), pts, layer, dirs, npts,
+                         incident ? 1 : 0, reinterpret_cast<double2*>(out),
+                         reinterpret_cast<double2*>(out_dn), reinterpret_cast<cudaStream_t>(stream));
 }
 
 int ps_apply_T_blocks(ps_ctx* h, int part, int nparts, const void* beta, void* out, void* stream) {

@@ -520,6 +520,63 @@ struct EmptyState {
   double t_assemble_ms = 0, t_svd_ms = 0;
 };
 
+// Residual of the empty-grating rows of the coupled system (Eq.
+// finalsys rows [A C][x; beta] = f; solve_empty's residual, eg:289-290):
+// r_i = sum_j A_s[i][j] x_j / cs_j + g_i - f_i, g = C beta on its nrow_c
+// rows (zero elsewhere).  Thread per row (A_s column-major: coalesced).
+__global__ void empty_residual_kernel(const double2* __restrict__ A, const double2* __restrict__ f,
+                                      const double* __restrict__ cs, const double2* __restrict__ x,
+                                      const double2* __restrict__ g, int m, int ncol, int nrow_c,
+                                      double2* __restrict__ res) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (i >= m) return;
+  const double2* Ar = A + (size_t)r * m * ncol;
+  const double2* xr = x + (size_t)r * ncol;
+  const double* cr = cs + (size_t)r * ncol;
+  double sx = 0.0, sy = 0.0;
+  for (int j = 0; j < ncol; ++j) {
+    const double2 a = Ar[(size_t)j * m + i];
+    const double2 v = xr[j];
+    const double ic = 1.0 / cr[j];
+    sx = fma(a.x, v.x * ic, fma(-a.y, v.y * ic, sx));
+    sy = fma(a.x, v.y * ic, fma(a.y, v.x * ic, sy));
+  }
+  const double2 fi = f[(size_t)r * m + i];
+  if (g && i < nrow_c) {
+    sx += g[(size_t)r * nrow_c + i].x;
+    sy += g[(size_t)r * nrow_c + i].y;
+  }
+  res[(size_t)r * m + i] = make_double2(sx - fi.x, sy - fi.y);
+}
+
+// out[r] = (||res_r||^2, ||f_r||^2), one block per RHS, fixed order
+__global__ void residual_norms(const double2* __restrict__ res, const double2* __restrict__ f,
+                               int m, double* __restrict__ out) {
+  __shared__ double sh[2][256];
+  const int r = blockIdx.x;
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const double2 v = res[(size_t)r * m + i], w = f[(size_t)r * m + i];
+    a = fma(v.x, v.x, fma(v.y, v.y, a));
+    b = fma(w.x, w.x, fma(w.y, w.y, b));
+  }
+  sh[0][threadIdx.x] = a;
+  sh[1][threadIdx.x] = b;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      sh[0][threadIdx.x] += sh[0][threadIdx.x + o];
+      sh[1][threadIdx.x] += sh[1][threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[2 * r] = sh[0][0];
+    out[2 * r + 1] = sh[1][0];
+  }
+}
+
 void empty_release(Ctx* c) {
   if (!c->empty) return;
   EmptyState* e = c->empty;
@@ -963,6 +1020,68 @@ int ps_get_empty(ps_ctx* h, int irhs, double* A, double* f, double* col_scale, d
   if (s)
     PS_TRY_CUDA(cudaMemcpy(s, e->d_s + (size_t)irhs * n, (size_t)n * sizeof(double),
                            cudaMemcpyDeviceToHost));
+  return PS_OK;
+}
+
+int ps_set_empty_system(ps_ctx* h, int irhs, int m, int ncol, const double* A, const double* f,
+                        const double* col_scale) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = ps::C(h);
+  if (irhs < 0 || irhs >= c->nrhs || m <= 0 || ncol <= 0 || !A || !f || !col_scale)
+    return fail(c, PS_ERR_ARG, "ps_set_empty_system: bad argument");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, PS_ERR_CUDA, "cudaSetDevice");
+  ps::EmptyState* e = c->empty;
+  if (e && (e->m != m || e->ncol != ncol || e->nrhs != c->nrhs)) {
+    ps::empty_release(c);
+    e = nullptr;
+  }
+  if (!e) {
+    e = c->empty = new ps::EmptyState();
+    e->m = m;
+    e->ncol = ncol;
+    e->nrhs = c->nrhs;
+    const size_t R = (size_t)c->nrhs;
+    PS_TRY_CUDA(ps::dev_malloc(&e->d_A, R * m * ncol * sizeof(double2)));
+    PS_TRY_CUDA(ps::dev_malloc(&e->d_f, R * m * sizeof(double2)));
+    PS_TRY_CUDA(ps::dev_malloc(&e->d_cs, R * ncol * sizeof(double)));
+    PS_TRY_CUDA(ps::dev_malloc(&e->d_s, R * ncol * sizeof(double)));
+    PS_TRY_CUDA(cudaMemset(e->d_s, 0, R * ncol * sizeof(double)));
+  }
+  std::vector<double2> cm((size_t)m * ncol);       // row-major host -> column-major device
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < ncol; ++j)
+      cm[(size_t)j * m + i] = make_double2(A[2 * ((size_t)i * ncol + j)],
+                                           A[2 * ((size_t)i * ncol + j) + 1]);
+  PS_TRY_CUDA(cudaMemcpy(e->d_A + (size_t)irhs * m * ncol, cm.data(), cm.size() * sizeof(double2),
+                         cudaMemcpyHostToDevice));
+  PS_TRY_CUDA(cudaMemcpy(e->d_f + (size_t)irhs * m, f, (size_t)m * sizeof(double2),
+                         cudaMemcpyHostToDevice));
+  PS_TRY_CUDA(cudaMemcpy(e->d_cs + (size_t)irhs * ncol, col_scale, (size_t)ncol * sizeof(double),
+                         cudaMemcpyHostToDevice));
+  return PS_OK;
+}
+
+int ps_empty_residual(ps_ctx* h, const void* x, const void* g, double* out, void* stream) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = ps::C(h);
+  ps::EmptyState* e = c->empty;
+  if (!e || !e->d_A) return fail(c, PS_ERR_STATE, "ps_empty_residual: no empty-grating matrix "
+                                                   "(ps_setup_empty or ps_set_empty_system)");
+  if (!x || !out) return fail(c, PS_ERR_ARG, "ps_empty_residual: null pointer");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, PS_ERR_CUDA, "cudaSetDevice");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  double2* res = nullptr;
+  PS_TRY_CUDA(ps::dev_malloc(&res, (size_t)e->nrhs * e->m * sizeof(double2)));
+  ps::empty_residual_kernel<<<dim3((e->m + 127) / 128, e->nrhs), 128, 0, st>>>(
+      e->d_A, e->d_f, e->d_cs, reinterpret_cast<const double2*>(x),
+      reinterpret_cast<const double2*>(g), e->m, e->ncol, c->nrow_c, res);
+  ps::residual_norms<<<e->nrhs, 256, 0, st>>>(res, e->d_f, e->m, out);
+  c->launches += 2;
+  const cudaError_t err = cudaGetLastError();
+  cudaStreamSynchronize(st);
+  ps::dev_free(res);
+  if (err != cudaSuccess) return fail(c, PS_ERR_CUDA, std::string("ps_empty_residual: ") +
+                                                        cudaGetErrorString(err));
   return PS_OK;
 }
 

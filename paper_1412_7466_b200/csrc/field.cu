@@ -26,12 +26,17 @@ namespace {
 
 constexpr int kWarps = 4;
 
-template <int P, int RC>
+// GRAD: also the derivative along the unit vector nrm[pt] of the point,
+//   d_n (H_n e^{i n phi}) = (k/2) [(nx + i ny) t_{n-1} - (nx - i ny) t_{n+1}]
+// ((d_x +- i d_y) identities of the outgoing waves, sf:128-154 restated), so
+// per point A = sum_n beta_n t_{n-1} and B = sum_n beta_n t_{n+1} are
+// accumulated over the source images and combined once at the end.
+template <int P, int RC, bool GRAD>
 __global__ void __launch_bounds__(kWarps * 32) particle_field_kernel(
     const double* __restrict__ centers, const double2* __restrict__ beta,
-    const double2* __restrict__ bpow, int np_stride, const double* __restrict__ pts, int npts,
-    int M, int copies, double period, double k2, int r0, int nrhs, int nsplit,
-    double2* __restrict__ part) {
+    const double2* __restrict__ bpow, int np_stride, const double* __restrict__ pts,
+    const double* __restrict__ nrm, int npts, int M, int copies, double period, double k2,
+    int r0, int nrhs, int nsplit, double2* __restrict__ part, double2* __restrict__ part_dn) {
   constexpr int L = 2 * P + 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pt = blockIdx.x * 32 + lane;
@@ -41,9 +46,11 @@ __global__ void __launch_bounds__(kWarps * 32) particle_field_kernel(
   const long long nimg = (long long)M * ncp;
   const int split = blockIdx.y * kWarps + warp, nspl = nsplit * kWarps;
   const long long g0 = nimg * split / nspl, g1 = nimg * (split + 1) / nspl;
-  double2 acc[RC];
+  double2 acc[RC], accA[GRAD ? RC : 1], accB[GRAD ? RC : 1];
 #pragma unroll
   for (int r = 0; r < RC; ++r) acc[r] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int r = 0; r < (GRAD ? RC : 1); ++r) accA[r] = accB[r] = make_double2(0.0, 0.0);
   for (long long g = g0; g < g1; ++g) {
     const int j = (int)(g / ncp), li = (int)(g % ncp);
     const int l = li - copies;
@@ -64,17 +71,23 @@ __global__ void __launch_bounds__(kWarps * 32) particle_field_kernel(
       const double2 b = bpow[(size_t)min(r0 + r, nrhs - 1) * np_stride + 1 + li];
       w[r] = b;
     }
-    hankel_symbols<P>(z, dx * inv, dy * inv, N, [&](int nu, double re, double im) {
-      if (nu < -P || nu > P) return;
+    // (bloch^l beta_r[n]) t into a
+    auto fold = [&](int r, int n, double re, double im, double2& a) {
+      const double2 bv = __ldg(bj + (size_t)(r0 + r) * M * L + (n + P));
+      const double br = fma(w[r].x, bv.x, -w[r].y * bv.y), bi = fma(w[r].x, bv.y, w[r].y * bv.x);
+      a.x = fma(br, re, fma(-bi, im, a.x));
+      a.y = fma(br, im, fma(bi, re, a.y));
+    };
+    hankel_symbols<GRAD ? P + 1 : P>(z, dx * inv, dy * inv, N, [&](int nu, double re, double im) {
       if (!live) return;
 #pragma unroll
       for (int r = 0; r < RC; ++r) {
         if (r0 + r >= nrhs) break;
-        const double2 bv = __ldg(bj + (size_t)(r0 + r) * M * L + (nu + P));
-        // (bloch^l beta) t
-        const double br = fma(w[r].x, bv.x, -w[r].y * bv.y), bi = fma(w[r].x, bv.y, w[r].y * bv.x);
-        acc[r].x = fma(br, re, fma(-bi, im, acc[r].x));
-        acc[r].y = fma(br, im, fma(bi, re, acc[r].y));
+        if (nu >= -P && nu <= P) fold(r, nu, re, im, acc[r]);
+        if (GRAD) {
+          if (nu + 1 >= -P && nu + 1 <= P) fold(r, nu + 1, re, im, accA[GRAD ? r : 0]);  // t_{n-1}
+          if (nu - 1 >= -P && nu - 1 <= P) fold(r, nu - 1, re, im, accB[GRAD ? r : 0]);  // t_{n+1}
+        }
       }
     });
   }
@@ -82,6 +95,18 @@ __global__ void __launch_bounds__(kWarps * 32) particle_field_kernel(
 #pragma unroll
   for (int r = 0; r < RC; ++r)
     if (r0 + r < nrhs) part[((size_t)split * nrhs + r0 + r) * npts + pt] = acc[r];
+  if (GRAD) {
+    const double nx = nrm[2 * pt], ny = nrm[2 * pt + 1], hk = 0.5 * k2;
+#pragma unroll
+    for (int r = 0; r < RC; ++r) {
+      if (r0 + r >= nrhs) break;
+      const double2 A = accA[GRAD ? r : 0], B = accB[GRAD ? r : 0];
+      // (k/2) [(nx + i ny) A - (nx - i ny) B]
+      const double2 d = make_double2(hk * (nx * (A.x - B.x) - ny * (A.y + B.y)),
+                                     hk * (nx * (A.y - B.y) + ny * (A.x + B.x)));
+      part_dn[((size_t)split * nrhs + r0 + r) * npts + pt] = d;
+    }
+  }
 }
 
 __global__ void sum_splits_field(const double2* __restrict__ part, int nspl, int nrhs, int npts,
@@ -97,9 +122,9 @@ __global__ void sum_splits_field(const double2* __restrict__ part, int nspl, int
   out[i] = s;
 }
 
-template <int P, int RC>
-int launch_f(Ctx* c, const double2* beta, const double* pts, int npts, double2* out,
-             cudaStream_t st) {
+template <int P, int RC, bool GRAD>
+int launch_f(Ctx* c, const double2* beta, const double* pts, const double* nrm, int npts,
+             double2* out, double2* out_dn, cudaStream_t st) {
   const int bx = (npts + 31) / 32;
   // fill about two waves of 4-warp CTAs with source splits
   int ny = (2 * c->sm_count * 4 + bx - 1) / bx;
@@ -109,12 +134,13 @@ int launch_f(Ctx* c, const double2* beta, const double* pts, int npts, double2* 
   const int nspl = ny * kWarps;
   const size_t need = (size_t)nspl * c->nrhs * npts;
   double2* part = nullptr;
-  PS_CUDA_TRY(c, ps::dev_malloc(&part, need * sizeof(double2)));
+  PS_CUDA_TRY(c, ps::dev_malloc(&part, (GRAD ? 2 : 1) * need * sizeof(double2)));
+  double2* part_dn = GRAD ? part + need : nullptr;
   const int np_stride = 2 * c->copies + 3;
   for (int r0 = 0; r0 < c->nrhs; r0 += RC) {
-    particle_field_kernel<P, RC><<<dim3(bx, ny), kWarps * 32, 0, st>>>(
-        c->d_centers, beta, c->d_blochpow, np_stride, pts, npts, c->M, c->copies, c->period,
-        c->k2, r0, c->nrhs, ny, part);
+    particle_field_kernel<P, RC, GRAD><<<dim3(bx, ny), kWarps * 32, 0, st>>>(
+        c->d_centers, beta, c->d_blochpow, np_stride, pts, nrm, npts, c->M, c->copies, c->period,
+        c->k2, r0, c->nrhs, ny, part, part_dn);
     PS_CUDA_TRY(c, cudaGetLastError());
     c->launches += 1;
   }
@@ -122,28 +148,36 @@ int launch_f(Ctx* c, const double2* beta, const double* pts, int npts, double2* 
   sum_splits_field<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nspl, c->nrhs, npts, out);
   PS_CUDA_TRY(c, cudaGetLastError());
   c->launches += 1;
+  if (GRAD) {
+    sum_splits_field<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part_dn, nspl, c->nrhs, npts,
+                                                                  out_dn);
+    PS_CUDA_TRY(c, cudaGetLastError());
+    c->launches += 1;
+  }
   PS_CUDA_TRY(c, cudaStreamSynchronize(st));
   ps::dev_free(part);
   return PS_OK;
 }
 
-template <int P>
-int launch_rc(Ctx* c, const double2* beta, const double* pts, int npts, double2* out,
-              cudaStream_t st) {
-  if (c->nrhs >= 4) return launch_f<P, 4>(c, beta, pts, npts, out, st);
-  if (c->nrhs >= 2) return launch_f<P, 2>(c, beta, pts, npts, out, st);
-  return launch_f<P, 1>(c, beta, pts, npts, out, st);
+template <int P, bool GRAD>
+int launch_rc(Ctx* c, const double2* beta, const double* pts, const double* nrm, int npts,
+              double2* out, double2* out_dn, cudaStream_t st) {
+  if (c->nrhs >= 4) return launch_f<P, 4, GRAD>(c, beta, pts, nrm, npts, out, out_dn, st);
+  if (c->nrhs >= 2) return launch_f<P, 2, GRAD>(c, beta, pts, nrm, npts, out, out_dn, st);
+  return launch_f<P, 1, GRAD>(c, beta, pts, nrm, npts, out, out_dn, st);
 }
 
 }  // namespace
 
-int particle_field(Ctx* c, const double2* beta, const double* pts, int npts, double2* out,
-                   cudaStream_t st) {
+int particle_field(Ctx* c, const double2* beta, const double* pts, const double* nrm, int npts,
+                   double2* out, double2* out_dn, cudaStream_t st) {
   if (npts <= 0) return PS_OK;
+  const bool grad = nrm && out_dn;
   switch (c->p) {
-#define PS_CASE(P) \
-  case P:          \
-    return launch_rc<P>(c, beta, pts, npts, out, st);
+#define PS_CASE(P)                                                              \
+  case P:                                                                       \
+    return grad ? launch_rc<P, true>(c, beta, pts, nrm, npts, out, out_dn, st) \
+                : launch_rc<P, false>(c, beta, pts, nullptr, npts, out, nullptr, st);
     PS_M2L_ORDERS(PS_CASE)
 #undef PS_CASE
     default:
@@ -172,24 +206,31 @@ struct LayerArgs {
   const double2* x;        // [nrhs][ncol]
   const double* pts;       // [npts][2]
   const int* layer;        // [npts]: 1, 2, 3 (anything else -> 0)
+  const double* nrm;       // [npts][2] derivative directions (GRAD)
   const double* g1;        // [n1][5] x y nx ny aw
   const double* g2;        // [n2][5]
   const double2* bpow;     // [nrhs][2P+3]
   const double* inc;       // [nrhs][2]
   double2* out;            // [nrhs][npts]
-  int npts, ncol, n1, n2, Q, copies, np;
+  double2* out_dn;         // [nrhs][npts] (GRAD)
+  int npts, ncol, n1, n2, Q, copies, np, incident;
   int c_mu1, c_s1, c_mu2, c_s2, c_a2, c_a1, c_a3;
   double k1, k2, k3, period;
   double c1x, c1y, c2x, c2y, c3x, c3y;
 };
 
 // sum_l alpha^l sum_j aw_j [S_k(x, y_j + l d) sigma_j + D_k(x, y_j + l d) mu_j]
-__device__ double2 layer_potential(const LayerArgs& a, const double* cv, int n, const double2* mu,
-                                   const double2* sg, double k, const double2* bp, double px,
-                                   double py) {
-  double2 tot = make_double2(0.0, 0.0);
+// and (GRAD) its derivative along e at x (layerpot.py:67-91: the N / T
+// kernels of the single / double layer with the target normal e):
+//   d_e S = -(i/4) k H1 (u.e)/r,
+//   d_e D = (i/4) k [k H0 P - 2 H1 P / r + H1 (e.n_y) / r],  P = (u.e)(u.n_y)/r^2
+template <bool GRAD>
+__device__ void layer_potential(const LayerArgs& a, const double* cv, int n, const double2* mu,
+                                const double2* sg, double k, const double2* bp, double px,
+                                double py, double ex, double ey, double2* val, double2* dn) {
+  double2 tot = make_double2(0.0, 0.0), totd = make_double2(0.0, 0.0);
   for (int l = -a.copies; l <= a.copies; ++l) {
-    double2 acc = make_double2(0.0, 0.0);
+    double2 acc = make_double2(0.0, 0.0), accd = make_double2(0.0, 0.0);
     for (int j = 0; j < n; ++j) {
       const double* y = cv + (size_t)j * 5;
       const double u0 = px - (y[0] + l * a.period), u1 = py - y[1];
@@ -204,73 +245,141 @@ __device__ double2 layer_potential(const LayerArgs& a, const double* cv, int n, 
       const double aw = y[4];
       acc.x += aw * (sv.x * s.x - sv.y * s.y + dv.x * m.x - dv.y * m.y);
       acc.y += aw * (sv.x * s.y + sv.y * s.x + dv.x * m.y + dv.y * m.x);
+      if (GRAD) {
+        const double ude = (u0 * ex + u1 * ey) / r;          // (u.e)/r
+        const double en = ex * y[2] + ey * y[3];
+        const double pp = ude * udn;
+        // N: -(i/4) k H1 (u.e)/r
+        const double2 nv = make_double2(0.25 * k * ude * y1, -0.25 * k * ude * j1);
+        // T: (i/4) k [k H0 P + H1 (e.n - 2P) / r]
+        const double cr = k * pp, ch = (en - 2.0 * pp) / r;
+        const double hr = cr * j0 + ch * j1, hi = cr * y0 + ch * y1;   // k H0 P + H1 (..)/r
+        const double2 tv = make_double2(-0.25 * k * hi, 0.25 * k * hr);
+        accd.x += aw * (nv.x * s.x - nv.y * s.y + tv.x * m.x - tv.y * m.y);
+        accd.y += aw * (nv.x * s.y + nv.y * s.x + tv.x * m.y + tv.y * m.x);
+      }
     }
     const double2 w = bp[l + a.copies + 1];
     const double2 t = fcmul(w, acc);
     tot.x += t.x;
     tot.y += t.y;
+    if (GRAD) {
+      const double2 td = fcmul(w, accd);
+      totd.x += td.x;
+      totd.y += td.y;
+    }
   }
-  return tot;
+  val->x += tot.x;
+  val->y += tot.y;
+  if (GRAD) {
+    dn->x += totd.x;
+    dn->y += totd.y;
+  }
 }
 
-// sum_{n=-Q}^{Q} a_n J_n(k r) e^{i n theta} about (cx, cy)
-__device__ double2 regular_sum(const double2* an, int Q, double k, double cx, double cy, double px,
-                               double py) {
+// sum_{n=-Q}^{Q} a_n W_n, W_n = J_n(k r) e^{i n theta} about (cx, cy), and
+// (GRAD) d_e of it: d_e W_n = (k/2) [(ex + i ey) W_{n-1} - (ex - i ey) W_{n+1}]
+// (the regular_wave_block gradients, sf:86-125, restated)
+template <bool GRAD>
+__device__ void regular_sum(const double2* an, int Q, double k, double cx, double cy, double px,
+                            double py, double ex, double ey, double2* val, double2* dn) {
   const double dx = px - cx, dy = py - cy;
   const double r = hypot(dx, dy);
-  if (r == 0.0) return an[Q];
-  double J[80];
-  double inv, y0, y1;
-  bessel_jy_sweep(k * r, Q, [&](int nu, double v) { J[nu] = v; }, &inv, &y0, &y1);
-  const double c = dx / r, s = dy / r;
+  double J[81];
+  double inv = 1.0, y0, y1;
+  const int nmax = GRAD ? Q + 1 : Q;
+  if (r == 0.0) {
+    J[0] = 1.0;
+    for (int n = 1; n <= nmax; ++n) J[n] = 0.0;
+  } else {
+    bessel_jy_sweep(k * r, nmax, [&](int nu, double v) { J[nu] = v; }, &inv, &y0, &y1);
+  }
+  const double c = r > 0.0 ? dx / r : 1.0, s = r > 0.0 ? dy / r : 0.0;
+  // W_n and W_{-n} for n = 0..nmax, folded on the fly
   double2 acc = make_double2(an[Q].x * J[0] * inv, an[Q].y * J[0] * inv);
+  double2 A = make_double2(0.0, 0.0), B = make_double2(0.0, 0.0);  // sum a_n W_{n-1}, sum a_n W_{n+1}
+  auto coef = [&](int n) { return (n >= -Q && n <= Q) ? an[Q + n] : make_double2(0.0, 0.0); };
+  auto add = [&](double2& t, double2 a, double wr, double wi) {
+    t.x += a.x * wr - a.y * wi;
+    t.y += a.x * wi + a.y * wr;
+  };
+  if (GRAD) {
+    const double w0 = J[0] * inv;
+    add(A, coef(1), w0, 0.0);     // n = 1: W_0
+    add(B, coef(-1), w0, 0.0);    // n = -1: W_0
+  }
   double pr = 1.0, pi = 0.0;   // e^{i n theta}
-  for (int n = 1; n <= Q; ++n) {
+  for (int n = 1; n <= nmax; ++n) {
     const double qr = pr * c - pi * s, qi = pr * s + pi * c;
     pr = qr;
     pi = qi;
     const double jn = J[n] * inv;
     const double jm = (n & 1) ? -jn : jn;               // J_{-n} = (-1)^n J_n
-    const double2 ap = an[Q + n], am = an[Q - n];
-    // a_n J_n e^{in th} + a_{-n} J_{-n} e^{-in th}
-    acc.x += jn * (ap.x * pr - ap.y * pi) + jm * (am.x * pr + am.y * pi);
-    acc.y += jn * (ap.x * pi + ap.y * pr) + jm * (am.y * pr - am.x * pi);
+    const double wpr = jn * pr, wpi = jn * pi;          // W_n
+    const double wmr = jm * pr, wmi = -jm * pi;         // W_{-n}
+    if (n <= Q) {
+      add(acc, an[Q + n], wpr, wpi);
+      add(acc, an[Q - n], wmr, wmi);
+    }
+    if (GRAD) {
+      add(A, coef(n + 1), wpr, wpi);       // a_{n+1} W_n
+      add(A, coef(-n + 1), wmr, wmi);      // a_{1-n} W_{-n}
+      add(B, coef(n - 1), wpr, wpi);       // a_{n-1} W_n
+      add(B, coef(-n - 1), wmr, wmi);      // a_{-n-1} W_{-n}
+    }
   }
-  return acc;
+  val->x += acc.x;
+  val->y += acc.y;
+  if (GRAD) {
+    const double hk = 0.5 * k;
+    dn->x += hk * (ex * (A.x - B.x) - ey * (A.y + B.y));
+    dn->y += hk * (ex * (A.y - B.y) + ey * (A.x + B.x));
+  }
 }
 
+template <bool GRAD>
 __global__ void __launch_bounds__(128) layer_field_kernel(LayerArgs a) {
   const int pt = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y;
   if (pt >= a.npts) return;
   const int ly = a.layer[pt];
-  double2 u = make_double2(0.0, 0.0);
+  double2 u = make_double2(0.0, 0.0), ud = make_double2(0.0, 0.0);
   const double px = a.pts[2 * pt], py = a.pts[2 * pt + 1];
+  const double ex = GRAD ? a.nrm[2 * pt] : 0.0, ey = GRAD ? a.nrm[2 * pt + 1] : 0.0;
   const double2* x = a.x + (size_t)r * a.ncol;
   const double2* bp = a.bpow + (size_t)r * a.np;
   if (ly == 1) {
-    u = layer_potential(a, a.g1, a.n1, x + a.c_mu1, x + a.c_s1, a.k1, bp, px, py);
-    const double2 e = regular_sum(x + a.c_a1, a.Q, a.k1, a.c1x, a.c1y, px, py);
-    double sn, cs;
-    sincos(px * a.inc[2 * r] + py * a.inc[2 * r + 1], &sn, &cs);
-    u = make_double2(u.x + e.x + cs, u.y + e.y + sn);
+    layer_potential<GRAD>(a, a.g1, a.n1, x + a.c_mu1, x + a.c_s1, a.k1, bp, px, py, ex, ey, &u, &ud);
+    regular_sum<GRAD>(x + a.c_a1, a.Q, a.k1, a.c1x, a.c1y, px, py, ex, ey, &u, &ud);
+    if (a.incident) {
+      const double kx = a.inc[2 * r], ky = a.inc[2 * r + 1];
+      double sn, cs;
+      sincos(px * kx + py * ky, &sn, &cs);
+      u.x += cs;
+      u.y += sn;
+      if (GRAD) {                       // i (k . e) e^{i k.x}
+        const double ke = kx * ex + ky * ey;
+        ud.x -= ke * sn;
+        ud.y += ke * cs;
+      }
+    }
   } else if (ly == 2) {
-    const double2 u1 = layer_potential(a, a.g1, a.n1, x + a.c_mu1, x + a.c_s1, a.k2, bp, px, py);
-    const double2 u2 = layer_potential(a, a.g2, a.n2, x + a.c_mu2, x + a.c_s2, a.k2, bp, px, py);
-    const double2 e = regular_sum(x + a.c_a2, a.Q, a.k2, a.c2x, a.c2y, px, py);
-    u = make_double2(u1.x + u2.x + e.x, u1.y + u2.y + e.y);
+    layer_potential<GRAD>(a, a.g1, a.n1, x + a.c_mu1, x + a.c_s1, a.k2, bp, px, py, ex, ey, &u, &ud);
+    layer_potential<GRAD>(a, a.g2, a.n2, x + a.c_mu2, x + a.c_s2, a.k2, bp, px, py, ex, ey, &u, &ud);
+    regular_sum<GRAD>(x + a.c_a2, a.Q, a.k2, a.c2x, a.c2y, px, py, ex, ey, &u, &ud);
   } else if (ly == 3) {
-    u = layer_potential(a, a.g2, a.n2, x + a.c_mu2, x + a.c_s2, a.k3, bp, px, py);
-    const double2 e = regular_sum(x + a.c_a3, a.Q, a.k3, a.c3x, a.c3y, px, py);
-    u = make_double2(u.x + e.x, u.y + e.y);
+    layer_potential<GRAD>(a, a.g2, a.n2, x + a.c_mu2, x + a.c_s2, a.k3, bp, px, py, ex, ey, &u, &ud);
+    regular_sum<GRAD>(x + a.c_a3, a.Q, a.k3, a.c3x, a.c3y, px, py, ex, ey, &u, &ud);
   }
   a.out[(size_t)r * a.npts + pt] = u;
+  if (GRAD) a.out_dn[(size_t)r * a.npts + pt] = ud;
 }
 
 }  // namespace
 
-int layer_field(Ctx* c, const double2* x, const double* pts, const int* layer, int npts,
-                double2* out, cudaStream_t st) {
+int layer_field(Ctx* c, const double2* x, const double* pts, const int* layer,
+                const double* nrm, int npts, int incident, double2* out, double2* out_dn,
+                cudaStream_t st) {
   if (!c->have_layers || !c->have_field || c->nfield == 0) {
     c->err = "ps_layer_field: no empty-grating setup with field data (ps_setup_empty, or "
              "ps_set_pinv + ps_set_field_params)";
@@ -286,6 +395,9 @@ int layer_field(Ctx* c, const double2* x, const double* pts, const int* layer, i
   a.x = x;
   a.pts = pts;
   a.layer = layer;
+  a.nrm = nrm;
+  a.out_dn = out_dn;
+  a.incident = incident;
   a.g1 = c->d_g1;
   a.g2 = c->d_g2;
   a.bpow = c->d_blochpow;
@@ -315,7 +427,10 @@ int layer_field(Ctx* c, const double2* x, const double* pts, const int* layer, i
   a.c2y = c->x2[1];
   a.c3x = c->f_c3[0];
   a.c3y = c->f_c3[1];
-  layer_field_kernel<<<dim3((npts + 127) / 128, c->nrhs), 128, 0, st>>>(a);
+  if (nrm && out_dn)
+    layer_field_kernel<true><<<dim3((npts + 127) / 128, c->nrhs), 128, 0, st>>>(a);
+  else
+    layer_field_kernel<false><<<dim3((npts + 127) / 128, c->nrhs), 128, 0, st>>>(a);
   PS_CUDA_TRY(c, cudaGetLastError());
   c->launches += 1;
   return PS_OK;

@@ -79,6 +79,13 @@ class Engine:
         self.copies = int(copies)
         self.t_range = (0, self.M)
 
+    def check_overlap(self, radius: float) -> float:
+        """ParticleSet.min_gap (geometry.py:131-144) on the device; raises
+        DomainError for overlapping disks."""
+        gap = ctypes.c_double()
+        self._check(self.lib.ps_check_overlap(self.ctx, float(radius), ctypes.byref(gap)))
+        return gap.value
+
     def set_target_range(self, t0: int, t1: int):
         self._check(self.lib.ps_set_target_range(self.ctx, int(t0), int(t1)))
         self.t_range = (int(t0), int(t1))
@@ -261,6 +268,23 @@ class Engine:
                                                _stream(self.device)))
         return out
 
+    def particle_field_grad(self, beta: torch.Tensor, points, dirs):
+        """([nrhs][npts] values, [nrhs][npts] derivatives along dirs) of the
+        particle multipole field (ps_particle_field_grad)."""
+        pts = torch.as_tensor(np.ascontiguousarray(np.asarray(points, dtype=float).reshape(-1, 2)),
+                              device=self.device)
+        dr = torch.as_tensor(np.ascontiguousarray(np.asarray(dirs, dtype=float).reshape(-1, 2)),
+                             device=self.device)
+        out = torch.empty((self.nrhs, pts.shape[0]), dtype=torch.complex128, device=self.device)
+        dn = torch.empty_like(out)
+        if pts.shape[0] == 0:
+            return out, dn
+        b = self._dev(beta, (self.nrhs, self.M, self.L))
+        self._check(self.lib.ps_particle_field_grad(self.ctx, b, int(pts.shape[0]),
+                                                    self._vp(pts), self._vp(dr), self._vp(out),
+                                                    self._vp(dn), _stream(self.device)))
+        return out, dn
+
     def schur_finish(self, v_own: torch.Tensor, a_own: torch.Tensor, g: torch.Tensor | None,
                      out: torch.Tensor | None = None) -> torch.Tensor:
         """y_own = v_own - S (a_own - B A^+ g) (one RHS)."""
@@ -344,6 +368,44 @@ class Engine:
                                             int(pts.shape[0]), ctypes.c_void_p(pts.data_ptr()),
                                             ctypes.c_void_p(lay.data_ptr()),
                                             ctypes.c_void_p(out.data_ptr()), _stream(self.device)))
+        return out
+
+    def layer_field_grad(self, x: torch.Tensor, points, layer, dirs, incident: bool = True):
+        """(values, derivatives along dirs) [nrhs][npts] of the empty-grating
+        layer field (ps_layer_field_grad); incident=False is
+        eval_empty_field(total=False)."""
+        pts = torch.as_tensor(np.ascontiguousarray(np.asarray(points, dtype=float).reshape(-1, 2)),
+                              device=self.device)
+        dr = torch.as_tensor(np.ascontiguousarray(np.asarray(dirs, dtype=float).reshape(-1, 2)),
+                             device=self.device)
+        lay = torch.as_tensor(np.ascontiguousarray(np.asarray(layer, dtype=np.int32).ravel()),
+                              device=self.device)
+        out = torch.empty((self.nrhs, pts.shape[0]), dtype=torch.complex128, device=self.device)
+        dn = torch.empty_like(out)
+        if pts.shape[0] == 0:
+            return out, dn
+        xp = x.to(device=self.device, dtype=torch.complex128).contiguous()
+        self._check(self.lib.ps_layer_field_grad(self.ctx, self._vp(xp), int(pts.shape[0]),
+                                                 self._vp(pts), self._vp(lay), self._vp(dr),
+                                                 1 if incident else 0, self._vp(out),
+                                                 self._vp(dn), _stream(self.device)))
+        return out, dn
+
+    def set_empty_system(self, irhs: int, system):
+        """Upload one RHS's column-scaled empty-grating matrix, f and column
+        scaling (ps_set_empty_system) for the coupled residual."""
+        A = _c128(system.matrix)
+        f = _c128(system.rhs)
+        cs = _f64(system.col_scale)
+        self._check(self.lib.ps_set_empty_system(self.ctx, int(irhs), A.shape[0], A.shape[1],
+                                                 _ptr(A), _ptr(f), _ptr(cs)))
+
+    def empty_residual(self, x: torch.Tensor, g: torch.Tensor | None):
+        """[nrhs][2] (||A x/cs + C beta - f||^2, ||f||^2) on the device."""
+        out = torch.empty((self.nrhs, 2), dtype=torch.float64, device=self.device)
+        gp = None if g is None else self._vp(g.contiguous())
+        self._check(self.lib.ps_empty_residual(self.ctx, self._vp(x.contiguous()), gp,
+                                               self._vp(out), _stream(self.device)))
         return out
 
     def gmres(self, rhs: torch.Tensor, tol: float = 1e-10, maxit: int = 150):

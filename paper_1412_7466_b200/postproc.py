@@ -63,6 +63,121 @@ def empty_field(op, beta, points, layer) -> np.ndarray:
     return eng.layer_field(x, points, layer).cpu().numpy()
 
 
+def _beta_dev(eng, beta):
+    import torch
+    b = torch.as_tensor(np.asarray(beta, dtype=complex)) if not isinstance(beta, torch.Tensor) \
+        else beta
+    return b.to(device=eng.device, dtype=torch.complex128).reshape(eng.nrhs, eng.M, eng.L).contiguous()
+
+
+def _c_rows(eng, b):
+    """C beta on the device ([nrhs][nrow_c]; zero without inclusions)."""
+    import torch
+    if eng.M == 0:
+        return torch.zeros((eng.nrhs, eng.nrow_c), dtype=torch.complex128, device=eng.device)
+    return eng.apply_C(b)
+
+
+def coupled_residual(op, beta, x_full=None) -> list:
+    """Relative residual of the full coupled system (PAPER Eq.
+    finalsys) per RHS, measured against ||f||:
+
+        r_A = A x + C beta - f          (empty-grating rows; eg:289-290's residual)
+        r_S = beta - S (T beta + B_phys x) = K beta - rhs   (particle rows)
+
+    with x = A^+ (f - C beta) (all unknowns).  Everything runs on the device:
+    ps_apply_C, ps_recover_full, ps_empty_residual, one Schur matvec and
+    ps_schur_rhs.  Returns dicts (relative, empty_rows, particle_rows)."""
+    import torch
+    eng = op.eng
+    b = _beta_dev(eng, beta)
+    if not getattr(op, "_empty_on_device", False):
+        if not op.device_setup:
+            for r, s in enumerate(op.systems):
+                eng.set_empty_system(r, s)
+        op._empty_on_device = True
+    g = _c_rows(eng, b)
+    x = eng.recover_full(g) if x_full is None else x_full
+    ea = eng.empty_residual(x, g).cpu().numpy()
+    if eng.M > 0:
+        rs = (eng.apply_schur(b) - eng.schur_rhs()).reshape(eng.nrhs, -1)
+        ns = (rs.real ** 2 + rs.imag ** 2).sum(dim=1).cpu().numpy()
+    else:
+        ns = np.zeros(eng.nrhs)
+    out = []
+    for r in range(eng.nrhs):
+        fn = np.sqrt(ea[r, 1])
+        out.append(dict(relative=float(np.sqrt(ea[r, 0] + ns[r]) / fn),
+                        empty_rows=float(np.sqrt(ea[r, 0]) / fn),
+                        particle_rows=float(np.sqrt(ns[r]) / fn)))
+    return out
+
+
+def _gauss_legendre(n: int, a: float, b: float):
+    """quadrature.gauss_legendre (quadrature.py:31-37)."""
+    x, w = np.polynomial.legendre.leggauss(n)
+    half = 0.5 * (b - a)
+    return a + half * (x + 1.0), half * w
+
+
+def wall_check_points(cfg, n_fresh: int = 31):
+    """Fresh probe points of wall_discrepancy_residual (eg:408-420): per wall
+    L1, L2, L3 of the unit cell, n_fresh Gauss-Legendre ordinates between
+    its extreme nodes inset by 6 d / N_Gamma, at x = -d/2 then at x = +d/2;
+    and their layer (classify_layer, eg:341-349).  Host geometry."""
+    from .empty_setup import unit_cell
+    d = cfg.period
+    cell = unit_cell(cfg)
+    inset = 6.0 * d / cfg.interface_nodes
+    pts = []
+    for wall in cell.walls:
+        ylo, yhi = float(np.min(wall[:, 1])), float(np.max(wall[:, 1]))
+        ys, _ = _gauss_legendre(n_fresh, ylo + inset, yhi - inset)
+        left = np.stack([np.full(n_fresh, -0.5 * d), ys], axis=-1)
+        pts.append(np.vstack([left, left + [d, 0.0]]))
+    pts = np.vstack(pts)
+    top = cfg.interface_top.height(pts[:, 0], d)
+    bot = cfg.interface_bottom.height(pts[:, 0], d)
+    layer = np.full(pts.shape[0], 2, dtype=np.int32)
+    layer[pts[:, 1] > top] = 1
+    layer[pts[:, 1] < bot] = 3
+    return pts, layer
+
+
+def wall_discrepancy_residual(op, beta, n_fresh: int = 31, x_full=None) -> list:
+    """empty_grating.wall_discrepancy_residual (eg:396-433) of the COUPLED
+    solution, per RHS: max |alpha u(L) - u(R)| over fresh Gauss-Legendre
+    points of the three walls (inset 6 d / N_Gamma from the junctions),
+    values and x-derivatives, with u = the empty-grating representation
+    (eval_empty_field total=False, x = A^+ (f - C beta)) plus the particles'
+    phased multipole field in layer 2 (the extra_field the reference checker
+    takes for a coupled solution).  All field sums on the device
+    (ps_layer_field_grad, ps_particle_field_grad)."""
+    eng = op.eng
+    b = _beta_dev(eng, beta)
+    pts, layer = wall_check_points(op.config, n_fresh)
+    nrm = np.tile([1.0, 0.0], (pts.shape[0], 1))
+    x = eng.recover_full(_c_rows(eng, b)) if x_full is None else x_full
+    val, dn = eng.layer_field_grad(x, pts, layer, nrm, incident=False)
+    val, dn = val.cpu().numpy(), dn.cpu().numpy()
+    mid = layer == 2
+    if np.any(mid) and eng.M > 0:
+        pv, pd = eng.particle_field_grad(b, pts[mid], nrm[mid])
+        val[:, mid] += pv.cpu().numpy()
+        dn[:, mid] += pd.cpu().numpy()
+    out = []
+    for r, s in enumerate(op.systems):
+        alpha = s.config.bloch_phase
+        worst = 0.0
+        for w in range(3):
+            sl = slice(2 * n_fresh * w, 2 * n_fresh * (w + 1))
+            for arr in (val[r, sl], dn[r, sl]):
+                disc = alpha * arr[:n_fresh] - arr[n_fresh:]
+                worst = max(worst, float(np.max(np.abs(disc))))
+        out.append(worst)
+    return out
+
+
 def _interface_heights(config, system, x):
     if hasattr(config, "interface_top"):                      # reference ProblemConfig
         return (config.interface_top.height(x, config.period),

@@ -28,7 +28,10 @@ class SchurOperator:
                  rot=None, device=None, target_range=None, coupled: bool = True,
                  engine: Engine | None = None, dense_gb: float = 40.0, group=None,
                  split_setup: bool = False):
-        """``split_setup`` (opt-in, collective): with configs and several
+        """``radius``: the disk radius (builds the diagonal S when ``smat`` is
+        None) or, with a given ``smat``, the enclosing radius; either way the
+        inclusions are checked for overlap on the device.
+        ``split_setup`` (opt-in, collective): with configs and several
         RHS, every rank of ``group`` factorises only its share of the
         per-angle SVDs and the factors are broadcast
         (parallel.setup_empty_split); all ranks of the group must construct
@@ -56,6 +59,10 @@ class SchurOperator:
         eng = self.eng
         self.centers = np.ascontiguousarray(np.asarray(centers, dtype=float).reshape(-1, 2))
         eng.set_geometry(self.centers, p, cfg.k2, cfg.period, cfg.near_field_copies)
+        if radius is not None:
+            # overlapping enclosing disks -> DomainError (
+            # ParticleSet.min_gap semantics, geometry.py:131-144)
+            self.min_gap = eng.check_overlap(radius)
         eng.set_bloch([c.bloch_phase for c in configs])
         eng.set_smatrix(self.smat, rot)
         self.coupled = coupled
@@ -147,8 +154,11 @@ def gmres(op, rhs, tol: float = 1e-10, maxit: int = 150, engine: Engine | None =
     return (x.cpu().numpy() if on_host else x), its, hist
 
 
-@dataclass
+@dataclass(frozen=True)
 class Solution:
+    """beta, the recovered empty-grating unknowns, GMRES
+    iterations and final relative residual, flux error, wall-discrepancy
+    residual (+ the coupled residual of SPEC.md:571).  Immutable."""
     beta: np.ndarray          # [nrhs][M][L]
     c: np.ndarray             # [nrhs][nrb]
     d: np.ndarray             # [nrhs][nrb]
@@ -156,10 +166,15 @@ class Solution:
     history: list
     flux: list = field(default_factory=list)
     timings: dict = field(default_factory=dict)
+    x_empty: np.ndarray | None = None   # [nrhs][ncol] all empty-grating unknowns (eg:154-156)
+    residual: list = field(default_factory=list)          # final GMRES relative residual
+    coupled_residual: list = field(default_factory=list)  # SPEC.md:571 (postproc)
+    wall_residual: list = field(default_factory=list)     # eg:396-433 (postproc)
 
 
 def solve_full(systems, centers, p: int, radius: float | None = None, smat=None, rot=None,
-               tol: float | None = None, maxit: int | None = None, device=None) -> Solution:
+               tol: float | None = None, maxit: int | None = None, device=None,
+               diagnostics: bool = True) -> Solution:
     """beta from GMRES on (I - S T - S B A^+ C) beta = -S B A^+ f,
     then x_empty = A^+ (f - C beta); flux balance per RHS.
 
@@ -193,4 +208,18 @@ def solve_full(systems, centers, p: int, radius: float | None = None, smat=None,
     timings = dict(setup=t1 - t0, solve=t2 - t1)
     if op.device_setup and op.coupled:
         timings["assemble_ms"], timings["svd_ms"] = op.eng.setup_timings()
-    return Solution(beta.cpu().numpy(), c, d, its, hist, flux, timings)
+    extra = {}
+    if diagnostics and op.coupled:
+        # after the timed solve: SPEC.md:534 / 571 diagnostics on the device
+        t3 = time.perf_counter()
+        xf = None
+        if op.eng.lib.ps_full_columns(op.eng.ctx) > 0:
+            bdev = beta if isinstance(beta, torch.Tensor) else torch.as_tensor(beta).to(op.device)
+            xf = op.eng.recover_full(postproc._c_rows(op.eng, bdev.contiguous()))
+            extra["x_empty"] = xf.cpu().numpy()
+            extra["coupled_residual"] = [r["relative"] for r in
+                                         postproc.coupled_residual(op, bdev, xf)]
+            extra["wall_residual"] = postproc.wall_discrepancy_residual(op, bdev, x_full=xf)
+        timings["diagnostics"] = time.perf_counter() - t3
+    res = [h[-1] if h else float("nan") for h in hist]
+    return Solution(beta.cpu().numpy(), c, d, its, hist, flux, timings, residual=res, **extra)

@@ -106,3 +106,16 @@ def test_unit_cell_from_reference_config(refmod, curved):
                  (cm.lid_up, cell.lid_up)):
         assert np.array_equal(a, b)
     assert mine.y0 == conf.y0
+
+
+def test_wall_check_points_match_reference_checker():
+    """postproc.wall_check_points rebuilds the fresh wall probes of
+    empty_grating.wall_discrepancy_residual (eg:408-420) and their layers
+    bit for bit (golden from oracle/make_walls.py)."""
+    import os
+
+    from paper_1412_7466_b200 import grating, postproc
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "walls_cfg1.npz"))
+    pts, layer = postproc.wall_check_points(grating.load_fixture("w10").config)
+    assert np.array_equal(pts, z["pts"])
+    assert np.array_equal(layer, z["layer"])
