@@ -117,6 +117,9 @@ int ps_set_mrhs_variant(ps_ctx* ctx, int variant);
  * other SMs (sms = 0: only the M2L tail is shared); sms < 0 runs them back
  * to back.  Default 2 (best at cfg3). */
 int ps_set_overlap(ps_ctx* ctx, int sms);
+/* Queue order of that SM partitioning: 0 (default) the coupling chain at the
+ * step's fork, 1 behind K1s (K1s' CTAs dispatched first; slower at cfg3). */
+int ps_set_overlap_order(ps_ctx* ctx, int k1_first);
 /* Single-RHS M2L launches (ps_apply_T, ps_apply_T_blocks) use SM count - sms
  * CTAs, leaving SMs free for work the caller overlaps on other streams (the
  * multi-GPU driver runs the coupling chain and its NCCL all-reduce there).
@@ -370,6 +373,10 @@ int ps_profile(ps_ctx* ctx, int enable);
  * (synchronises on the recorded events). */
 int ps_stats(ps_ctx* ctx, long long* launches, double* k1_ms, long long* k1_count);
 int ps_stats_reset(ps_ctx* ctx);
+/* Mean timeline of the SM-partitioned single-RHS Schur steps run with
+ * profiling on (ms from the step's fork): out3 = {K1s end, coupling-chain
+ * end, step end}; *count = steps folded. */
+int ps_timeline(ps_ctx* ctx, double* out3, long long* count);
 
 /* ---- roofline denominator ---------------------------------------------- */
 /* DFMA-chain FP64 throughput of the device (TFLOP/s, 2 flops per FMA). */

@@ -55,12 +55,14 @@ SIGNATURES = {
     "ps_set_k1_variant": (_I, [_P, _I]),
     "ps_set_mrhs_variant": (_I, [_P, _I]),
     "ps_set_overlap": (_I, [_P, _I]),
+    "ps_set_overlap_order": (_I, [_P, _I]),
     "ps_set_k1_reserve": (_I, [_P, _I]),
     "ps_apply_T_blocks": (_I, [_P, _I, _I, _P, _P, _P]),
     "ps_particle_field": (_I, [_P, _P, _I, _P, _P, _P]),
     "ps_schur_finish": (_I, [_P, _P, _P, _P, _P, _P]),
     "ps_stats": (_I, [_P, ctypes.POINTER(ctypes.c_longlong), _DP, ctypes.POINTER(ctypes.c_longlong)]),
     "ps_stats_reset": (_I, [_P]),
+    "ps_timeline": (_I, [_P, _DP, ctypes.POINTER(ctypes.c_longlong)]),
     "ps_setup_empty": (_I, [_P, _P, _P]),
     "ps_empty_shape": (_I, [_P, _IP, _IP]),
     "ps_get_empty": (_I, [_P, _I, _P, _P, _P, _P]),

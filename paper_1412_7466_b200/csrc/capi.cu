@@ -149,7 +149,7 @@ void ps_destroy(ps_ctx* h) {
   ps::empty_release(c);
   if (c->s_hi) cudaStreamDestroy(c->s_hi);
   if (c->s_lo) cudaStreamDestroy(c->s_lo);
-  cudaEvent_t evs[] = {c->ev_fork, c->ev_k1, c->ev_cpl};
+  cudaEvent_t evs[] = {c->ev_fork, c->ev_k1, c->ev_cpl, c->ev_bw};
   for (cudaEvent_t e : evs)
     if (e) cudaEventDestroy(e);
   delete c;
@@ -782,6 +782,12 @@ int ps_set_overlap(ps_ctx* h, int sms) {
   return PS_OK;
 }
 
+int ps_set_overlap_order(ps_ctx* h, int k1_first) {
+  if (!h) return PS_ERR_ARG;
+  C(h)->overlap_k1_first = k1_first ? 1 : 0;
+  return PS_OK;
+}
+
 int ps_coupling_mode(const ps_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->dense : -1; }
 
 int ps_profile(ps_ctx* h, int enable) {
@@ -811,6 +817,28 @@ int ps_stats(ps_ctx* h, long long* launches, double* k1_ms, long long* k1_count)
   return PS_OK;
 }
 
+int ps_timeline(ps_ctx* h, double* out3, long long* count) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  for (auto& t : c->timelines) {
+    PS_CUDA_TRY(c, cudaEventSynchronize(t.end));
+    float a = 0.f, b = 0.f, e = 0.f;
+    PS_CUDA_TRY(c, cudaEventElapsedTime(&a, t.fork, t.k1));
+    PS_CUDA_TRY(c, cudaEventElapsedTime(&b, t.fork, t.chain));
+    PS_CUDA_TRY(c, cudaEventElapsedTime(&e, t.fork, t.end));
+    c->tl_sum[0] += a;
+    c->tl_sum[1] += b;
+    c->tl_sum[2] += e;
+    c->tl_count += 1;
+    for (cudaEvent_t ev : {t.fork, t.k1, t.chain, t.end}) cudaEventDestroy(ev);
+  }
+  c->timelines.clear();
+  if (out3)
+    for (int i = 0; i < 3; ++i) out3[i] = c->tl_count ? c->tl_sum[i] / c->tl_count : 0.0;
+  if (count) *count = c->tl_count;
+  return PS_OK;
+}
+
 int ps_stats_reset(ps_ctx* h) {
   if (!h) return PS_ERR_ARG;
   Ctx* c = C(h);
@@ -821,6 +849,9 @@ int ps_stats_reset(ps_ctx* h) {
   c->launches = 0;
   c->k1_ms = 0.0;
   c->k1_count = 0;
+  if (int rc = ps_timeline(h, nullptr, nullptr)) return rc;
+  c->tl_sum[0] = c->tl_sum[1] = c->tl_sum[2] = 0.0;
+  c->tl_count = 0;
   return PS_OK;
 }
 

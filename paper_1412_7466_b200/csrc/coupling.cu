@@ -754,6 +754,34 @@ int schur_finish(Ctx* c, const double2* v_own, const double2* a_own, const doubl
 // K1s on sm_count - overlap_sms CTAs (high-priority stream) runs concurrently
 // with the HBM-bound chain C -> A^+ -> B (low-priority stream, which gets
 // the SMs K1s leaves free); the deterministic K1s reduce joins both.
+// Queued at the fork (default), the 587-CTA C^T GEMV takes every SM for its
+// ~0.1 ms at full HBM bandwidth before K1s' CTAs get in, and B streams on the
+// free SMs during K1s.  overlap_k1_first queues the chain after K1s behind
+// the Bloch weights, so K1s' high-priority CTAs are dispatched first and the
+// whole chain streams on the free SMs -- measured slower at cfg3 (2.35 vs
+// 2.31 ms): a few SMs pull only ~116 GB/s each with plain loads
+// (tools/probe_timeline.py, tools/sm_stream_bw.cu).  TMA bulk copies reach
+// ~216 GB/s per SM in isolation, but staged GEMVs built on them ran at
+// 64-98 GB/s per SM (per-stage synchronisation), so the chain stays here.
+struct ChainArgs {
+  Ctx* c;
+  const double2* v;
+  Work* w;
+  cudaEvent_t bw_done;
+  cudaEvent_t chain_tl;   // profile timeline event (or null)
+};
+
+static int overlapped_chain(void* p) {
+  ChainArgs* a = static_cast<ChainArgs*>(p);
+  Ctx* c = a->c;
+  if (a->bw_done) PS_CUDA_TRY(c, cudaStreamWaitEvent(c->s_lo, a->bw_done, 0));
+  if (int rc = dense_apply_C(c, 0, a->v, a->w->gpart, a->w->g, c->s_lo)) return rc;
+  if (int rc = b_pinv(c, 0, a->w->g, a->w, c->s_lo)) return rc;
+  PS_CUDA_TRY(c, cudaEventRecord(c->ev_cpl, c->s_lo));
+  if (a->chain_tl) PS_CUDA_TRY(c, cudaEventRecord(a->chain_tl, c->s_lo));
+  return PS_OK;
+}
+
 static int schur_overlapped(Ctx* c, const double2* v, double2* y, cudaStream_t st) {
   if (!c->s_hi) {
     int lo = 0, hi = 0;
@@ -763,19 +791,37 @@ static int schur_overlapped(Ctx* c, const double2* v, double2* y, cudaStream_t s
     PS_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     PS_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_k1, cudaEventDisableTiming));
     PS_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_cpl, cudaEventDisableTiming));
+    PS_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_bw, cudaEventDisableTiming));
   }
   Work w;
   if (int rc = work(c, 0, &w)) return rc;
   PS_CUDA_TRY(c, cudaEventRecord(c->ev_fork, st));
   PS_CUDA_TRY(c, cudaStreamWaitEvent(c->s_hi, c->ev_fork, 0));
   PS_CUDA_TRY(c, cudaStreamWaitEvent(c->s_lo, c->ev_fork, 0));
-  SymOverlap ov{c->s_hi, c->sm_count - c->overlap_sms, c->ev_k1, c->ev_cpl};
-  // the coupling chain is enqueued first on the host but K1s' CTAs are
-  // dispatched first (stream priority); the reduce waits on ev_cpl
-  if (int rc = dense_apply_C(c, 0, v, w.gpart, w.g, c->s_lo)) return rc;
-  if (int rc = b_pinv(c, 0, w.g, &w, c->s_lo)) return rc;
-  PS_CUDA_TRY(c, cudaEventRecord(c->ev_cpl, c->s_lo));
-  return m2l_apply_sym(c, v, bpow_of(c, 0) + 1, y, 1, v, w.bsub, st, &ov);
+  Ctx::Timeline tl{};
+  if (c->profile) {
+    for (cudaEvent_t* e : {&tl.fork, &tl.k1, &tl.chain, &tl.end})
+      PS_CUDA_TRY(c, cudaEventCreate(e));
+    PS_CUDA_TRY(c, cudaEventRecord(tl.fork, st));
+    c->tl_k1 = tl.k1;
+  }
+  ChainArgs ca{c, v, &w, nullptr, c->profile ? tl.chain : nullptr};
+  SymOverlap ov{c->s_hi, c->sm_count - c->overlap_sms, c->ev_k1, c->ev_cpl, c->ev_bw,
+                nullptr, nullptr};
+  if (c->overlap_k1_first) {
+    ca.bw_done = c->ev_bw;
+    ov.chain = overlapped_chain;
+    ov.chain_arg = &ca;
+  } else if (int rc = overlapped_chain(&ca)) {
+    return rc;
+  }
+  const int rc = m2l_apply_sym(c, v, bpow_of(c, 0) + 1, y, 1, v, w.bsub, st, &ov);
+  if (c->profile) {
+    c->tl_k1 = nullptr;
+    PS_CUDA_TRY(c, cudaEventRecord(tl.end, st));
+    c->timelines.push_back(tl);
+  }
+  return rc;
 }
 
 int apply_schur(Ctx* c, const double2* v, double2* y, cudaStream_t st) {

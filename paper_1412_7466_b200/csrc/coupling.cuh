@@ -19,4 +19,5 @@ void release_dense_coupling(Ctx* c);
 int dense_apply_C(Ctx* c, int r, const double2* v_r, double2* gpart, double2* g_r, cudaStream_t st);
 int dense_apply_B(Ctx* c, int r, const double2* x_r, double2* b_r, cudaStream_t st);
 size_t dense_gpart_elems(const Ctx* c);
+
 }  // namespace ps

@@ -75,8 +75,9 @@ struct Ctx {
   int sym_part = 0, sym_nparts = 1;   // K1s block range (ps_apply_T_blocks)
   int k1_reserve_sms = 0;   // single-RHS M2L grids leave this many SMs free (multi-GPU overlap)
   int overlap_sms = 2;      // < 0: serial (swept with tools/probe_k1.py: 2 is best at cfg3)
+  int overlap_k1_first = 0; // 1: queue the coupling chain behind K1s (see schur_overlapped)
   cudaStream_t s_hi = nullptr, s_lo = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_k1 = nullptr, ev_cpl = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_k1 = nullptr, ev_cpl = nullptr, ev_bw = nullptr;
 
   // right-hand sides
   int nrhs = 1;
@@ -103,6 +104,15 @@ struct Ctx {
   double k1_ms = 0.0;
   long long k1_count = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k1_events;
+  // overlapped-step timeline (profile mode): events at the fork, K1s end,
+  // coupling-chain end and step end; folded by ps_timeline
+  struct Timeline {
+    cudaEvent_t fork, k1, chain, end;
+  };
+  std::vector<Timeline> timelines;
+  cudaEvent_t tl_k1 = nullptr;     // set by launch_s for the current overlapped step
+  double tl_sum[3] = {0, 0, 0};
+  long long tl_count = 0;
 };
 
 inline Ctx* C(ps_ctx* h) { return reinterpret_cast<Ctx*>(h); }

@@ -16,7 +16,13 @@ struct SymOverlap {
   cudaStream_t k1_stream;   // bloch weights + K1s
   int grid;                 // CTAs for K1s
   cudaEvent_t k1_done;      // recorded on k1_stream after K1s
-  cudaEvent_t cpl_done;     // coupling chain finished (recorded by the caller)
+  cudaEvent_t cpl_done;     // coupling chain finished (recorded by the chain callback)
+  cudaEvent_t bw_done;      // recorded on k1_stream after the Bloch weights
+  // enqueues the coupling chain (its stream waits on bw_done first): called
+  // after K1s is queued, so K1s and the chain become ready together and the
+  // high-priority K1s CTAs are dispatched first; records cpl_done
+  int (*chain)(void*);
+  void* chain_arg;
 };
 int m2l_max_order();
 // out: [nt][L] for the owned targets; see m2l.cu for the epilogue modes.

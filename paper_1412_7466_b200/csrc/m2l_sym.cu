@@ -381,32 +381,55 @@ __global__ void bloch_weight_1(const double2* __restrict__ beta, const double2* 
 // blocks (A, X), A < X, then the forward parts of the CTAs covering block row
 // X -- restricted to the launch's block range [kb0, kb0 + nb) (a multi-GPU
 // part; the other parts' contributions arrive through the reduce-scatter).
-__global__ void k1s_reduce(const double2* __restrict__ apart, const double2* __restrict__ bpart,
-                           int T, long long kb0, long long nb, int G, int maxseg, int M, int L,
-                           int mode, const double2* __restrict__ v_own,
-                           const double2* __restrict__ sdiag, const double2* __restrict__ bsub,
-                           double2* __restrict__ out) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= M * L) return;
-  const int m = idx / L, r = idx % L;
+// The reverse run (up to T - 1 partial rows per output) is split over kRS
+// threads in fixed contiguous chunks, combined in chunk order through shared
+// memory: deterministic, and the last tiles' long runs no longer serialise
+// one thread's L2 loads (a thread per output took ~45 us at cfg3).
+constexpr int kRO = 32;   // outputs per CTA
+constexpr int kRS = 8;    // chunks of the reverse run per output
+__global__ void __launch_bounds__(kRO * kRS) k1s_reduce(
+    const double2* __restrict__ apart, const double2* __restrict__ bpart, int T, long long kb0,
+    long long nb, int G, int maxseg, int M, int L, int mode, const double2* __restrict__ v_own,
+    const double2* __restrict__ sdiag, const double2* __restrict__ bsub, double2* __restrict__ out) {
+  __shared__ double2 red[kRS][kRO];
+  const int o = threadIdx.x % kRO, q = threadIdx.x / kRO;
+  const int idx = blockIdx.x * kRO + o;
+  const bool live = idx < M * L;
+  const int m = live ? idx / L : 0, r = live ? idx % L : 0;
   const int X = m / kTT, w = m % kTT;
   const long long kb1 = kb0 + nb;
   auto off = [&](int a) -> long long { return (long long)a * T - (long long)a * (a - 1) / 2; };
   auto kbeg = [&](int c) -> long long { return kb0 + (nb * c) / G; };
   double2 sum = make_double2(0.0, 0.0);
-  // the blocks (A, X), A < X, have increasing indices off(A) + X - A: the
-  // in-range ones are a contiguous run of A
-  int A0 = 0, A1 = X;
-  if (kb0 > 0 || kb1 < off(T)) {
-    while (A0 < X && off(A0) + (X - A0) < kb0) ++A0;
-    A1 = A0;
-    while (A1 < X && off(A1) + (X - A1) < kb1) ++A1;
+  if (live) {
+    // the blocks (A, X), A < X, have increasing indices off(A) + X - A: the
+    // in-range ones are a contiguous run of A
+    int A0 = 0, A1 = X;
+    if (kb0 > 0 || kb1 < off(T)) {
+      while (A0 < X && off(A0) + (X - A0) < kb0) ++A0;
+      A1 = A0;
+      while (A1 < X && off(A1) + (X - A1) < kb1) ++A1;
+    }
+    const int n = A1 - A0;
+    const int c0 = A0 + (n * q) / kRS, c1 = A0 + (n * (q + 1)) / kRS;
+    double2 s2 = make_double2(0.0, 0.0);
+#pragma unroll 4
+    for (int A = c0; A < c1; ++A) {
+      const long long k = off(A) + (X - A);
+      const double2 v = bpart[((size_t)k * kTT + w) * L + r];
+      s2.x += v.x;
+      s2.y += v.y;
+    }
+    sum = s2;
   }
-  for (int A = A0; A < A1; ++A) {
-    const long long k = off(A) + (X - A);
-    const double2 v = bpart[((size_t)k * kTT + w) * L + r];
-    sum.x += v.x;
-    sum.y += v.y;
+  red[q][o] = sum;
+  __syncthreads();
+  if (q != 0 || !live) return;
+  sum = red[0][o];
+#pragma unroll
+  for (int c = 1; c < kRS; ++c) {
+    sum.x += red[c][o].x;
+    sum.y += red[c][o].y;
   }
   const long long ra = off(X) > kb0 ? off(X) : kb0;                 // in-range blocks of row X
   const long long rb = off(X + 1) < kb1 ? off(X + 1) : kb1;
@@ -510,6 +533,7 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   bloch_weight_1<<<2 * ctx->sm_count, 256, 0, ks>>>(beta, bpow - 1, ctx->M, S::L, a.ncp, bw, bws,
                                                     bwr, bwsr);
   PS_CUDA_TRY(ctx, cudaGetLastError());
+  if (ov) PS_CUDA_TRY(ctx, cudaEventRecord(ov->bw_done, ks));
   static unsigned long long attr_mask = 0;
   if (first_on_device(&attr_mask, ctx->device)) {
     PS_CUDA_TRY(ctx, cudaFuncSetAttribute(m2l_sym_kernel<P>,
@@ -529,12 +553,16 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   }
   const int n = ctx->M * S::L;
   if (ov) {
+    if (ctx->tl_k1) PS_CUDA_TRY(ctx, cudaEventRecord(ctx->tl_k1, ks));
     PS_CUDA_TRY(ctx, cudaEventRecord(ov->k1_done, ks));
+    if (ov->chain)
+      if (int rc = ov->chain(ov->chain_arg)) return rc;
     PS_CUDA_TRY(ctx, cudaStreamWaitEvent(st, ov->k1_done, 0));
     PS_CUDA_TRY(ctx, cudaStreamWaitEvent(st, ov->cpl_done, 0));
   }
-  k1s_reduce<<<(n + 255) / 256, 256, 0, st>>>(a.apart, a.bpart, a.T, a.kb0, a.nb, G, a.maxseg, ctx->M,
-                                              S::L, mode, v_own, ctx->d_S, bsub, out);
+  k1s_reduce<<<(n + kRO - 1) / kRO, kRO * kRS, 0, st>>>(a.apart, a.bpart, a.T, a.kb0, a.nb, G,
+                                                        a.maxseg, ctx->M, S::L, mode, v_own,
+                                                        ctx->d_S, bsub, out);
   PS_CUDA_TRY(ctx, cudaGetLastError());
   ctx->launches += 3;
   return PS_OK;

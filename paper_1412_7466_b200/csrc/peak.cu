@@ -9,10 +9,12 @@
 
 namespace {
 
-// 8 independent chains per thread at 16 CTAs of 256 threads per SM: the best
-// of the swept variants (tools/dfma_variants: 8/16/32 chains x 2-16 CTAs/SM).
+// 8 independent chains per thread at 8 CTAs of 256 threads per SM (64 warps,
+// full residency): 36.5 TF/s on the B200, 98% of the nominal 148 x 64 x 2 x
+// 1.965 GHz = 37.2 TF/s (tools/fp64_pipes.cu; the 16-CTA launch of round 1
+// oversubscribed residency and read 34.2).
 constexpr int kChains = 8;
-constexpr int kCtasPerSm = 16;
+constexpr int kCtasPerSm = 8;
 __global__ void __launch_bounds__(256) dfma_chains(double* out, int iters, double a, double b) {
   double x[kChains];
 #pragma unroll

@@ -209,6 +209,10 @@ class Engine:
         """SMs left to the coupling chain while K1s runs (< 0: serial)."""
         self._check(self.lib.ps_set_overlap(self.ctx, int(sms)))
 
+    def set_overlap_order(self, k1_first: bool):
+        """Queue the coupling chain behind K1s (True) or at the fork (False)."""
+        self._check(self.lib.ps_set_overlap_order(self.ctx, 1 if k1_first else 0))
+
     def set_k1_reserve(self, sms: int):
         """Single-RHS M2L grids leave `sms` SMs free for overlapped work."""
         self._check(self.lib.ps_set_k1_reserve(self.ctx, int(sms)))
@@ -427,6 +431,13 @@ class Engine:
         n, ms, cnt = ctypes.c_longlong(), ctypes.c_double(), ctypes.c_longlong()
         self._check(self.lib.ps_stats(self.ctx, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(cnt)))
         return dict(launches=n.value, k1_ms=ms.value, k1_count=cnt.value)
+
+    def timeline(self) -> dict:
+        """Mean {k1_end, chain_end, step_end} ms of profiled overlapped steps."""
+        out = (ctypes.c_double * 3)()
+        n = ctypes.c_longlong()
+        self._check(self.lib.ps_timeline(self.ctx, out, ctypes.byref(n)))
+        return dict(k1_end_ms=out[0], chain_end_ms=out[1], step_end_ms=out[2], steps=n.value)
 
     def stats_reset(self):
         self._check(self.lib.ps_stats_reset(self.ctx))
