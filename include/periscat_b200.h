@@ -40,6 +40,13 @@ typedef struct ps_ctx ps_ctx;
 
 /* ---- lifetime ---------------------------------------------------------- */
 int ps_version(void);
+/* Guard-band (canary) builds only (-DPS_CANARY, tools/canary_run.sh): bytes
+ * found overwritten past the end of any context allocation so far (live ones
+ * are checked now, freed ones were checked at free); -1 in normal builds. */
+long long ps_canary_check(void);
+/* Canary builds: a deliberate overrun of a fresh allocation; returns the
+ * overwritten byte count the guard band saw (1), -1 in normal builds. */
+long long ps_canary_selftest(void);
 int ps_create(ps_ctx** out, int device);
 void ps_destroy(ps_ctx* ctx);
 const char* ps_last_error(const ps_ctx* ctx);

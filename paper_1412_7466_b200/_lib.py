@@ -21,6 +21,8 @@ _DP = ctypes.POINTER(ctypes.c_double)
 _IP = ctypes.POINTER(ctypes.c_int)
 SIGNATURES = {
     "ps_version": (_I, []),
+    "ps_canary_check": (ctypes.c_longlong, []),
+    "ps_canary_selftest": (ctypes.c_longlong, []),
     "ps_max_order": (_I, []),
     "ps_create": (_I, [ctypes.POINTER(_P), _I]),
     "ps_destroy": (None, [_P]),

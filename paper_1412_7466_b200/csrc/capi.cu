@@ -116,6 +116,51 @@ extern "C" {
 
 int ps_version(void) { return 1; }
 
+#ifdef PS_CANARY
+}  // extern "C"
+namespace {
+__global__ void canary_overrun(unsigned char* p, int n) {
+  if (threadIdx.x == 0) p[n + 3] = 0x5A;      // deliberately 4 bytes past the end
+}
+}  // namespace
+extern "C" {
+#endif
+
+/* Self-test of the guard bands: a deliberate 1-byte overrun must be counted. */
+long long ps_canary_selftest(void) {
+#ifdef PS_CANARY
+  unsigned char* p = nullptr;
+  if (ps::dev_malloc(&p, 1024) != cudaSuccess) return -2;
+  canary_overrun<<<1, 32>>>(p, 1024);
+  cudaDeviceSynchronize();
+  long long before;
+  {
+    std::lock_guard<std::mutex> g(ps::canary_reg().mu);
+    before = ps::canary_reg().violations;
+  }
+  ps::dev_free(p);
+  std::lock_guard<std::mutex> g(ps::canary_reg().mu);
+  const long long found = ps::canary_reg().violations - before;
+  ps::canary_reg().violations = before;        // not a product-kernel violation
+  return found;
+#else
+  return -1;
+#endif
+}
+
+long long ps_canary_check(void) {
+#ifdef PS_CANARY
+  std::lock_guard<std::mutex> g(ps::canary_reg().mu);
+  for (auto& kv : ps::canary_reg().live) {
+    const long long bad = ps::canary_bad_bytes(kv.first, kv.second);
+    if (bad) ps::canary_reg().violations += bad;
+  }
+  return ps::canary_reg().violations;
+#else
+  return -1;
+#endif
+}
+
 int ps_max_order(void) { return ps::m2l_max_order(); }
 
 int ps_create(ps_ctx** out, int device) {

@@ -5,6 +5,10 @@
 #include <cstdint>
 #include <string>
 #include <vector>
+#ifdef PS_CANARY
+#include <mutex>
+#include <unordered_map>
+#endif
 
 #include "../../include/periscat_b200.h"
 
@@ -141,6 +145,33 @@ inline bool first_on_device(unsigned long long* mask, int device) {
 // blocks and Krylov basis instead of paying cudaMalloc/cudaFree of ~1 GB.
 // Allocation and free are rare (setup, growth, destroy) and fully
 // synchronise, so the non-blocking worker streams never race them.
+#ifdef PS_CANARY
+// Guard-band build (tools/canary_run.sh; compute-sanitizer is not available on
+// the GPU pool): every context allocation gets kCanaryBytes of 0xA5 after its
+// end, verified when it is freed and by ps_canary_check() -- any kernel
+// writing past a workspace it owns is counted.
+constexpr size_t kCanaryBytes = 1 << 16;
+struct CanaryReg {
+  std::mutex mu;
+  std::unordered_map<void*, size_t> live;
+  long long violations = 0;
+};
+inline CanaryReg& canary_reg() {
+  static CanaryReg r;
+  return r;
+}
+inline long long canary_bad_bytes(void* p, size_t bytes) {
+  std::vector<unsigned char> h(kCanaryBytes);
+  cudaDeviceSynchronize();
+  if (cudaMemcpy(h.data(), static_cast<char*>(p) + bytes, kCanaryBytes, cudaMemcpyDeviceToHost) !=
+      cudaSuccess)
+    return -1;
+  long long bad = 0;
+  for (unsigned char b : h) bad += (b != 0xA5);
+  return bad;
+}
+#endif
+
 inline cudaError_t dev_malloc_raw(void** p, size_t bytes) {
   static int pool_ready[64] = {0};
   int dev = 0;
@@ -154,7 +185,17 @@ inline cudaError_t dev_malloc_raw(void** p, size_t bytes) {
       return e;
     pool_ready[dev] = 1;
   }
+#ifdef PS_CANARY
+  if ((e = cudaMallocAsync(p, bytes + kCanaryBytes, 0)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(static_cast<char*>(*p) + bytes, 0xA5, kCanaryBytes, 0)) != cudaSuccess)
+    return e;
+  {
+    std::lock_guard<std::mutex> g(canary_reg().mu);
+    canary_reg().live[*p] = bytes;
+  }
+#else
   if ((e = cudaMallocAsync(p, bytes, 0)) != cudaSuccess) return e;
+#endif
   return cudaStreamSynchronize(0);
 }
 template <class T>
@@ -164,6 +205,17 @@ inline cudaError_t dev_malloc(T** p, size_t bytes) {
 inline void dev_free(void* p) {
   if (!p) return;
   cudaDeviceSynchronize();
+#ifdef PS_CANARY
+  {
+    std::lock_guard<std::mutex> g(canary_reg().mu);
+    auto it = canary_reg().live.find(p);
+    if (it != canary_reg().live.end()) {
+      const long long bad = canary_bad_bytes(p, it->second);
+      if (bad) canary_reg().violations += bad;
+      canary_reg().live.erase(it);
+    }
+  }
+#endif
   cudaFreeAsync(p, 0);
   cudaStreamSynchronize(0);
 }
