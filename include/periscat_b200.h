@@ -366,7 +366,8 @@ typedef struct ps_particle_desc {
 /* Scattering matrix s_ln, |l|, |n| <= p, of one particle from the Mueller
  * BIE (scatmat.scattering_matrix): the
  * 2n x 2n Nystrom system of Eqs. intg1-intg2 assembled on the device, solved
- * for the 2p+1 incident regular waves (cuSOLVER LU), projected onto outgoing
+ * for the 2p+1 incident regular waves (in-house Gauss-Jordan with partial
+ * pivoting on the device, scatmat.cu gj_*), projected onto outgoing
  * coefficients.  S_host: complex [2p+1][2p+1] row-major (row l, column n);
  * residual (may be NULL): ||A X - B|| / ||B|| of the discrete solve.
  * PS_ERR_NUMERICAL for a singular system or non-finite entries. */

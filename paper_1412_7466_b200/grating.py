@@ -6,21 +6,18 @@ Schur correction needs its SVD factors, column scaling, right-hand side and
 the curve nodes the coupling blocks touch.  ``GratingSystem`` duck-types
 that object (same attribute names: ``config``, ``curves``, ``centers``,
 ``matrix``, ``rhs``, ``col_scale``, ``cols``, ``rows``, ``svd``), so a caller
-holding a real reference system passes it unchanged, and the benchmark /
-tests load the same data from the fixtures ``oracle/make_empty.py`` wrote
-with the reference.  Assembly of the matrix itself is setup outside the hot
+holding a real reference system passes it unchanged; the benchmark and tests
+load the same data from the fixtures ``oracle/make_empty.py`` wrote with the
+reference (``workloads.py`` at the repository root -- the product package
+never reads test data).  Assembly of the matrix itself is setup outside the hot
 path.
 """
 from __future__ import annotations
 
 import math
-import os
 from dataclasses import dataclass, field
 
 import numpy as np
-
-GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
-
 
 @dataclass(frozen=True)
 class InterfaceSpec:
@@ -141,60 +138,6 @@ def factorize(system) -> None:
         system.svd = tuple(np.linalg.svd(system.matrix, full_matrices=False))
 
 
-def fixture_path(name: str, directory: str = GOLDEN) -> str:
-    for d in (directory, os.path.join(directory, "cfg5")):
-        p = os.path.join(d, f"empty_{name}.npz")
-        if os.path.exists(p):
-            return p
-    raise FileNotFoundError(f"empty-grating fixture {name!r} not found under {directory} "
-                            "(cfg5 angles are generated by __graft_entry__.build())")
-
-
-def load_fixture(name: str, directory: str = GOLDEN) -> GratingSystem:
-    z = np.load(fixture_path(name, directory))
-    cols = {str(n): slice(int(a), int(b)) for n, (a, b) in zip(z["col_names"], z["cols"])}
-    rows = {str(n): slice(int(a), int(b)) for n, (a, b) in zip(z["row_names"], z["rows"])}
-    sc = z["scalars"]
-    cfg = GratingConfig(period=float(sc[0]), k1=float(sc[1]), k2=float(sc[2]), k3=float(sc[3]),
-                        kp=float(sc[4]), incident_angle=float(sc[5]),
-                        near_field_copies=int(sc[6]), j_expansion_order=int(sc[7]),
-                        regularization=float(sc[8]), y0=float(sc[9]),
-                        rb_modes_per_direction=cols["c"].stop - cols["c"].start)
-    if "top_spec" in z.files:       # fixtures written with their interface parametrisation
-        specs = []
-        for key in ("top_spec", "bottom_spec"):
-            v = z[key]
-            ns = int(v[1])
-            specs.append(InterfaceSpec(float(v[0]), tuple(v[2:2 + ns]), tuple(v[2 + ns:])))
-        cfg.interface_top, cfg.interface_bottom = specs
-    nw = z["L2_nodes"].shape[0]
-    curves = {
-        "g1": Curve(z["g1_nodes"], z["g1_normals"], z["g1_w"]),
-        "g2": Curve(z["g2_nodes"], z["g2_normals"], z["g2_w"]),
-        "L2": Curve(z["L2_nodes"], np.tile([1.0, 0.0], (nw, 1)), np.zeros(nw)),
-    }
-    return GratingSystem(cfg, curves, {2: z["center2"]}, z["A"], z["f"], z["col_scale"],
-                         cols, rows, None, name)
-
-
-# BASELINE.json configs: cfg -> (fixture, centres file, p, radius)
-CONFIGS = {
-    1: dict(system="w10", centers="centers_cfg1.npy", p=20, radius=0.04),
-    2: dict(system="w10", centers="centers_cfg2.npy", p=20, radius=0.04),
-    3: dict(system="w10", centers="centers_cfg3.npy", p=25, radius=0.012),
-    4: dict(system="wood", centers="centers_cfg3.npy", p=25, radius=0.012),
-}
-
-
-CFG5_ANGLES = [f"w10_a{i:02d}" for i in range(16)]   # theta_B = linspace(-pi/3, pi/3, 16)
-
-
-def load_cfg5():
-    """cfg5: M=1e4, r=0.004, p=20, 16 incidence angles at omega=10."""
-    centers = np.load(os.path.join(GOLDEN, "centers_cfg5.npy"))
-    return [load_fixture(n) for n in CFG5_ANGLES], centers, 20, 0.004
-
-
 def baseline_config(omega: float, theta_ref: float, **kw) -> GratingConfig:
     """BASELINE.json grating: period 1, layer indices 1.0/1.2/1.0,
     inclusions 1.5, flat interfaces at y = +-0.5; theta_ref measured from +x."""
@@ -203,15 +146,3 @@ def baseline_config(omega: float, theta_ref: float, **kw) -> GratingConfig:
     return GratingConfig(period=1.0, k1=omega, k2=1.2 * omega, k3=omega, kp=1.5 * omega,
                          incident_angle=theta_ref, y0=y0, interface_top=top,
                          interface_bottom=bot, **kw)
-
-
-def fixture_config(name: str) -> GratingConfig:
-    """The GratingConfig a committed fixture was assembled from (w10, wood,
-    w10_aNN): its stored scalars, BASELINE interfaces and node counts."""
-    return load_fixture(name).config
-
-
-def load_config(cfg: int):
-    c = CONFIGS[cfg]
-    centers = np.load(os.path.join(GOLDEN, c["centers"]))
-    return load_fixture(c["system"]), centers, c["p"], c["radius"]

@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 from conftest import REFERENCE
+import workloads  # noqa: E402
 
 FIXTURES = ["w10", "wood", "w10_a00", "curved"]
 
@@ -18,7 +19,7 @@ FIXTURES = ["w10", "wood", "w10_a00", "curved"]
 def test_unit_cell_matches_fixture_curves(name):
     from paper_1412_7466_b200 import empty_setup as es
     from paper_1412_7466_b200 import grating
-    ref = grating.load_fixture(name)
+    ref = workloads.load_fixture(name)
     cell = es.unit_cell(ref.config)
     for key, arr in (("g1", cell.g1), ("g2", cell.g2)):
         cv = ref.curves[key]
@@ -36,7 +37,7 @@ def test_build_desc_layout():
     from paper_1412_7466_b200 import _lib
     from paper_1412_7466_b200 import empty_setup as es
     from paper_1412_7466_b200 import grating
-    cfg = grating.fixture_config("curved")
+    cfg = workloads.fixture_config("curved")
     desc, keep = es.build_desc(cfg, es.unit_cell(cfg))
     assert desc.g1.n == 120 and desc.lid_up.n == 50 and desc.rule_n == 15
     assert desc.rule_skip == 10 and desc.rule_interp == 16
@@ -49,10 +50,10 @@ def test_validate_rejects_mixed_geometry():
     from paper_1412_7466_b200 import empty_setup as es
     from paper_1412_7466_b200 import grating
     with pytest.raises(ValueError):
-        es.validate([grating.fixture_config("w10"), grating.fixture_config("wood")])
+        es.validate([workloads.fixture_config("w10"), workloads.fixture_config("wood")])
     with pytest.raises(ValueError):
         es.validate([grating.baseline_config(10.0, 0.2)])
-    es.validate([grating.fixture_config(n) for n in ("w10_a00", "w10_a15")])
+    es.validate([workloads.fixture_config(n) for n in ("w10_a00", "w10_a15")])
 
 
 @pytest.fixture(scope="module")
@@ -100,7 +101,7 @@ def test_unit_cell_from_reference_config(refmod, curved):
         assert np.array_equal(cell.centers[k], ctr[k])
     # our own GratingConfig restates the reference's geometry exactly
     from paper_1412_7466_b200 import grating
-    mine = grating.fixture_config("curved" if curved else "w10")
+    mine = workloads.fixture_config("curved" if curved else "w10")
     cm = es.unit_cell(mine)
     for a, b in ((cm.g1, cell.g1), (cm.g2, cell.g2), (cm.walls[1], cell.walls[1]),
                  (cm.lid_up, cell.lid_up)):
@@ -116,6 +117,6 @@ def test_wall_check_points_match_reference_checker():
 
     from paper_1412_7466_b200 import grating, postproc
     z = np.load(os.path.join(os.path.dirname(__file__), "golden", "walls_cfg1.npz"))
-    pts, layer = postproc.wall_check_points(grating.load_fixture("w10").config)
+    pts, layer = postproc.wall_check_points(workloads.load_fixture("w10").config)
     assert np.array_equal(pts, z["pts"])
     assert np.array_equal(layer, z["layer"])

@@ -25,6 +25,7 @@ import numpy as np
 import pytest
 
 from conftest import rel
+import workloads  # noqa: E402
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -66,7 +67,7 @@ def test_cfg5_apply_T_16rhs_k1d(cfg5):
     bloch = np.exp(1j * 10.0 * np.cos(theta))
     assert np.allclose(bloch[[0, 15]], [cfg5["pbs"][0].es.bloch, cfg5["pbs"][1].es.bloch],
                        rtol=0, atol=1e-15)
-    k2 = grating.load_fixture(NAMES[0]).config.k2
+    k2 = workloads.load_fixture(NAMES[0]).config.k2
     eng = Engine(0)
     eng.set_geometry(centers, P, k2, 1.0, 1)
     eng.set_bloch(bloch)
@@ -83,7 +84,7 @@ def schur5(cfg5):
     from oracle import parallel as OP
     from paper_1412_7466_b200 import grating, solver
     centers, sl = cfg5["centers"], cfg5["sl"]
-    op = solver.SchurOperator([grating.load_fixture(n) for n in NAMES], centers, P, radius=R,
+    op = solver.SchurOperator([workloads.load_fixture(n) for n in NAMES], centers, P, radius=R,
                               dense_gb=0.0)             # matrix-free coupling, as cfg5 runs
     v = _krylov(cfg5["pbs"][0], np.random.default_rng(5), 2)
     vd = torch.as_tensor(v).cuda()
@@ -126,7 +127,7 @@ def test_cfg5_solve_rhs0(cfg5):
     from oracle import periscat_oracle as O
     from paper_1412_7466_b200 import grating, postproc, solver
     centers, sl = cfg5["centers"], cfg5["sl"]
-    op = solver.SchurOperator(grating.load_fixture(NAMES[0]), centers, P, radius=R,
+    op = solver.SchurOperator(workloads.load_fixture(NAMES[0]), centers, P, radius=R,
                               dense_gb=0.0)
     rhs = op.rhs()
     beta, its, hist = solver.gmres(op, rhs, 1e-10, 150)

@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 from conftest import rel
+import workloads  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -52,8 +53,8 @@ def test_device_assembly_matches_reference_system(name):
     gratings: omega=10 (cfg1-3), the Wood anomaly (cfg4), cfg5's extreme
     angles, and the reference's default sinusoidal interfaces (curved)."""
     from paper_1412_7466_b200 import grating
-    ref = grating.load_fixture(name)
-    eng, systems = _setup([grating.fixture_config(name)])
+    ref = workloads.load_fixture(name)
+    eng, systems = _setup([workloads.fixture_config(name)])
     try:
         _check_against_fixture(systems[0].fetch(), ref)
         assert systems[0].cols == ref.cols and systems[0].rows == ref.rows
@@ -66,11 +67,11 @@ def test_device_assembly_batched_angles_concurrent_svd():
     on 4 concurrent cuSOLVER streams): the first and last angle match their
     reference systems, and every angle equals its own single-angle setup."""
     from paper_1412_7466_b200 import grating
-    cfgs = [grating.fixture_config(n) for n in grating.CFG5_ANGLES]
+    cfgs = [workloads.fixture_config(n) for n in workloads.CFG5_ANGLES]
     eng, systems = _setup(cfgs, svd_workers=4)
     try:
         for i, name in ((0, "w10_a00"), (15, "w10_a15")):
-            _check_against_fixture(systems[i].fetch(), grating.load_fixture(name))
+            _check_against_fixture(systems[i].fetch(), workloads.load_fixture(name))
         for i in (3, 9):
             e1, s1 = _setup([cfgs[i]])
             try:
@@ -92,7 +93,7 @@ def test_schur_with_device_setup_matches_golden(cfg):
     from paper_1412_7466_b200 import grating, solver
     pb = O.load_problem(cfg)
     z = np.load(os.path.join(O.GOLDEN, f"golden_cfg{cfg}.npz"))
-    conf = grating.fixture_config(grating.CONFIGS[cfg]["system"])
+    conf = workloads.fixture_config(workloads.CONFIGS[cfg]["system"])
     import torch
     op = solver.SchurOperator(conf, pb.centers, pb.p, smat=pb.smat, device=0)
     assert op.device_setup
@@ -112,7 +113,7 @@ def test_solve_full_from_config_matches_golden(cfg):
     from paper_1412_7466_b200 import grating, solver
     pb = O.load_problem(cfg)
     z = np.load(os.path.join(O.GOLDEN, f"golden_cfg{cfg}.npz"))
-    conf = grating.fixture_config(grating.CONFIGS[cfg]["system"])
+    conf = workloads.fixture_config(workloads.CONFIGS[cfg]["system"])
     sol = solver.solve_full(conf, pb.centers, pb.p, smat=pb.smat, device=0)
     assert rel(sol.c[0], z["c"]) <= 1e-9 and rel(sol.d[0], z["d"]) <= 1e-9
     assert abs(sol.flux[0]["error"] - float(z["flux_error"])) <= 1e-9
@@ -122,8 +123,8 @@ def test_solve_full_from_config_matches_golden(cfg):
 
 def test_setup_rejects_mixed_geometry_and_bad_angle():
     from paper_1412_7466_b200 import grating
-    a = grating.fixture_config("w10")
-    b = grating.fixture_config("wood")
+    a = workloads.fixture_config("w10")
+    b = workloads.fixture_config("wood")
     with pytest.raises(ValueError):
         _setup([a, b])
     bad = grating.baseline_config(10.0, 0.3)
@@ -143,7 +144,7 @@ def test_curved_grating_solve_matches_oracle(from_config):
     from paper_1412_7466_b200 import grating, solver
     pb = O.load_problem(1)
     z = np.load(os.path.join(O.GOLDEN, "golden_curved.npz"))
-    systems = grating.fixture_config("curved") if from_config else grating.load_fixture("curved")
+    systems = workloads.fixture_config("curved") if from_config else workloads.load_fixture("curved")
     op = solver.SchurOperator(systems, pb.centers, pb.p, smat=pb.smat, device=0)
     got = op(torch.as_tensor(z["v"][None]).cuda()).cpu().numpy()[0]
     assert rel(got, z["schur"]) <= MATVEC_TOL
@@ -161,7 +162,7 @@ def test_setup_argument_errors():
     from paper_1412_7466_b200 import _lib, grating
     from paper_1412_7466_b200 import empty_setup as es
     from paper_1412_7466_b200.engine import Engine
-    cfg = grating.fixture_config("w10")
+    cfg = workloads.fixture_config("w10")
     eng = Engine(0)
     try:
         eng.set_geometry(np.array([[0.0, 0.0]]), 2, cfg.k2)
@@ -202,7 +203,7 @@ def test_setup_split_and_factor_exchange():
     from paper_1412_7466_b200 import grating, solver
     from paper_1412_7466_b200.engine import Engine
     pb = O.load_problem(1)
-    cfgs = [grating.fixture_config(n) for n in grating.CFG5_ANGLES]
+    cfgs = [workloads.fixture_config(n) for n in workloads.CFG5_ANGLES]
     ref = solver.SchurOperator(cfgs, pb.centers, pb.p, smat=pb.smat, device=0)
     engs = [Engine(0), Engine(0)]
     ops = []
@@ -237,7 +238,7 @@ def test_layer_fields_match_reference_evaluator(name, golden, from_config):
     from paper_1412_7466_b200 import grating, postproc, solver
     pb = O.load_problem(1)
     z = np.load(os.path.join(O.GOLDEN, f"field_{name}.npz"))
-    systems = grating.fixture_config(name) if from_config else grating.load_fixture(name)
+    systems = workloads.fixture_config(name) if from_config else workloads.load_fixture(name)
     op = solver.SchurOperator(systems, pb.centers, pb.p, smat=pb.smat, device=0)
     got = postproc.empty_field(op, z["beta"][None], z["pts"], z["layer"])[0]
     ref = z["field"]
@@ -252,11 +253,11 @@ def test_no_inclusions_reduces_to_empty_grating(from_config):
     grating's own solution x = A^+ f (empty_grating.solve_empty, eg:276-290)
     and its flux balance."""
     from paper_1412_7466_b200 import grating, postproc, solver
-    ref = grating.load_fixture("w10")
+    ref = workloads.load_fixture("w10")
     u, s, vh = np.linalg.svd(ref.matrix, full_matrices=False)
     x = ref.col_scale * (vh.conj().T @ (np.minimum(1 / s, 1e10) * (u.conj().T @ ref.rhs)))
     c_ref, d_ref = x[ref.cols["c"]], x[ref.cols["d"]]
-    systems = grating.fixture_config("w10") if from_config else ref
+    systems = workloads.fixture_config("w10") if from_config else ref
     sol = solver.solve_full(systems, np.zeros((0, 2)), 20, radius=0.04, device=0)
     assert sol.iterations[0] == 0
     assert rel(sol.c[0], c_ref) <= 1e-12 and rel(sol.d[0], d_ref) <= 1e-12

@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 from conftest import rel
+import workloads  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -18,7 +19,7 @@ def test_ctypes_stub_apply_T_and_solve():
     z = np.load(os.path.join(O.GOLDEN, "golden_cfg1.npz"))
     ps = Periscat(0)
     try:
-        ps.setup(grating.load_fixture("w10"), pb.centers, pb.p, pb.smat)
+        ps.setup(workloads.load_fixture("w10"), pb.centers, pb.p, pb.smat)
         aT = ps.apply_T(z["v"])[0]
         assert rel(aT, z["apply_T"]) <= 1e-10
         beta, c, d, its = ps.solve()
@@ -54,7 +55,7 @@ def test_ctypes_stub_setup_from_config_and_bie():
     from paper_1412_7466_b200 import empty_setup as es
     from paper_1412_7466_b200 import grating, scatmat
     pb = O.load_problem(1)
-    cfg = grating.fixture_config("w10")
+    cfg = workloads.fixture_config("w10")
     cell = es.unit_cell(cfg)
     curves = {"g1": _Cv(cell.g1), "g2": _Cv(cell.g2), "L1": _Cv(cell.walls[0]),
               "L2": _Cv(cell.walls[1]), "L3": _Cv(cell.walls[2]), "Gu": _Cv(cell.lid_up),
@@ -101,7 +102,7 @@ def test_sharded_driver_nccl_world1():
     try:
         pb = O.load_problem(2)
         z = np.load(os.path.join(O.GOLDEN, "golden_cfg2.npz"))
-        op = solver.SchurOperator(grating.load_fixture("w10"), pb.centers, pb.p, smat=pb.smat,
+        op = solver.SchurOperator(workloads.load_fixture("w10"), pb.centers, pb.p, smat=pb.smat,
                                   target_range=parallel.shard_range(pb.M, 0, 1), dense_gb=0.0)
         sh = parallel.ShardedSchur(op)
         x, its, hist = parallel.gmres_dist(sh, sh.rhs(), 1e-10, 150, engine=op.eng)

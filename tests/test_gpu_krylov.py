@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 from conftest import rel
+import workloads  # noqa: E402
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -72,7 +73,7 @@ def test_gmres_dist_world1_multi_rhs_matches_ps_gmres():
     from oracle import periscat_oracle as O
     from paper_1412_7466_b200 import grating, parallel, solver
     pb = O.load_problem(2)
-    systems = [grating.load_fixture(n) for n in ("w10", "w10_a00", "w10_a15")]
+    systems = [workloads.load_fixture(n) for n in ("w10", "w10_a00", "w10_a15")]
     op = solver.SchurOperator(systems, pb.centers, pb.p, smat=pb.smat)
     rhs = op.rhs()
     x0, its0, hist0 = solver.gmres(op, rhs, 1e-10, 150)
@@ -113,7 +114,7 @@ def _sharded_body(rank, world, cfg):
     from paper_1412_7466_b200 import grating, parallel, solver
     pb = O.load_problem(cfg)
     t0, t1 = parallel.shard_range(pb.M, rank, world)
-    op = solver.SchurOperator(grating.load_fixture(O.CONFIGS[cfg]["empty"]), pb.centers, pb.p,
+    op = solver.SchurOperator(workloads.load_fixture(O.CONFIGS[cfg]["empty"]), pb.centers, pb.p,
                               smat=pb.smat, target_range=(t0, t1))
     rng = np.random.default_rng(11)
     v = pb.smat[None, None, :] * (rng.standard_normal((1, pb.M, pb.L))

@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 from conftest import rel
+import workloads  # noqa: E402
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -114,7 +115,7 @@ def test_domain_error_coincident():
 def _operator(O, cfg, coupled=True, dense_gb=40.0):
     from paper_1412_7466_b200 import grating, solver
     pb = O.load_problem(cfg)
-    sysm = grating.load_fixture(O.CONFIGS[cfg]["empty"])
+    sysm = workloads.load_fixture(O.CONFIGS[cfg]["empty"])
     op = solver.SchurOperator(sysm, pb.centers, pb.p, smat=pb.smat, coupled=coupled,
                               dense_gb=dense_gb)
     return pb, op
@@ -167,7 +168,7 @@ def test_solve_full_cfg1(O):
     from paper_1412_7466_b200 import grating, solver
     pb = O.load_problem(1)
     ref = O.solve_full(pb)
-    sol = solver.solve_full(grating.load_fixture("w10"), pb.centers, pb.p, smat=pb.smat)
+    sol = solver.solve_full(workloads.load_fixture("w10"), pb.centers, pb.p, smat=pb.smat)
     assert rel(sol.c[0], ref.c) <= 1e-9
     assert rel(sol.d[0], ref.d) <= 1e-9
     assert abs(sol.flux[0]["error"] - ref.flux["error"]) <= 1e-9
@@ -211,7 +212,7 @@ def test_schur_multi_rhs_matches_oracle(O, dense_gb):
     """Three incidence angles (own Bloch phase, SVD factors, f) in one batch."""
     from paper_1412_7466_b200 import grating, solver
     pb = O.load_problem(1)
-    systems = [grating.load_fixture(n) for n in ANGLES]
+    systems = [workloads.load_fixture(n) for n in ANGLES]
     op = solver.SchurOperator(systems, pb.centers, pb.p, smat=pb.smat, dense_gb=dense_gb)
     rng = np.random.default_rng(33)
     v = pb.smat[None, None, :] * _cplx(rng, (3, pb.M, pb.L))
@@ -227,7 +228,7 @@ def test_solve_full_multi_rhs(O):
     """Batched device GMRES: per-RHS convergence and Bragg coefficients."""
     from paper_1412_7466_b200 import grating, solver
     pb = O.load_problem(1)
-    systems = [grating.load_fixture(n) for n in ANGLES]
+    systems = [workloads.load_fixture(n) for n in ANGLES]
     sol = solver.solve_full(systems, pb.centers, pb.p, smat=pb.smat)
     for r, name in enumerate(ANGLES):
         pr = O.Problem(O.load_empty(name), pb.centers, pb.p, pb.radius, pb.smat)
@@ -285,7 +286,7 @@ def test_solve_full_vs_golden(O, cfg):
     from paper_1412_7466_b200 import grating, solver
     z = _golden(cfg)
     pb = O.load_problem(cfg)
-    sol = solver.solve_full(grating.load_fixture(O.CONFIGS[cfg]["empty"]), pb.centers, pb.p,
+    sol = solver.solve_full(workloads.load_fixture(O.CONFIGS[cfg]["empty"]), pb.centers, pb.p,
                             smat=pb.smat)
     assert rel(sol.c[0], z["c"]) <= 1e-9
     assert rel(sol.d[0], z["d"]) <= 1e-9
@@ -305,7 +306,7 @@ def test_dense_rotated_smatrix(O, nrhs):
     S = np.diag(pb.smat) + 1e-3 * np.outer(pb.smat, np.ones(L)) * _cplx(rng, (L, L))
     rot = rng.uniform(0, 2 * np.pi, pb.M)
     names = ANGLES[:nrhs]
-    op = solver.SchurOperator([grating.load_fixture(n) for n in names], pb.centers, pb.p,
+    op = solver.SchurOperator([workloads.load_fixture(n) for n in names], pb.centers, pb.p,
                               smat=S, rot=rot)
     v = _cplx(rng, (nrhs, pb.M, L))
     got = op(_dev(v)).cpu().numpy()
@@ -341,7 +342,7 @@ def test_gmres_identity_one_iteration(O):
     coupling -> T = 0) converges in one iteration to x = rhs."""
     from paper_1412_7466_b200 import grating, solver
     pb = O.load_problem(1)
-    sysm = grating.load_fixture("w10")
+    sysm = workloads.load_fixture("w10")
     sysm.config.near_field_copies = 0
     op = solver.SchurOperator(sysm, pb.centers[:1], pb.p, smat=pb.smat, coupled=False)
     b = torch.as_tensor(np.random.default_rng(2).standard_normal((1, 1, pb.L)) + 0j).cuda()
@@ -397,7 +398,7 @@ def test_target_shards_reassemble(O, ranks):
     rng = np.random.default_rng(ranks)
     v = pb.smat[None, :] * _cplx(rng, (pb.M, pb.L))
     ref = O.apply_schur_operator(pb, v).reshape(pb.M, pb.L)
-    sysm = grating.load_fixture("w10")
+    sysm = workloads.load_fixture("w10")
     vd = _dev(v[None])
     # C partials over each rank's own sources, summed as the all-reduce would
     ops = [solver.SchurOperator(sysm, pb.centers, pb.p, smat=pb.smat,
@@ -444,7 +445,7 @@ def test_pair_split_shards_reassemble(O, ranks):
     rng = np.random.default_rng(10 + ranks)
     v = pb.smat[None, :] * _cplx(rng, (pb.M, pb.L))
     ref = O.apply_schur_operator(pb, v).reshape(pb.M, pb.L)
-    sysm = grating.load_fixture("w10")
+    sysm = workloads.load_fixture("w10")
     vd = _dev(v[None])
     rngs = [parallel.shard_range(pb.M, r, ranks) for r in range(ranks)]
     ops = [solver.SchurOperator(sysm, pb.centers, pb.p, smat=pb.smat, target_range=rngs[r])
@@ -490,7 +491,7 @@ def test_eval_total_field_grid_cfg2(O):
     particle field matches the oracle's phased multipole sums."""
     from paper_1412_7466_b200 import grating, postproc, solver
     pb = O.load_problem(2)
-    sysm = grating.load_fixture("w10")
+    sysm = workloads.load_fixture("w10")
     op = solver.SchurOperator(sysm, pb.centers, pb.p, smat=pb.smat)
     rng = np.random.default_rng(4)
     beta = pb.smat[None, None, :] * _cplx(rng, (1, pb.M, pb.L))
@@ -519,7 +520,7 @@ def test_matvec_and_solve_are_bit_reproducible(O, cfg, nrhs):
     (K1s + SM-partitioned coupling for cfg3, K1d for 16 RHS)."""
     from paper_1412_7466_b200 import grating, solver
     pb = O.load_problem(cfg)
-    sysm = grating.load_fixture(O.CONFIGS[cfg]["empty"])
+    sysm = workloads.load_fixture(O.CONFIGS[cfg]["empty"])
     systems = [sysm] * nrhs
     op = solver.SchurOperator(systems, pb.centers, pb.p, smat=pb.smat)
     rng = np.random.default_rng(99)
@@ -570,7 +571,7 @@ def test_schur_cfg3_full_vector(O):
     with mp.get_context("spawn").Pool(n, initializer=_cfg3_init) as pool:
         u = np.concatenate(pool.map(_cfg3_chunk, [(c, v, xg) for c in chunks]), axis=0)
     ref = v - pb.smat[None, :] * u
-    op = solver.SchurOperator(grating.load_fixture("w10"), pb.centers, pb.p, smat=pb.smat)
+    op = solver.SchurOperator(workloads.load_fixture("w10"), pb.centers, pb.p, smat=pb.smat)
     got = op(_dev(v[None])).cpu().numpy()[0]
     assert rel(got, ref) <= MATVEC_TOL
     aT = op.apply_T(_dev(v[None])).cpu().numpy()[0]
@@ -588,7 +589,7 @@ def test_dense_coupling_many_ct_blocks(O, M, p):
     rng = np.random.default_rng(M * 100 + p)
     xs = (np.arange(M) + 0.5) / M - 0.5
     centers = np.column_stack([xs, rng.uniform(-0.3, 0.3, M)])
-    sysm = grating.load_fixture("w10")
+    sysm = workloads.load_fixture("w10")
     pr = O.Problem(O.load_empty("w10"), centers, p, 0.012)
     op = solver.SchurOperator(sysm, centers, p, smat=pr.smat, dense_gb=40.0)
     assert op.dense

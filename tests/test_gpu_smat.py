@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 from conftest import rel
+import workloads  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -58,7 +59,7 @@ def _star_problem():
     z = np.load(os.path.join(GOLDEN, "golden_star.npz"))
     pb = O.load_problem(1)
     sm, _ = _device_smat("star3_w10")
-    return z, pb, sm, grating.load_fixture("w10")
+    return z, pb, sm, workloads.load_fixture("w10")
 
 
 def test_schur_with_rotated_stars_matches_oracle():
@@ -77,7 +78,7 @@ def test_solve_full_with_rotated_stars_matches_oracle(from_config):
     rotation phases per inclusion, (device-assembled) empty grating, GMRES."""
     from paper_1412_7466_b200 import grating, solver
     z, pb, sm, sysm = _star_problem()
-    systems = grating.fixture_config("w10") if from_config else sysm
+    systems = workloads.fixture_config("w10") if from_config else sysm
     sol = solver.solve_full(systems, pb.centers, pb.p, smat=sm, rot=z["rot"], device=0)
     assert rel(sol.c[0], z["c"]) <= 1e-9 and rel(sol.d[0], z["d"]) <= 1e-9
     assert abs(sol.flux[0]["error"] - float(z["flux_error"])) <= 1e-9

@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from conftest import rel
+import workloads  # noqa: E402
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -88,7 +89,7 @@ def test_overlap_domain_error(O):
     """overlapping disks -> domain error, radius-aware,
     phased copies included (ParticleSet.min_gap, geometry.py:131-144)."""
     from paper_1412_7466_b200 import DomainError, grating, multiscat, solver
-    sysm = grating.load_fixture("w10")
+    sysm = workloads.load_fixture("w10")
     pb = O.load_problem(1)
     ok = solver.SchurOperator(sysm, pb.centers, pb.p, radius=pb.radius)
     assert ok.min_gap >= 0.0
@@ -116,7 +117,7 @@ def test_zero_contrast_gives_empty_solution(O):
     the empty grating's (c, d vs A^+ f to 1e-8)."""
     from paper_1412_7466_b200 import grating, scatmat, solver
     pb = O.load_problem(1)
-    sysm = grating.load_fixture("w10")
+    sysm = workloads.load_fixture("w10")
     cfg = sysm.config
     S = scatmat.disk_scattering_matrix(pb.radius, cfg.k2, cfg.k2, pb.p)
     assert np.all(np.abs(S) <= 1e-15)
@@ -139,7 +140,7 @@ def test_preconditioner_equivalence_M5(O):
     p, R = 3, 0.04
     centers = np.array([[-0.31, 0.12], [-0.05, -0.21], [0.18, 0.3], [0.33, -0.05],
                         [0.02, 0.05]])
-    sysm = grating.load_fixture("w10")
+    sysm = workloads.load_fixture("w10")
     pr = O.Problem(O.load_empty("w10"), centers, p, R)
     op = solver.SchurOperator(sysm, centers, p, smat=pr.smat, radius=R)
     rhs = op.rhs()
@@ -164,7 +165,7 @@ def test_wall_field_kernels_match_reference(O, cfg):
     from paper_1412_7466_b200 import grating, solver
     z = np.load(os.path.join(GOLDEN, f"walls_cfg{cfg}.npz"))
     pb = O.load_problem(cfg)
-    op = solver.SchurOperator(grating.load_fixture("w10"), pb.centers, pb.p, smat=pb.smat)
+    op = solver.SchurOperator(workloads.load_fixture("w10"), pb.centers, pb.p, smat=pb.smat)
     eng = op.eng
     pts, layer = z["pts"], z["layer"]
     nrm = np.tile([1.0, 0.0], (pts.shape[0], 1))
@@ -193,7 +194,7 @@ def test_solution_diagnostics(O, cfg):
     reference checker's own value on the golden solution)."""
     from paper_1412_7466_b200 import grating, solver
     pb = O.load_problem(cfg)
-    sysm = grating.load_fixture(O.CONFIGS[cfg]["empty"])
+    sysm = workloads.load_fixture(O.CONFIGS[cfg]["empty"])
     sol = solver.solve_full(sysm, pb.centers, pb.p, smat=pb.smat)
     assert sol.residual[0] <= 1e-10
     assert sol.x_empty is not None and sol.x_empty.shape == (1, sysm.matrix.shape[1])
@@ -211,7 +212,7 @@ def test_coupled_residual_detects_a_wrong_beta(O):
     """The coupled residual is a real check: a perturbed beta fails it."""
     from paper_1412_7466_b200 import grating, postproc, solver
     pb = O.load_problem(1)
-    op = solver.SchurOperator(grating.load_fixture("w10"), pb.centers, pb.p, smat=pb.smat)
+    op = solver.SchurOperator(workloads.load_fixture("w10"), pb.centers, pb.p, smat=pb.smat)
     beta, _, _ = solver.gmres(op, op.rhs(), 1e-12, 150)
     good = postproc.coupled_residual(op, beta)[0]
     bad = postproc.coupled_residual(op, beta * (1 + 1e-3))[0]

@@ -18,6 +18,7 @@ import numpy as np
 
 ROOT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
 sys.path.insert(0, ROOT)
+import workloads  # noqa: E402
 
 
 def rel(a, b):
@@ -40,7 +41,7 @@ def main():
     names = ["w10_a00", "w10_a15"]
     p, R = 20, 0.004
     t0 = time.time()
-    op = solver.SchurOperator([grating.load_fixture(n) for n in names], centers, p, radius=R,
+    op = solver.SchurOperator([workloads.load_fixture(n) for n in names], centers, p, radius=R,
                               dense_gb=40.0 if a.dense else 0.0)
     M, L = op.M, op.L
     rng = np.random.default_rng(a.seed)

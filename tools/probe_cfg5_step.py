@@ -10,8 +10,9 @@ import numpy as np
 import torch
 
 from paper_1412_7466_b200 import grating, solver
+import workloads  # noqa: E402
 
-systems, centers, p, radius = grating.load_cfg5()
+systems, centers, p, radius = workloads.load_cfg5()
 with ThreadPoolExecutor(16) as ex:
     list(ex.map(grating.factorize, systems))
 op = solver.SchurOperator(systems, centers, p, radius=radius)

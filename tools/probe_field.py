@@ -12,8 +12,9 @@ import torch
 
 import periscat_oracle as O
 from paper_1412_7466_b200 import grating, postproc, solver
+import workloads  # noqa: E402
 
-sysm, centers, p, radius = grating.load_config(3)
+sysm, centers, p, radius = workloads.load_config(3)
 sol = solver.solve_full(sysm, centers, p, radius=radius)
 op = solver.SchurOperator(sysm, centers, p, radius=radius)
 beta = sol.beta

@@ -10,13 +10,14 @@ import torch
 
 from paper_1412_7466_b200 import _lib, grating, solver
 from paper_1412_7466_b200.scatmat import disk_scattering_matrix
+import workloads  # noqa: E402
 
 lib = _lib.load()
 tf, ms = ctypes.c_double(), ctypes.c_double()
 rc = lib.ps_dfma_peak(0, ctypes.byref(tf), ctypes.byref(ms))
 print(f"dfma peak rc={rc} {tf.value:.2f} TFLOP/s ({ms.value:.2f} ms)", flush=True)
 for cfg in (3, 2):
-    sysm, centers, p, radius = grating.load_config(cfg)
+    sysm, centers, p, radius = workloads.load_config(cfg)
     op = solver.SchurOperator(sysm, centers, p, radius=radius)
     M, L = op.M, op.L
     rng = np.random.default_rng(0)

@@ -3,7 +3,8 @@ import sys, os, math, numpy as np, torch
 sys.path.insert(0,'/root/repo')
 from paper_1412_7466_b200.engine import Engine
 from paper_1412_7466_b200 import grating
-_, centers, p, _ = grating.load_config(3)
+import workloads  # noqa: E402
+_, centers, p, _ = workloads.load_config(3)
 p = int(sys.argv[1]) if len(sys.argv) > 1 else p
 M=centers.shape[0]; L=2*p+1; R=16
 eng=Engine(0); eng.set_geometry(centers,p,12.0,1.0,1); eng.set_bloch(np.exp(1j*np.linspace(0,2,R)))

@@ -20,6 +20,7 @@ import torch
 from paper_1412_7466_b200 import grating, solver
 from paper_1412_7466_b200.engine import Engine
 from paper_1412_7466_b200.parallel import shard_range
+import workloads  # noqa: E402
 
 
 def timed(fn, n):
@@ -35,7 +36,7 @@ def timed(fn, n):
 
 
 def cfg3():
-    sysm, centers, p, radius = grating.load_config(3)
+    sysm, centers, p, radius = workloads.load_config(3)
     M, L = centers.shape[0], 2 * p + 1
     rng = np.random.default_rng(0)
     v = torch.as_tensor(rng.standard_normal((1, M, L)) + 1j * rng.standard_normal((1, M, L))).cuda()

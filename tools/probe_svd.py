@@ -2,7 +2,8 @@
 import time, numpy as np, torch, sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1412_7466_b200 import grating
-s = grating.load_fixture("w10")
+import workloads  # noqa: E402
+s = workloads.load_fixture("w10")
 A = torch.as_tensor(s.matrix).cuda()
 u0, s0, vh0 = np.linalg.svd(s.matrix, full_matrices=False)
 g = s.rhs

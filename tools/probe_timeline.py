@@ -8,8 +8,9 @@ import numpy as np
 import torch
 
 from paper_1412_7466_b200 import grating, solver
+import workloads  # noqa: E402
 
-sysm, centers, p, radius = grating.load_config(3)
+sysm, centers, p, radius = workloads.load_config(3)
 op = solver.SchurOperator(sysm, centers, p, radius=radius)
 rng = np.random.default_rng(0)
 v = torch.as_tensor(op.smat[None, None, :] * (rng.standard_normal((1, op.M, op.L))

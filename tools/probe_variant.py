@@ -9,8 +9,9 @@ import torch
 
 from paper_1412_7466_b200 import grating
 from paper_1412_7466_b200.engine import Engine
+import workloads  # noqa: E402
 
-sysm, centers, p, radius = grating.load_config(3)
+sysm, centers, p, radius = workloads.load_config(3)
 L = 2 * p + 1
 for M in (64, 100, 150, 200, 300, 400, 500, 700, 1000):
     eng = Engine(0)

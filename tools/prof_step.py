@@ -8,13 +8,14 @@ import numpy as np
 import torch
 
 from paper_1412_7466_b200 import grating, solver
+import workloads  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", type=int, default=3)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--k1-variant", type=int, default=0, help="0 auto, 1 tiled K1, 2 symmetric K1s")
 a = ap.parse_args()
-sysm, centers, p, radius = grating.load_config(a.cfg)
+sysm, centers, p, radius = workloads.load_config(a.cfg)
 op = solver.SchurOperator(sysm, centers, p, radius=radius)
 op.eng.set_k1_variant(a.k1_variant)
 rng = np.random.default_rng(0)

@@ -20,6 +20,7 @@ import torch
 from oracle import periscat_oracle as O
 from paper_1412_7466_b200 import grating, postproc, solver
 from paper_1412_7466_b200.engine import Engine
+import workloads  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--small", action="store_true", help="cfg1 only (racecheck is slow)")
@@ -34,7 +35,7 @@ rng = np.random.default_rng(0)
 cfgs = [1] if a.small else [1, 2]
 for cfg in cfgs:
     pb = O.load_problem(cfg)
-    sysm = grating.load_fixture("w10")
+    sysm = workloads.load_fixture("w10")
     for dense_gb in (40.0, 0.0):
         op = solver.SchurOperator(sysm, pb.centers, pb.p, smat=pb.smat, dense_gb=dense_gb)
         v = torch.as_tensor(pb.smat[None, None, :] * cplx(rng, (1, pb.M, pb.L))).cuda()
@@ -59,12 +60,12 @@ for cfg in cfgs:
         print(f"cfg{cfg} mrhs variant {variant} ok", flush=True)
 # batched-RHS coupled operator (matrix-free + dense), generic Krylov driver
 pb = O.load_problem(1)
-systems = [grating.load_fixture(n) for n in ("w10", "w10_a00", "w10_a15")]
+systems = [workloads.load_fixture(n) for n in ("w10", "w10_a00", "w10_a15")]
 op = solver.SchurOperator(systems, pb.centers, pb.p, smat=pb.smat)
 x, its, hist = solver.gmres(lambda t: op(t), op.rhs(), 1e-10, 30, engine=op.eng)
 print("multi-RHS generic gmres", its, flush=True)
 # device empty-grating setup + field evaluation
-sol = solver.solve_full(grating.fixture_config("w10"), pb.centers, pb.p, smat=pb.smat)
+sol = solver.solve_full(workloads.fixture_config("w10"), pb.centers, pb.p, smat=pb.smat)
 print("device setup solve", sol.iterations, sol.coupled_residual, flush=True)
 # Muller BIE scattering matrix of a star
 from paper_1412_7466_b200 import scatmat  # noqa: E402

@@ -30,6 +30,7 @@ import numpy as np
 import torch
 
 from paper_1412_7466_b200 import grating, postproc, solver
+import workloads  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--check", action="store_true")
@@ -43,13 +44,13 @@ a = ap.parse_args()
 
 t0 = time.perf_counter()
 if a.host_setup:
-    systems, centers, p, radius = grating.load_cfg5()
+    systems, centers, p, radius = workloads.load_cfg5()
     with ThreadPoolExecutor(16) as ex:      # 16 host SVDs (empty_grating.factorize) in parallel
         list(ex.map(grating.factorize, systems))
 else:                                       # configs only: assembly + SVD on the device
     centers = np.load(os.path.join(grating.GOLDEN, "centers_cfg5.npy"))
     p, radius = 20, 0.004
-    systems = [grating.fixture_config(n) for n in grating.CFG5_ANGLES]
+    systems = [workloads.fixture_config(n) for n in workloads.CFG5_ANGLES]
 t_svd = time.perf_counter() - t0
 
 world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -109,7 +110,7 @@ if a.check and world == 1:
     sl = np.r_[0:4, 5000:5004, 9996:10000]
     checks = {}
     for r in (0, 15):
-        es = O.load_empty(grating.CFG5_ANGLES[r])
+        es = O.load_empty(workloads.CFG5_ANGLES[r])
         pb = O.Problem(es, centers, p, radius)
         ts = time.perf_counter()
         u = O.apply_T(bh[r], centers, es.k2, p, es.bloch, es.period, es.copies, targets=sl)
@@ -142,7 +143,7 @@ if a.check_full and world == 1:
     ts = time.perf_counter()
     bh = beta.cpu().numpy()[0]
     rh = rhs.cpu().numpy()[0]
-    es = O.load_empty(grating.CFG5_ANGLES[0])
+    es = O.load_empty(workloads.CFG5_ANGLES[0])
     pb = O.Problem(es, centers, p, radius)
     xg = es.apply_pinv(O.apply_C(es, bh, centers))
     _FULL.update(beta=bh, centers=centers, es=es, p=p)

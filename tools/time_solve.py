@@ -10,9 +10,10 @@ import torch
 from paper_1412_7466_b200 import grating, postproc, solver
 from paper_1412_7466_b200.engine import Engine
 from paper_1412_7466_b200.scatmat import disk_scattering_matrix
+import workloads  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-sysm, centers, p, radius = grating.load_config(cfg)
+sysm, centers, p, radius = workloads.load_config(cfg)
 for rep in range(3):
     T = {}
     t = time.perf_counter()
