@@ -110,7 +110,36 @@ __device__ __forceinline__ void consume(const double2* __restrict__ spe, const d
       ws[q] = nxt.x + nxt.y;
     }
   };
-  static_for<S::L>(step);
+  if constexpr (VB == 6) {
+    // runtime loop over chunks of BO steps (u = step within the chunk is
+    // static), then the static tail
+    constexpr int NC = S::L / BO, TL = S::L % BO;
+    const double2* bsrc0 = bsrc;
+    const double* ssrc0 = ssrc;
+#pragma unroll 1
+    for (int ch = 0; ch < NC; ++ch) {
+      static_for<BO>([&](auto u_c) {
+        constexpr int u = decltype(u_c)::value;
+        const int n = ch * BO + u;
+        const double2 nxt = (((R0 + 1 + u) / BO) & 1 ? spo : spe)[(n + 1) * kTT];
+        const double2 bb = __ldg(bsrc0 + n);
+        const double bs = __ldg(ssrc0 + n);
+#pragma unroll
+        for (int i = 0; i < BO; ++i) acc[0][i] = fma(bb.x, wx[(R0 + u - i + MODB) % BO], acc[0][i]);
+#pragma unroll
+        for (int i = 0; i < BO; ++i) acc[1][i] = fma(bb.y, wy[(R0 + u - i + MODB) % BO], acc[1][i]);
+#pragma unroll
+        for (int i = 0; i < BO; ++i) acc[2][i] = fma(bs, ws[(R0 + u - i + MODB) % BO], acc[2][i]);
+        constexpr int q = (R0 + u + 1 + MODB) % BO;
+        wx[q] = nxt.x;
+        wy[q] = nxt.y;
+        ws[q] = nxt.x + nxt.y;
+      });
+    }
+    static_for<TL>([&](auto u_c) { step(IC<NC * BO + decltype(u_c)::value>{}); });
+  } else {
+    static_for<S::L>(step);
+  }
 }
 
 template <int P, int VB, int SYNC, int ORD = 0, int PF = 0, int NB = 4, int SWAP = 0>
@@ -208,10 +237,8 @@ int main() {
   cudaMemset(bw, 0, nsrc * 51 * sizeof(double2));
   cudaMemset(bws, 0, nsrc * 51 * sizeof(double));
   run<25, 0, 1>("ldg coef + sync (K1s)", bw, bws, nsrc, sms, out);
-  run<25, 0, 1, 0, 0, 4, 1>("ldg, swapped fma operands", bw, bws, nsrc, sms, out);
-  run<25, 0, 1, 0, 0, 2, 0>("ldg, 2 row blocks (BO=26)", bw, bws, nsrc, sms, out);
-  run<25, 0, 1, 0, 0, 2, 1>("ldg, 2 row blocks, swapped", bw, bws, nsrc, sms, out);
+  run<25, 6, 1>("ldg, chunked runtime loop", bw, bws, nsrc, sms, out);
   run<20, 0, 1>("ldg coef + sync (K1s)", bw, bws, nsrc, sms, out);
-  run<20, 0, 1, 0, 0, 2, 0>("ldg, 2 row blocks (BO=21)", bw, bws, nsrc, sms, out);
+  run<20, 6, 1>("ldg, chunked runtime loop", bw, bws, nsrc, sms, out);
   return 0;
 }
