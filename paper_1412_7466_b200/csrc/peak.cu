@@ -15,13 +15,18 @@ namespace {
 // oversubscribed residency and read 34.2).
 constexpr int kChains = 8;
 constexpr int kCtasPerSm = 8;
-__global__ void __launch_bounds__(256) dfma_chains(double* out, int iters, double a, double b) {
+// The multiplier and addend are literals (constant-bank operands), so every
+// DFMA reads ONE vector register: with both as kernel arguments the second
+// one occupies a register operand and the chain reads 34.2 TF/s -- the DFMA
+// rate is bounded by register-file operand bandwidth (tools/fp64_pipes.cu,
+// tools/k1s_consumer_bench.cu), not only by the pipe.
+__global__ void __launch_bounds__(256) dfma_chains(double* out, int iters, double, double) {
   double x[kChains];
 #pragma unroll
   for (int i = 0; i < kChains; ++i) x[i] = threadIdx.x * 1e-3 + i;
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int i = 0; i < kChains; ++i) x[i] = fma(x[i], a, b);
+    for (int i = 0; i < kChains; ++i) x[i] = fma(x[i], 0.9999999, 1e-7);
   }
   double s = 0;
 #pragma unroll
