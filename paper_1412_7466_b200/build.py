@@ -12,7 +12,7 @@ import time
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libperiscat_b200.so")
-SOURCES = ["m2l.cu", "m2l_mrhs.cu", "m2l_sym.cu", "m2l_mma.cu", "coupling.cu", "coupling_dense.cu", "gmres.cu", "field.cu", "empty.cu", "scatmat.cu", "capi.cu", "peak.cu"]
+SOURCES = ["m2l.cu", "m2l_mrhs.cu", "m2l_sym.cu", "m2l_symh.cu", "m2l_mma.cu", "coupling.cu", "coupling_dense.cu", "gmres.cu", "field.cu", "empty.cu", "scatmat.cu", "capi.cu", "peak.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

@@ -791,8 +791,8 @@ int ps_precompute_coupling(ps_ctx* h, double max_gb) {
 int ps_set_k1_variant(ps_ctx* h, int variant) {
   if (!h) return PS_ERR_ARG;
   Ctx* c = C(h);
-  if (variant < 0 || variant > 2) {
-    c->err = "ps_set_k1_variant: 0 auto, 1 tiled, 2 symmetric";
+  if (variant < 0 || variant > 3) {
+    c->err = "ps_set_k1_variant: 0 auto, 1 tiled, 2 symmetric (DFMA), 3 symmetric (DMMA)";
     return PS_ERR_ARG;
   }
   c->k1_variant = variant;

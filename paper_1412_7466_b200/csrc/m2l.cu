@@ -399,7 +399,7 @@ bool m2l_sym_selected(const Ctx* ctx) {
   const bool full = ctx->t_begin == 0 && ctx->t_end == ctx->M;
   // crossover measured with tools/probe_variant.py (Karatsuba K1 / K1s): the
   // symmetric kernel wins from M ~ 500 (4% at M = 1000), the tiled one below
-  const bool sym = ctx->k1_variant == 2 || (ctx->k1_variant == 0 && full && ctx->M >= 512);
+  const bool sym = ctx->k1_variant >= 2 || (ctx->k1_variant == 0 && full && ctx->M >= 512);
   return sym && full;
 }
 

@@ -28,6 +28,7 @@
 
 #include "ctx.cuh"
 #include "m2l.cuh"
+#include "m2l_sym.cuh"
 #include "symbols.cuh"
 
 namespace ps {
@@ -71,36 +72,6 @@ struct ShapeS {
   static constexpr int SYM = kTT * SJ;            // double2 per buffer
   static constexpr size_t SMEM = 2 * (size_t)SYM * sizeof(double2);
 };
-
-struct ArgsS {
-  const double* centers;   // [M][2]
-  const double2* bw;       // [M * ncp][L] bloch-weighted beta per source image
-  const double* bws;       // [M * ncp][L] re + im of bw (Karatsuba operand)
-  const double2* bwr;      // (-1)^(n-P) bw: coefficients of the reverse apply
-  const double* bwsr;      // (-1)^(n-P) bws
-  double2* apart;          // [G][maxseg][kTT][L]  forward parts, one per (CTA, block row)
-  double2* bpart;          // [NB][kTT][L]         reverse parts, one per cross block
-  int M, T, NB, copies, ncp, maxseg;
-  long long kb0, nb;       // block range [kb0, kb0 + nb) of this launch (multi-GPU part)
-  double period, k2;
-};
-
-__device__ __forceinline__ long long tri_off(int a, int T) {   // blocks with first tile < a
-  return (long long)a * T - (long long)a * (a - 1) / 2;
-}
-
-__device__ __forceinline__ void block_ab(long long k, int T, int& A, int& B) {
-  int a = 0;
-  // small T: linear scan from a floating estimate
-  double disc = (2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * (double)k;
-  a = (int)(((2.0 * T + 1.0) - sqrt(disc > 0 ? disc : 0)) * 0.5);
-  if (a < 0) a = 0;
-  if (a > T - 1) a = T - 1;
-  while (a > 0 && tri_off(a, T) > k) --a;
-  while (a < T - 1 && tri_off(a + 1, T) <= k) ++a;
-  A = a;
-  B = a + (int)(k - tri_off(a, T));
-}
 
 // Shared-memory layout of a batch: element (row (m, j), slot) at
 //   j * SJ + slot * kTT + (m ^ sw(slot)),   sw(slot) = 4 * ((slot / BO) & 1).
@@ -512,27 +483,33 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   const size_t na = (size_t)G * a.maxseg * kTT * S::L;
   const size_t nbp = (size_t)a.NB * kTT * S::L;
   const size_t npart = na + nbp;
+  const bool hmma = ctx->k1_variant == 3;      // K1h (m2l_symh.cu): its own padded weights
   const size_t nbw = (size_t)ctx->M * a.ncp * S::L;
-  if (ctx->partial_elems < npart + 4 * nbw) {
+  const size_t nwts = hmma ? symh_weight_elems(P, ctx->M, a.ncp) : 4 * nbw;
+  if (ctx->partial_elems < npart + nwts) {
     if (ctx->d_partial) ps::dev_free(ctx->d_partial);
     ctx->d_partial = nullptr;
     ctx->partial_elems = 0;
-    PS_CUDA_TRY(ctx, ps::dev_malloc(&ctx->d_partial, (npart + 4 * nbw) * sizeof(double2)));
-    ctx->partial_elems = npart + 4 * nbw;
+    PS_CUDA_TRY(ctx, ps::dev_malloc(&ctx->d_partial, (npart + nwts) * sizeof(double2)));
+    ctx->partial_elems = npart + nwts;
   }
   a.apart = ctx->d_partial;
   a.bpart = ctx->d_partial + na;
   double2* bw = ctx->d_partial + npart;
-  a.bw = bw;
-  double* bws = reinterpret_cast<double*>(bw + nbw);
-  double2* bwr = bw + 2 * nbw;
-  double* bwsr = reinterpret_cast<double*>(bw + 3 * nbw);
-  a.bws = bws;
-  a.bwr = bwr;
-  a.bwsr = bwsr;
-  bloch_weight_1<<<2 * ctx->sm_count, 256, 0, ks>>>(beta, bpow - 1, ctx->M, S::L, a.ncp, bw, bws,
-                                                    bwr, bwsr);
-  PS_CUDA_TRY(ctx, cudaGetLastError());
+  if (hmma) {
+    PS_CUDA_TRY(ctx, (cudaError_t)symh_weights(P, &a, beta, bpow - 1, bw, ctx->sm_count, ks));
+  } else {
+    a.bw = bw;
+    double* bws = reinterpret_cast<double*>(bw + nbw);
+    double2* bwr = bw + 2 * nbw;
+    double* bwsr = reinterpret_cast<double*>(bw + 3 * nbw);
+    a.bws = bws;
+    a.bwr = bwr;
+    a.bwsr = bwsr;
+    bloch_weight_1<<<2 * ctx->sm_count, 256, 0, ks>>>(beta, bpow - 1, ctx->M, S::L, a.ncp, bw, bws,
+                                                      bwr, bwsr);
+    PS_CUDA_TRY(ctx, cudaGetLastError());
+  }
   if (ov) PS_CUDA_TRY(ctx, cudaEventRecord(ov->bw_done, ks));
   static unsigned long long attr_mask = 0;
   if (first_on_device(&attr_mask, ctx->device)) {
@@ -545,8 +522,12 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
     PS_CUDA_TRY(ctx, cudaEventCreate(&e1));
     PS_CUDA_TRY(ctx, cudaEventRecord(e0, ks));
   }
-  m2l_sym_kernel<P><<<G, kThreads, S::SMEM, ks>>>(a);
-  PS_CUDA_TRY(ctx, cudaGetLastError());
+  if (ctx->k1_variant == 3) {                   // K1h: DMMA consumers (m2l_symh.cu)
+    PS_CUDA_TRY(ctx, (cudaError_t)symh_kernel(P, a, G, ks, ctx->device));
+  } else {
+    m2l_sym_kernel<P><<<G, kThreads, S::SMEM, ks>>>(a);
+    PS_CUDA_TRY(ctx, cudaGetLastError());
+  }
   if (ctx->profile) {
     PS_CUDA_TRY(ctx, cudaEventRecord(e1, ks));
     ctx->k1_events.push_back({e0, e1});

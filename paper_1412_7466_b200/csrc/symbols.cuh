@@ -94,4 +94,47 @@ PS_HD void hankel_symbols_half(double z, double c, double s, int N, bool mirror,
   }
 }
 
+
+// Same output as hankel_symbols_half, arranged for a short dependency chain
+// (producers that share the FP64 pipe with tensor-core or DFMA consumers are
+// latency-bound): the reference's own upward recurrence on the unphased
+// H_nu = J_nu + i Y_nu (sf:54-67; one FMA per order on each real chain, the
+// factor nu * 2/z off the chain), times phases w^nu kept as two power chains
+// (even / odd nu, stepping by w^2).  The mirror lane uses w = -e^{-i phi}, so
+// (-1)^nu H_nu e^{-i nu phi} = H_nu w^nu needs no sign handling.
+template <int NU, typename Out>
+PS_HD void hankel_symbols_ilp(double z, double c, double s, int N, bool mirror, Out out) {
+  double j0, j1, y0, y1;
+  bessel_jy01(z, N, &j0, &j1, &y0, &y1);
+  if (!mirror) out(0, j0, y0);
+  const double wr = mirror ? -c : c, wi = s;   // mirror: -e^{-i phi} = (-c, s)
+  const double w2r = fma(wr, wr, -wi * wi), w2i = 2.0 * wr * wi;
+  const double tz = 2.0 / z;
+  double hmr = j0, hmi = y0;      // H_{nu-1}
+  double hr = j1, hi = y1;        // H_nu
+  double per = 1.0, pei = 0.0;    // w^nu for the even chain (nu = 0 here)
+  double por = wr, poi = wi;      // w^nu for the odd chain (nu = 1 here)
+#pragma unroll
+  for (int nu = 1; nu <= NU; ++nu) {
+    const bool odd = nu & 1;
+    if (!odd) {                   // even chain: w^{nu} = w^{nu-2} w^2
+      const double r = fma(per, w2r, -pei * w2i), i = fma(per, w2i, pei * w2r);
+      per = r;
+      pei = i;
+    } else if (nu > 1) {
+      const double r = fma(por, w2r, -poi * w2i), i = fma(por, w2i, poi * w2r);
+      por = r;
+      poi = i;
+    }
+    const double pr = odd ? por : per, pi = odd ? poi : pei;
+    out(mirror ? -nu : nu, fma(hr, pr, -hi * pi), fma(hr, pi, hi * pr));
+    const double cf = (double)nu * tz;
+    const double nr = fma(cf, hr, -hmr), ni = fma(cf, hi, -hmi);
+    hmr = hr;
+    hmi = hi;
+    hr = nr;
+    hi = ni;
+  }
+}
+
 }  // namespace ps

@@ -71,11 +71,11 @@ def test_apply_T_small_orders(O, p, copies, M):
         assert rel(got, ref) <= MATVEC_TOL
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 3])
 @pytest.mark.parametrize("p,copies,M", [(0, 1, 1), (1, 1, 2), (2, 0, 17), (3, 1, 9), (7, 2, 33),
                                         (12, 1, 24), (20, 1, 41), (25, 1, 70)])
 def test_apply_T_small_orders_kernel_variants(O, variant, p, copies, M):
-    """Tiled K1 (1) and symmetric K1s (2) forced at every block size BO the
+    """Tiled K1 (1), symmetric K1s (2) and its DMMA form K1h (3) forced at every block size BO the
     swizzled K1s layout sees (p = 0..25), ragged tiles, 0..2 image copies."""
     import torch
     from paper_1412_7466_b200.engine import Engine
@@ -372,9 +372,9 @@ def test_mrhs_variants(O, variant, nrhs, p, M):
 
 
 # ---------------------------------------------------------------- K1 variants / shards
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 3])
 def test_k1_variants_full_range(O, variant):
-    """Tiled K1 (1) and symmetric K1s (2) on cfg2, random and Krylov-scaled input."""
+    """Tiled K1 (1), symmetric K1s (2) and K1h (3) on cfg2, random and Krylov-scaled input."""
     from paper_1412_7466_b200.engine import Engine
     pb = O.load_problem(2)
     rng = np.random.default_rng(50 + variant)
