@@ -209,36 +209,51 @@ __global__ void sum_splits(const double2* __restrict__ part, int nsplit, int n,
 }
 
 // ---------------------------------------------------------------- K4: A^+ g
-// h[k] = sinv[k] * sum_i Uh[k][i] g[i]      (one warp per k)
-__global__ void pinv_uh(const double2* __restrict__ Uh, const double* __restrict__ sinv,
-                        const double2* __restrict__ g, int nsv, int nrc, double2* __restrict__ h) {
-  const int k = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (k >= nsv) return;
-  const double2* u = Uh + (size_t)k * nrc;
+// y[r] = scale[r] * sum_k A[r][k] x[k]: kRowT threads per row (kRows rows per
+// CTA), each thread's strided elements loaded before any FMA (independent
+// loads in flight), warp shuffles then the row's warps summed in warp order
+// through shared memory (deterministic).  781 / 635 rows of 576 / 781 complex
+// entries: ~400 CTAs instead of ~100 warp-per-row blocks.
+constexpr int kRowT = 128, kRows = 2;
+__global__ void __launch_bounds__(kRowT * kRows) pinv_gemv(const double2* __restrict__ A,
+                                                           const double* __restrict__ scale,
+                                                           const double2* __restrict__ x, int nrow,
+                                                           int ncol, double2* __restrict__ y) {
+  __shared__ double2 red[kRows][kRowT / 32];
+  const int rl = threadIdx.x / kRowT, t = threadIdx.x % kRowT;
+  const int r = blockIdx.x * kRows + rl;
   double2 s = make_double2(0, 0);
-  for (int i = lane; i < nrc; i += 32) s = cfma(u[i], g[i], s);
+  if (r < nrow) {
+    // every element of the thread's stride in flight at once (ncol <= 8 kRowT
+    // here: 576 / 781), then the FMAs in order
+    const double2* a = A + (size_t)r * ncol;
+    constexpr int U = 8;
+    double2 av[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = t + u * kRowT;
+      av[u] = k < ncol ? __ldg(a + k) : make_double2(0, 0);
+      xv[u] = k < ncol ? __ldg(x + k) : make_double2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) s = cfma(av[u], xv[u], s);
+    for (int k = t + U * kRowT; k < ncol; k += kRowT) s = cfma(__ldg(a + k), __ldg(x + k), s);
+  }
   for (int o = 16; o > 0; o >>= 1) {
     s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
     s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
   }
-  if (lane == 0) h[k] = make_double2(s.x * sinv[k], s.y * sinv[k]);
-}
-
-// x[o] = cscale[o] * sum_k Vb[o][k] h[k]     (one warp per output column)
-__global__ void pinv_v(const double2* __restrict__ Vb, const double* __restrict__ cs,
-                       const double2* __restrict__ h, int nout, int nsv, double2* __restrict__ x) {
-  const int o = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (o >= nout) return;
-  const double2* v = Vb + (size_t)o * nsv;
-  double2 s = make_double2(0, 0);
-  for (int k = lane; k < nsv; k += 32) s = cfma(v[k], h[k], s);
-  for (int d = 16; d > 0; d >>= 1) {
-    s.x += __shfl_xor_sync(0xffffffffu, s.x, d);
-    s.y += __shfl_xor_sync(0xffffffffu, s.y, d);
+  if ((t & 31) == 0) red[rl][t / 32] = s;
+  __syncthreads();
+  if (t == 0 && r < nrow) {
+    double2 v = red[rl][0];
+#pragma unroll
+    for (int w = 1; w < kRowT / 32; ++w) {
+      v.x += red[rl][w].x;
+      v.y += red[rl][w].y;
+    }
+    y[r] = make_double2(v.x * scale[r], v.y * scale[r]);
   }
-  if (lane == 0) x[o] = make_double2(s.x * cs[o], s.y * cs[o]);
 }
 
 // g_out = f - g_in  (recovery right-hand side)
@@ -602,9 +617,12 @@ int pinv(Ctx* c, int r, const double2* g, double2* x, int nout, cudaStream_t st)
   const RhsData& R = c->rhs[r];
   Work w;
   if (int rc = work(c, r, &w)) return rc;
-  pinv_uh<<<(c->nsv + 7) / 8, 256, 0, st>>>(R.d_Uh, R.d_sinv, g, c->nsv, c->nrow_c, w.h);
+  // h = sinv * (U^* g) over the C rows, then x = cscale * (V h) over the read columns
+  pinv_gemv<<<(c->nsv + kRows - 1) / kRows, kRowT * kRows, 0, st>>>(R.d_Uh, R.d_sinv, g, c->nsv,
+                                                                      c->nrow_c, w.h);
   PS_CUDA_TRY(c, cudaGetLastError());
-  pinv_v<<<(nout + 7) / 8, 256, 0, st>>>(R.d_Vb, R.d_cscale, w.h, nout, c->nsv, x);
+  pinv_gemv<<<(nout + kRows - 1) / kRows, kRowT * kRows, 0, st>>>(R.d_Vb, R.d_cscale, w.h, nout,
+                                                                  c->nsv, x);
   PS_CUDA_TRY(c, cudaGetLastError());
   c->launches += 2;
   return PS_OK;
