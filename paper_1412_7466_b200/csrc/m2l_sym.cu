@@ -56,7 +56,7 @@ constexpr int kThreads = (kCW + kPW) * 32;
 #define PS_K1S_CREGS 216
 #endif
 constexpr int kConsumerRegs = PS_K1S_CREGS;
-constexpr int kProducerRegs = 504 - 2 * PS_K1S_CREGS;   // 3 warps x 168 per sub-partition
+constexpr int kProducerRegs = 504 - 2 * PS_K1S_CREGS;   // the CTA holds 168 x 384 registers (launch bound): 2 C + Pr <= 3 x 168
 static_assert(kProducerRegs >= 24 && kProducerRegs % 8 == 0, "setmaxnreg range");
 static_assert(2 * kTT * kTT == kPW * 32, "64 rows: two producer lanes per row");
 

@@ -13,11 +13,17 @@ import workloads  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", type=int, default=3)
 ap.add_argument("--steps", type=int, default=3)
-ap.add_argument("--k1-variant", type=int, default=0, help="0 auto, 1 tiled K1, 2 symmetric K1s")
+ap.add_argument("--k1-variant", type=int, default=0, help="0 auto, 1 tiled K1, 2 symmetric K1s, 3 K1h")
+ap.add_argument("--overlap", type=int, default=None, help="SMs left to the coupling chain")
+ap.add_argument("--order", type=int, default=None, help="0 chain first, 1 K1s first")
 a = ap.parse_args()
 sysm, centers, p, radius = workloads.load_config(a.cfg)
 op = solver.SchurOperator(sysm, centers, p, radius=radius)
 op.eng.set_k1_variant(a.k1_variant)
+if a.overlap is not None:
+    op.eng.set_overlap(a.overlap)
+if a.order is not None:
+    op.eng.set_overlap_order(a.order)
 rng = np.random.default_rng(0)
 v = op.smat[None, None, :] * (rng.standard_normal((1, op.M, op.L)) + 1j * rng.standard_normal((1, op.M, op.L)))
 v = torch.as_tensor(v).cuda()
