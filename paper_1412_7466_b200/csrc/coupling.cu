@@ -232,12 +232,12 @@ __global__ void __launch_bounds__(kRowT * kRows) pinv_gemv(const double2* __rest
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int k = t + u * kRowT;
-      av[u] = k < ncol ? __ldg(a + k) : make_double2(0, 0);
+      av[u] = k < ncol ? __ldcs(a + k) : make_double2(0, 0);
       xv[u] = k < ncol ? __ldg(x + k) : make_double2(0, 0);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) s = cfma(av[u], xv[u], s);
-    for (int k = t + U * kRowT; k < ncol; k += kRowT) s = cfma(__ldg(a + k), __ldg(x + k), s);
+    for (int k = t + U * kRowT; k < ncol; k += kRowT) s = cfma(__ldcs(a + k), __ldg(x + k), s);
   }
   for (int o = 16; o > 0; o >>= 1) {
     s.x += __shfl_xor_sync(0xffffffffu, s.x, o);

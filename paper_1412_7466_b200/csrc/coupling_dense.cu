@@ -276,7 +276,9 @@ __global__ void b_gemv(const double2* __restrict__ B, const double2* __restrict_
   if (row >= nrows) return;
   const double2* br = B + (size_t)row * ncol;
   double2 acc = make_double2(0, 0);
-  for (int c = lane; c < ncol; c += 32) acc = cfma(br[c], xs[c], acc);
+  // streamed once per matvec: evict-first, so the 0.45 GB pass does not push
+  // the K1s partial sums (L2-resident, read by k1s_reduce) out to DRAM
+  for (int c = lane; c < ncol; c += 32) acc = cfma(__ldcs(br + c), xs[c], acc);
   for (int o = 16; o > 0; o >>= 1) {
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
     acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);

@@ -534,6 +534,27 @@ def test_matvec_and_solve_are_bit_reproducible(O, cfg, nrhs):
         assert torch.equal(x1, x2)
 
 
+def test_k1h_bit_reproducible_and_matches_k1s(O):
+    """The opt-in DMMA variant of the symmetric M2L (K1h, variant 3) keeps the
+    deterministic order (repeat launches bitwise identical) and equals K1s
+    to rounding on cfg3 with Krylov-scaled input."""
+    from paper_1412_7466_b200.engine import Engine
+    pb = O.load_problem(3)
+    rng = np.random.default_rng(123)
+    beta = _dev(pb.smat[None, None, :] * _cplx(rng, (1, pb.M, pb.L)))
+    eng = Engine(0)
+    eng.set_geometry(pb.centers, pb.p, pb.es.k2, pb.es.period, pb.es.copies)
+    eng.set_bloch([pb.es.bloch])
+    eng.set_k1_variant(3)
+    y0 = eng.apply_T(beta).cpu().numpy()
+    for _ in range(2):
+        assert np.array_equal(eng.apply_T(beta).cpu().numpy(), y0)
+    eng.set_k1_variant(2)
+    ys = eng.apply_T(beta).cpu().numpy()
+    eng.close()
+    assert rel(y0, ys) <= 1e-13
+
+
 _FULL3 = {}
 
 

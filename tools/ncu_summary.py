@@ -83,20 +83,22 @@ def launches(path, out):
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         short = re.sub(r"\(.*", "", k)[:70]
         lines.append(f"| `{short}` | {len(v)} | {sum(v) / len(v):.1f} | {sum(v) / tot * 100:.1f}% |")
-    # shares within the timed Schur step only (drop the peak microbenchmarks,
-    # the one-off coupling-block builds, torch's L2-flush fill and the GMRES
-    # kernels of the full-solve block)
-    skip = re.compile(r"chains|build_kernel|FillFunctor|dot_|norm2_|axpy_|givens|scale_into|"
-                      r"cadd_rows|init_state|diag_s_apply|back_solve")
-    step = {k: v for k, v in agg.items() if not skip.search(k)}
-    ts = sum(sum(v) / len(v) for v in step.values())
-    lines += ["", "per Schur step (mean launch time of each step kernel; shares of their sum):", "",
-              "| kernel | mean us | share of step |", "|---|---|---|"]
-    for k, v in sorted(step.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
+    # the timed Schur step only: the kernels one SM-partitioned cfg3 step
+    # launches (setup, GMRES, SVD, peaks and torch's L2-flush fills excluded),
+    # each kernel's total time divided by the number of steps (= K1s launches)
+    step_re = re.compile(r"bloch_weight_1|ct_gemv|sum_parts|pinv_gemv|pinv_uh|pinv_v|b_gemv|"
+                         r"m2l_sym_kernel|k1s_reduce")
+    nsteps = sum(len(v) for k, v in agg.items() if "m2l_sym_kernel" in k) or 1
+    step = {k: v for k, v in agg.items() if step_re.search(k)}
+    ts = sum(sum(v) for v in step.values()) / nsteps
+    lines += ["", f"per Schur step ({nsteps} steps = K1s launches; every step kernel's total time / "
+              "steps; shares of their sum):", "",
+              "| kernel | launches per step | us per step | share of step |", "|---|---|---|---|"]
+    for k, v in sorted(step.items(), key=lambda kv: -sum(kv[1])):
         short = re.sub(r"\(.*", "", k)[:70]
-        m = sum(v) / len(v)
-        lines.append(f"| `{short}` | {m:.1f} | {m / ts * 100:.1f}% |")
-    lines.append(f"| total | {ts:.1f} | |")
+        m = sum(v) / nsteps
+        lines.append(f"| `{short}` | {len(v) / nsteps:g} | {m:.1f} | {m / ts * 100:.1f}% |")
+    lines.append(f"| total | | {ts:.1f} | |")
     open(out, "w").write("\n".join(lines) + "\n")
 
 
