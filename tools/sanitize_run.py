@@ -39,7 +39,7 @@ for cfg in cfgs:
     for dense_gb in (40.0, 0.0):
         op = solver.SchurOperator(sysm, pb.centers, pb.p, smat=pb.smat, dense_gb=dense_gb)
         v = torch.as_tensor(pb.smat[None, None, :] * cplx(rng, (1, pb.M, pb.L))).cuda()
-        for variant in (1, 2):                      # K1 tiled, K1s symmetric
+        for variant in (1, 2, 3):                   # K1 tiled, K1s symmetric, K1h (DMMA)
             op.eng.set_k1_variant(variant)
             for ov in (-1, 2):                      # serial, SM-partitioned
                 op.eng.set_overlap(ov)
