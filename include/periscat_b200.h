@@ -112,7 +112,9 @@ int ps_set_pinv(ps_ctx* ctx, int irhs, int nrow, int ncol, const double* U_host,
 int ps_precompute_coupling(ps_ctx* ctx, double max_gb);
 /* Single-RHS M2L kernel choice: 0 auto (symmetric K1s -- each Graf symbol
  * row serves the pair and its reverse -- when this context owns every
- * target, else tiled K1), 1 force tiled K1, 2 force K1s (full range only). */
+ * target, else tiled K1), 1 force tiled K1, 2 force K1s (full range only),
+ * 3 force K1h: K1s's schedule with the Toeplitz applies on the FP64 tensor
+ * cores (banded Hankel DMMA; measured slower than K1s, kept opt-in). */
 int ps_set_k1_variant(ps_ctx* ctx, int variant);
 /* Multi-RHS M2L kernel choice: 0 auto (FP64 tensor cores, mma.sync f64, for
  * >= 12 RHS; below that one single-RHS launch per RHS), 1 force the DFMA

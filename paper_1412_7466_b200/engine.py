@@ -202,7 +202,7 @@ class Engine:
         self.coupled = True
 
     def set_k1_variant(self, variant: int):
-        """0 auto, 1 tiled K1, 2 symmetric K1s (see include/periscat_b200.h)."""
+        """0 auto, 1 tiled K1, 2 symmetric K1s, 3 K1h (K1s on DMMA, opt-in); see include/periscat_b200.h."""
         self._check(self.lib.ps_set_k1_variant(self.ctx, int(variant)))
 
     def set_overlap(self, sms: int):
