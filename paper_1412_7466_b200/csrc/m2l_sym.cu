@@ -258,7 +258,9 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
           B = A;
         }
       }
+#ifndef PS_K1S_NOPROD   // experiment: consumers alone (wrong results)
       if (it + 1 < nbat) produce_s<P>(a, A, B, li, (it & 1) ? sym0 : sym1, pw, lane);
+#endif
       __syncthreads();
     }
     return;
