@@ -116,6 +116,15 @@ int ps_precompute_coupling(ps_ctx* ctx, double max_gb);
  * 3 force K1h: K1s's schedule with the Toeplitz applies on the FP64 tensor
  * cores (banded Hankel DMMA; measured slower than K1s, kept opt-in). */
 int ps_set_k1_variant(ps_ctx* ctx, int variant);
+/* Symbol store of the symmetric single-RHS M2L (K1s): the translation symbols
+ * t_nu(x_m - x_j - l d) of every tile-pair batch depend only on the geometry,
+ * so the first launch after ps_set_geometry writes them to device memory in
+ * the kernel's shared-memory layout (2.5 GB at BASELINE cfg3) and every later
+ * launch bulk-copies them instead of regenerating them.  max_gb bounds the
+ * store (default 32; 0 regenerates the symbols in every launch); the store is
+ * also skipped when it exceeds half the free device memory.  max_gb < 0 only
+ * queries; *bytes (optional) = current store size. */
+int ps_set_symbol_store(ps_ctx* ctx, double max_gb, size_t* bytes);
 /* Multi-RHS M2L kernel choice: 0 auto (FP64 tensor cores, mma.sync f64, for
  * >= 12 RHS; below that one single-RHS launch per RHS), 1 force the DFMA
  * multi-RHS K1m, 2 force DMMA K1d. */

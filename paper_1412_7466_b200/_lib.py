@@ -55,6 +55,7 @@ SIGNATURES = {
     "ps_precompute_coupling": (_I, [_P, _D]),
     "ps_coupling_mode": (_I, [_P]),
     "ps_set_k1_variant": (_I, [_P, _I]),
+    "ps_set_symbol_store": (_I, [_P, _D, ctypes.POINTER(ctypes.c_size_t)]),
     "ps_set_mrhs_variant": (_I, [_P, _I]),
     "ps_set_overlap": (_I, [_P, _I]),
     "ps_set_overlap_order": (_I, [_P, _I]),

@@ -181,7 +181,7 @@ void ps_destroy(ps_ctx* h) {
   Ctx* c = C(h);
   cudaSetDevice(c->device);
   void* ptrs[] = {c->d_centers, c->d_S, c->d_rot, c->d_g1, c->d_g2, c->d_w2, c->d_blochpow,
-                  c->d_partial, c->d_work, c->d_inc};
+                  c->d_partial, c->d_work, c->d_inc, c->d_symstore};
   for (void* p : ptrs)
     if (p) ps::dev_free(p);
   for (auto& r : c->rhs) {
@@ -219,6 +219,12 @@ int ps_set_geometry(ps_ctx* h, int M, int p, int copies, double period, double k
     return PS_ERR_UNSUPPORTED;
   }
   if (int rc = set_device(c)) return rc;
+  ++c->geom_gen;                   // invalidates the K1s symbol store
+  if (c->d_symstore) {
+    ps::dev_free(c->d_symstore);
+    c->d_symstore = nullptr;
+    c->symstore_bytes = 0;
+  }
   c->M = M;
   c->p = p;
   c->L = 2 * p + 1;
@@ -786,6 +792,22 @@ int ps_precompute_coupling(ps_ctx* h, double max_gb) {
   }
   if (int rc = set_device(c)) return rc;
   return ps::precompute_coupling(c, max_gb * 1e9);
+}
+
+int ps_set_symbol_store(ps_ctx* h, double max_gb, size_t* bytes) {
+  if (!h) return PS_ERR_ARG;
+  Ctx* c = C(h);
+  if (bytes) *bytes = c->symstore_bytes;
+  if (max_gb < 0) return PS_OK;   // query only
+  if (int rc = set_device(c)) return rc;
+  c->symstore_max_gb = max_gb;
+  if (c->d_symstore && (double)c->symstore_bytes > max_gb * 1e9) {
+    ps::dev_free(c->d_symstore);
+    c->d_symstore = nullptr;
+    c->symstore_bytes = 0;
+    c->sst_kb0 = c->sst_nb = -1;
+  }
+  return PS_OK;
 }
 
 int ps_set_k1_variant(ps_ctx* h, int variant) {

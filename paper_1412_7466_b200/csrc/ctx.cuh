@@ -88,6 +88,16 @@ struct Ctx {
   std::vector<RhsData> rhs;
   double2* d_blochpow = nullptr;  // [nrhs][2*copies+3]: bloch^l, l=-(copies+1)..copies+1
 
+  // K1s symbol store: every batch of translation symbols of the launch's
+  // block range, in the kernel's shared-memory layout, built once per
+  // geometry (symbols depend on the centres, k2, period and copies only)
+  double2* d_symstore = nullptr;
+  size_t symstore_bytes = 0;
+  long long sst_kb0 = -1, sst_nb = -1;
+  int sst_geom = -1, sst_p = -1;
+  int geom_gen = 0;                 // bumped by ps_set_geometry
+  double symstore_max_gb = 32.0;    // 0: regenerate the symbols in every launch
+
   // workspaces
   double2* d_partial = nullptr;
   size_t partial_elems = 0;
@@ -140,9 +150,10 @@ inline bool first_on_device(unsigned long long* mask, int device) {
 }
 
 // Device memory of every context comes from the device's stream-ordered
-// default pool with a 4 GiB release threshold: freed blocks stay cached, so a
+// default pool with a 32 GiB release threshold: freed blocks stay cached, so a
 // new context (e.g. each solve_full) reuses the previous one's coupling
-// blocks and Krylov basis instead of paying cudaMalloc/cudaFree of ~1 GB.
+// blocks, symbol store and Krylov basis instead of paying cudaMalloc/cudaFree
+// of ~3.5 GB per solve at cfg3.
 // Allocation and free are rare (setup, growth, destroy) and fully
 // synchronise, so the non-blocking worker streams never race them.
 #ifdef PS_CANARY
@@ -180,7 +191,7 @@ inline cudaError_t dev_malloc_raw(void** p, size_t bytes) {
   if (dev >= 0 && dev < 64 && !pool_ready[dev]) {
     cudaMemPool_t pool;
     if ((e = cudaDeviceGetDefaultMemPool(&pool, dev)) != cudaSuccess) return e;
-    uint64_t thr = 4ull << 30;
+    uint64_t thr = 32ull << 30;
     if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr)) != cudaSuccess)
       return e;
     pool_ready[dev] = 1;

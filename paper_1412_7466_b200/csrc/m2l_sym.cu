@@ -229,7 +229,8 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
   const int nbat = (int)(k1 - k0) * a.ncp;      // batches of this CTA
 
   // zero the pad slots (front FP slots, tail slot) of both buffers once
-  for (int idx = threadIdx.x; idx < 2 * kTT * kTT * (S::FP + 1); idx += kThreads) {
+  // (stored batches carry their own zero pads)
+  for (int idx = threadIdx.x; !a.symstore && idx < 2 * kTT * kTT * (S::FP + 1); idx += kThreads) {
     const int buf = idx / (kTT * kTT * (S::FP + 1));
     const int r = idx % (kTT * kTT * (S::FP + 1));
     const int jt = r / (kTT * (S::FP + 1));
@@ -244,6 +245,61 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
   if (producer) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
     const int pw = warp - kCW;
+    if (a.symstore) {
+      // stored symbols: one lane bulk-copies each batch (TMA, evict-first in
+      // L2) into the free buffer and waits for it before the batch barrier
+      __shared__ __align__(8) unsigned long long sbar[2];
+      const bool lead = pw == 0 && lane == 0;
+      const size_t g0 = (size_t)(k0 - a.kb0) * a.ncp;
+      unsigned long long pol = 0;
+      if (lead) {
+        for (int q = 0; q < 2; ++q)
+          asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(
+              (unsigned)__cvta_generic_to_shared(&sbar[q])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      }
+      auto fetch = [&](size_t g, double2* dst, int q) {
+        const unsigned bar = (unsigned)__cvta_generic_to_shared(&sbar[q]);
+        constexpr unsigned kBytes = (unsigned)(S::SYM * sizeof(double2));
+        constexpr unsigned kChunk = 32768;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(kBytes)
+                     : "memory");
+        const char* src = reinterpret_cast<const char*>(a.symstore + g * S::SYM);
+        const unsigned d0 = (unsigned)__cvta_generic_to_shared(dst);
+        for (unsigned off = 0; off < kBytes; off += kChunk) {
+          const unsigned n = kBytes - off < kChunk ? kBytes - off : kChunk;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+              " [%0], [%1], %2, [%3], %4;" ::"r"(d0 + off),
+              "l"(src + off), "r"(n), "r"(bar), "l"(pol)
+              : "memory");
+        }
+      };
+      auto wait = [&](int q, unsigned parity) {
+        const unsigned bar = (unsigned)__cvta_generic_to_shared(&sbar[q]);
+        asm volatile(
+            "{ .reg .pred p; W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1; @!p bra W; }" ::"r"(
+                bar),
+            "r"(parity)
+            : "memory");
+      };
+      if (lead) {
+        fetch(g0, sym0, 0);
+        wait(0, 0);
+      }
+      __syncthreads();
+      for (int it = 0; it < nbat; ++it) {
+        if (lead && it + 1 < nbat) {
+          const int q = (it + 1) & 1;
+          fetch(g0 + it + 1, q ? sym1 : sym0, q);
+          wait(q, ((it + 1) >> 1) & 1);
+        }
+        __syncthreads();
+      }
+      return;
+    }
     int A, B;
     block_ab(k0, a.T, A, B);
     int li = 0;
@@ -348,6 +404,29 @@ __global__ void bloch_weight_1(const double2* __restrict__ beta, const double2* 
     bwr[i] = odd ? make_double2(-v.x, -v.y) : v;
     bwsr[i] = odd ? -(v.x + v.y) : v.x + v.y;
   }
+}
+
+// The symbol store: batch g of the range [kb0, kb0 + nb) -- block
+// kb0 + g / ncp, image g % ncp -- in the K1s shared-memory layout (pad slots
+// zero), written by the kernel's own producer code.  One CTA of the 4
+// producer warps per batch.
+template <int P>
+__global__ void __launch_bounds__(kPW * 32) sym_store_kernel(ArgsS a, double2* __restrict__ out) {
+  using S = ShapeS<P>;
+  const long long g = blockIdx.x;
+  const long long k = a.kb0 + g / a.ncp;
+  const int li = (int)(g % a.ncp);
+  int A, B;
+  block_ab(k, a.T, A, B);
+  double2* sym = out + (size_t)g * S::SYM;
+  for (int idx = threadIdx.x; idx < kTT * kTT * (S::FP + 1); idx += blockDim.x) {
+    const int jt = idx / (kTT * (S::FP + 1));
+    const int r2 = idx % (kTT * (S::FP + 1));
+    const int q = r2 / kTT, mt = r2 % kTT;
+    const int slot = q < S::FP ? q : S::FP + S::NS;
+    sym[(size_t)jt * S::SJ + (size_t)slot * kTT + (mt ^ sw_of<S::BO>(slot))] = make_double2(0.0, 0.0);
+  }
+  produce_s<P>(a, A, B, li, sym, threadIdx.x >> 5, threadIdx.x & 31);
 }
 
 // out[m][r] for tile X = m / 8, fixed order: reverse parts of the cross
@@ -461,6 +540,36 @@ int max_rows_per_cta(int T, long long kb0, long long nb, int G) {
   return mx;
 }
 
+// Build (or keep) the symbol store of a's block range when it fits the
+// budget and half the free memory; otherwise leave it empty (on-the-fly).
+template <int P>
+int symbol_store(Ctx* ctx, const ArgsS& a, cudaStream_t st) {
+  using S = ShapeS<P>;
+  const size_t bytes = (size_t)a.nb * a.ncp * S::SYM * sizeof(double2);
+  if (ctx->d_symstore && ctx->sst_kb0 == a.kb0 && ctx->sst_nb == a.nb &&
+      ctx->sst_geom == ctx->geom_gen && ctx->sst_p == P)
+    return PS_OK;
+  if (ctx->d_symstore) ps::dev_free(ctx->d_symstore);
+  ctx->d_symstore = nullptr;
+  ctx->symstore_bytes = 0;
+  ctx->sst_kb0 = ctx->sst_nb = -1;
+  if (!(ctx->symstore_max_gb > 0) || (double)bytes > ctx->symstore_max_gb * 1e9 || a.nb <= 0)
+    return PS_OK;
+  size_t fr = 0, tot = 0;
+  PS_CUDA_TRY(ctx, cudaMemGetInfo(&fr, &tot));
+  if (bytes > fr / 2) return PS_OK;
+  PS_CUDA_TRY(ctx, ps::dev_malloc(&ctx->d_symstore, bytes));
+  sym_store_kernel<P><<<(unsigned)(a.nb * a.ncp), kPW * 32, 0, st>>>(a, ctx->d_symstore);
+  PS_CUDA_TRY(ctx, cudaGetLastError());
+  ctx->launches += 1;
+  ctx->symstore_bytes = bytes;
+  ctx->sst_kb0 = a.kb0;
+  ctx->sst_nb = a.nb;
+  ctx->sst_geom = ctx->geom_gen;
+  ctx->sst_p = P;
+  return PS_OK;
+}
+
 template <int P>
 int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, int mode,
              const double2* v_own, const double2* bsub, cudaStream_t st, const SymOverlap* ov) {
@@ -478,6 +587,7 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   // multi-GPU part: this launch covers blocks [NB part / nparts, NB (part+1) / nparts)
   a.kb0 = ((long long)a.NB * ctx->sym_part) / ctx->sym_nparts;
   a.nb = ((long long)a.NB * (ctx->sym_part + 1)) / ctx->sym_nparts - a.kb0;
+  a.symstore = nullptr;
   int G = ov ? ov->grid : ctx->sm_count - ctx->k1_reserve_sms;
   if (G > a.nb) G = (int)a.nb;
   if (G < 1) G = 1;
@@ -513,6 +623,10 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
     PS_CUDA_TRY(ctx, cudaGetLastError());
   }
   if (ov) PS_CUDA_TRY(ctx, cudaEventRecord(ov->bw_done, ks));
+  if (!hmma) {
+    if (int rc = symbol_store<P>(ctx, a, ks)) return rc;
+    a.symstore = ctx->d_symstore;
+  }
   static unsigned long long attr_mask = 0;
   if (first_on_device(&attr_mask, ctx->device)) {
     PS_CUDA_TRY(ctx, cudaFuncSetAttribute(m2l_sym_kernel<P>,

@@ -19,6 +19,9 @@ struct ArgsS {
   int M, T, NB, copies, ncp, maxseg;
   long long kb0, nb;       // block range [kb0, kb0 + nb) of this launch (multi-GPU part)
   double period, k2;
+  // K1s only: precomputed symbol batches of [kb0, kb0 + nb) (batch g = (block
+  // - kb0) * ncp + image at g * SYM double2), or null to generate them
+  const double2* symstore;
 };
 
 // unordered tile pairs (A <= B), row-major: block k -> (A, B)

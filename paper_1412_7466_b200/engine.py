@@ -205,6 +205,14 @@ class Engine:
         """0 auto, 1 tiled K1, 2 symmetric K1s, 3 K1h (K1s on DMMA, opt-in); see include/periscat_b200.h."""
         self._check(self.lib.ps_set_k1_variant(self.ctx, int(variant)))
 
+    def set_symbol_store(self, max_gb: float) -> int:
+        """Bound (GB) of the K1s symbol store (0: regenerate the symbols in
+        every launch; < 0: query only).  Returns the current store size in
+        bytes (see include/periscat_b200.h)."""
+        n = ctypes.c_size_t(0)
+        self._check(self.lib.ps_set_symbol_store(self.ctx, float(max_gb), ctypes.byref(n)))
+        return int(n.value)
+
     def set_overlap(self, sms: int):
         """SMs left to the coupling chain while K1s runs (< 0: serial)."""
         self._check(self.lib.ps_set_overlap(self.ctx, int(sms)))

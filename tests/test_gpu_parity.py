@@ -534,6 +534,40 @@ def test_matvec_and_solve_are_bit_reproducible(O, cfg, nrhs):
         assert torch.equal(x1, x2)
 
 
+def test_k1s_symbol_store_is_bitwise_the_generated_symbols(O):
+    """K1s with its geometry-only symbols precomputed once (the default when
+    the store fits) and bulk-copied per batch gives bitwise the result of
+    regenerating them in every launch; the store follows a geometry change."""
+    from paper_1412_7466_b200.engine import Engine
+    pb = O.load_problem(3)
+    rng = np.random.default_rng(321)
+    beta = _dev(pb.smat[None, None, :] * _cplx(rng, (1, pb.M, pb.L)))
+    eng = Engine(0)
+    eng.set_geometry(pb.centers, pb.p, pb.es.k2, pb.es.period, pb.es.copies)
+    eng.set_bloch([pb.es.bloch])
+    eng.set_k1_variant(2)
+    y_store = eng.apply_T(beta).cpu().numpy()
+    assert eng.set_symbol_store(-1) > 0                 # the store was built and used
+    y_again = eng.apply_T(beta).cpu().numpy()
+    eng.set_symbol_store(0)
+    assert eng.set_symbol_store(-1) == 0
+    y_gen = eng.apply_T(beta).cpu().numpy()
+    assert np.array_equal(y_store, y_gen) and np.array_equal(y_again, y_gen)
+    ref = O.apply_T(beta.cpu().numpy()[0], pb.centers, pb.es.k2, pb.p, pb.es.bloch)
+    assert rel(y_store[0], ref) <= MATVEC_TOL
+    # new geometry: the store is rebuilt, not reused
+    eng.set_symbol_store(32)
+    c2 = pb.centers.copy()
+    c2[:, 1] *= 0.99
+    eng.set_geometry(c2, pb.p, pb.es.k2, pb.es.period, pb.es.copies)
+    eng.set_bloch([pb.es.bloch])
+    y2 = eng.apply_T(beta).cpu().numpy()
+    eng.set_symbol_store(0)
+    y2g = eng.apply_T(beta).cpu().numpy()
+    eng.close()
+    assert np.array_equal(y2, y2g)
+
+
 def test_k1h_bit_reproducible_and_matches_k1s(O):
     """The opt-in DMMA variant of the symmetric M2L (K1h, variant 3) keeps the
     deterministic order (repeat launches bitwise identical) and equals K1s
