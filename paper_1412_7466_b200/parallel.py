@@ -157,7 +157,7 @@ class ShardedSchur:
     the same C / B coupling split):
       * "targets": every rank runs the tiled K1 for its own targets over all
         sources (no M2L exchange);
-      * "pairs" (one RHS, M >= 512 and M / world >= 200, the default there):
+      * "pairs" (one RHS, M >= 512 and M / world >= 100, the default there):
         every rank runs the symmetric K1s over 1/world of the unordered tile
         pairs -- each symbol row serves a pair and its reverse, half the
         producer work of the tiled kernel -- for ALL targets, and a
@@ -173,12 +173,12 @@ class ShardedSchur:
         self.t0, self.t1 = shard_range(op.M, self.rank, self.world)
         self.s_range = (self.t0, self.t1)     # own sources for the C partial sum
         if mode == "auto":
-            # measured per-rank compute at cfg3 (tools/probe_shard.py): pairs
-            # wins at 2 and 4 ranks (1.25 vs 1.34 ms, 0.70 vs 0.72 ms), the
-            # tiled target split at 8 (0.38 vs 0.40 ms: 125 targets per rank
-            # leave too few tile pairs per CTA) -> pairs while M / world >= 200
+            # measured per-rank compute at cfg3 (tools/probe_shard.py, K1s
+            # with its symbol store): pairs wins at 2, 4 and 8 ranks (1.11 vs
+            # 1.33 ms, 0.62 vs 0.70 ms, 0.352 vs 0.376 ms); without the store
+            # the tiled target split won at 8 -> pairs while M / world >= 100
             mode = "pairs" if (op.nrhs == 1 and self.world > 1 and op.M >= 512
-                               and op.M >= 200 * self.world) else "targets"
+                               and op.M >= 100 * self.world) else "targets"
         if mode not in ("pairs", "targets"):
             raise ValueError(f"unknown decomposition {mode!r}")
         self.mode = mode
