@@ -202,10 +202,19 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PS_BENCH_ONE_GPU=1 + PS_BENCH_BACKEND=gloo: every rank on cuda:0 over
+    # gloo -- exercises the multi-rank bench path on a one-GPU box (timings
+    # meaningless); the driver's runs use one GPU per rank over NCCL
+    if os.environ.get("PS_BENCH_ONE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("PS_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     lib = _lib.load()
     peak = ctypes.c_double()
@@ -412,8 +421,11 @@ def run_ours(args):
                              "algorithmic": "8(2p+1)^2 flops per translation",
                              "executed": "Karatsuba complex MACs: 3 real FMA (6 flops) per "
                                          "complex MAC, i.e. 6(2p+1)^2 FP64 flops issued per "
-                                         "translation plus symbol generation; 'achieved' "
-                                         "counts the 8(2p+1)^2 algorithmic flops",
+                                         "translation; the geometry-only translation symbols "
+                                         "come from the precomputed symbol store (TMA bulk "
+                                         "copies; generated in the kernel when the store does "
+                                         "not fit); 'achieved' counts the 8(2p+1)^2 "
+                                         "algorithmic flops",
                              "peak_source": "max of the two FP64 chain microbenchmarks measured on "
                                             "this GPU in this run (MEASURED_PEAKS.json has no FP64 "
                                             "entry): ps_dfma_peak (DFMA chains, 8 CTAs/SM) and "
