@@ -125,3 +125,25 @@ def test_sharded_driver_nccl_world1():
             op.eng.set_k1_reserve(0)
     finally:
         dist.destroy_process_group()
+
+
+def test_bench_multirank_path_two_ranks_one_gpu(tmp_path):
+    """The driver's scaling run (bench.py under torchrun, N > 1) end to end
+    with 2 ranks: here both on cuda:0 over gloo (PS_BENCH_ONE_GPU /
+    PS_BENCH_BACKEND); checks the JSON line, the tile-pair decomposition and
+    the distributed GMRES solve's flux balance."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PS_BENCH_ONE_GPU="1", PS_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--no-cpu", "--no-cfg5"]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["config"]["parallelism"].startswith("tile-pair-sharded x2")
+    fs = line["full_solve_m1000"]
+    assert fs["iterations"] == 27 and abs(fs["flux_error"]) < 1e-9
