@@ -558,7 +558,13 @@ int symbol_store(Ctx* ctx, const ArgsS& a, cudaStream_t st) {
   size_t fr = 0, tot = 0;
   PS_CUDA_TRY(ctx, cudaMemGetInfo(&fr, &tot));
   if (bytes > fr / 2) return PS_OK;
-  PS_CUDA_TRY(ctx, ps::dev_malloc(&ctx->d_symstore, bytes));
+  if (ps::dev_malloc(&ctx->d_symstore, bytes) != cudaSuccess) {
+    // out of memory (fragmentation despite the free-memory check): no store,
+    // the symbols are generated in the kernel as without a budget
+    cudaGetLastError();
+    ctx->d_symstore = nullptr;
+    return PS_OK;
+  }
   sym_store_kernel<P><<<(unsigned)(a.nb * a.ncp), kPW * 32, 0, st>>>(a, ctx->d_symstore);
   PS_CUDA_TRY(ctx, cudaGetLastError());
   ctx->launches += 1;
