@@ -247,7 +247,96 @@ class Periscat:
         d = xr[:, self.ncol_b + self.nrb:]
         return beta, c, d, list(iters)
 
+    def set_target_range(self, t0, t1):
+        """Own the target slice [t0, t1) (one rank of a sharded operator)."""
+        self._ok(self.lib.ps_set_target_range(self.ctx, t0, t1))
+        self.t0, self.t1 = t0, t1
+
     def close(self):
         if self.ctx:
             self.lib.ps_destroy(self.ctx)
             self.ctx = ctypes.c_void_p()
+
+
+def shard_range(M, rank, world):
+    return (M * rank) // world, (M * (rank + 1)) // world
+
+
+class ShardedSchur:
+    """The multi-rank Schur matvec driven
+    through the C ABI alone, with the collectives supplied by the caller --
+    the way an MPI / NCCL C program shards it.  ``ranks`` are Periscat
+    contexts that already hold the operator (setup) and each own a target
+    slice (set_target_range); ``allgather(list of own blocks) -> full`` and
+    ``allreduce(list of partials) -> sum`` stand in for the caller's
+    collectives (here: host arrays summed in rank order).
+
+    mode "targets": every rank applies T over all sources to its own targets
+    (ps_apply_schur_g after an all-reduce of the partial C v over the ranks'
+    own sources).  mode "pairs": every rank applies the symmetric K1s to its
+    1/world of the tile pairs for ALL targets (ps_apply_T_blocks), a
+    reduce-scatter sums the parts, ps_schur_finish applies the epilogue."""
+
+    def __init__(self, ranks, mode="targets"):
+        self.ranks = ranks
+        self.mode = mode
+        self.world = len(ranks)
+
+    @staticmethod
+    def allgather(blocks):
+        return np.concatenate(blocks, axis=1)
+
+    @staticmethod
+    def allreduce(parts):
+        out = parts[0].copy()
+        for q in parts[1:]:
+            out += q
+        return out
+
+    def __call__(self, v_own_blocks):
+        """v_own_blocks[r]: rank r's rows [nrhs][Mt_r][L] (host); returns the
+        ranks' rows of y = K v."""
+        r0 = self.ranks[0]
+        rt = r0.rt
+        v = self.allgather(v_own_blocks)                       # all-gather beta
+        nrhs, M, L = v.shape
+        g_parts = []
+        dv = [DeviceArray(rt, v.nbytes).upload(v) for _ in self.ranks]
+        try:
+            for pc, d in zip(self.ranks, dv):                  # C over own sources
+                dg = DeviceArray(rt, nrhs * pc.nrow_c * 16)
+                pc._ok(pc.lib.ps_apply_C(pc.ctx, d.ptr, dg.ptr, pc.t0, pc.t1, None))
+                g_parts.append(dg.download((nrhs, pc.nrow_c)))
+                dg.free()
+            g = self.allreduce(g_parts)                        # all-reduce C v
+            out = []
+            if self.mode == "targets":
+                for pc, d in zip(self.ranks, dv):
+                    dg = DeviceArray(rt, g.nbytes).upload(g)
+                    dy = DeviceArray(rt, nrhs * (pc.t1 - pc.t0) * L * 16)
+                    pc._ok(pc.lib.ps_apply_schur_g(pc.ctx, d.ptr, dg.ptr, dy.ptr, None))
+                    out.append(dy.download((nrhs, pc.t1 - pc.t0, L)))
+                    dg.free()
+                    dy.free()
+                return out
+            a_parts = []                                       # "pairs": K1s parts
+            for r, (pc, d) in enumerate(zip(self.ranks, dv)):
+                da = DeviceArray(rt, v.nbytes)
+                pc._ok(pc.lib.ps_apply_T_blocks(pc.ctx, r, self.world, d.ptr, da.ptr, None))
+                a_parts.append(da.download(v.shape))
+                da.free()
+            a = self.allreduce(a_parts)                        # reduce-scatter
+            for pc, vo in zip(self.ranks, v_own_blocks):
+                a_own = np.ascontiguousarray(a[:, pc.t0:pc.t1])
+                dvo = DeviceArray(rt, vo.nbytes).upload(np.ascontiguousarray(vo))
+                dao = DeviceArray(rt, a_own.nbytes).upload(a_own)
+                dg = DeviceArray(rt, g.nbytes).upload(g)
+                dy = DeviceArray(rt, vo.nbytes)
+                pc._ok(pc.lib.ps_schur_finish(pc.ctx, dvo.ptr, dao.ptr, dg.ptr, dy.ptr, None))
+                out.append(dy.download(vo.shape))
+                for x in (dvo, dao, dg, dy):
+                    x.free()
+            return out
+        finally:
+            for d in dv:
+                d.free()

@@ -29,6 +29,33 @@ def test_ctypes_stub_apply_T_and_solve():
         ps.close()
 
 
+@pytest.mark.parametrize("mode,world", [("targets", 3), ("pairs", 2), ("pairs", 3)])
+def test_ctypes_stub_sharded_schur_with_caller_collectives(mode, world):
+    """A C / ctypes caller shards the Schur matvec through the C ABI alone,
+    bringing its own collectives: world contexts with target
+    slices, all-gather / all-reduce / reduce-scatter done by the caller (host
+    arrays here), reassembled rows = the oracle golden (cfg2)."""
+    from integration.ctypes_stub import Periscat, ShardedSchur, shard_range
+    from oracle import periscat_oracle as O
+    pb = O.load_problem(2)
+    z = np.load(os.path.join(O.GOLDEN, "golden_cfg2.npz"))
+    sysm = workloads.load_fixture(O.CONFIGS[2]["empty"])
+    ranks = []
+    try:
+        for r in range(world):
+            pc = Periscat(0)
+            pc.setup(sysm, pb.centers, pb.p, pb.smat)
+            pc.set_target_range(*shard_range(pb.M, r, world))
+            ranks.append(pc)
+        v = z["v"][None]
+        blocks = [np.ascontiguousarray(v[:, pc.t0:pc.t1]) for pc in ranks]
+        y = np.concatenate(ShardedSchur(ranks, mode)(blocks), axis=1)[0]
+        assert rel(y, z["schur"]) <= 1e-10
+    finally:
+        for pc in ranks:
+            pc.close()
+
+
 class _Cv:
     """DiscretizedCurve duck type from empty_setup / scatmat rows."""
     def __init__(self, rows):
