@@ -16,6 +16,12 @@ SOURCES = ["m2l.cu", "m2l_mrhs.cu", "m2l_sym.cu", "m2l_symh.cu", "m2l_mma.cu", "
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+# The DFMA sweeps of these sources get a post-link SASS scheduling patch
+# (sass_reuse_patch.py: operand-reuse flags through the coefficient runs
+# instead of ptxas's mid-run yield hints); their device code must therefore sit
+# uncompressed in the fatbin.  PS_NO_SASS_PATCH=1 builds the unpatched library.
+PATCHED_SOURCES = {"m2l.cu", "m2l_mrhs.cu", "m2l_sym.cu"}
+PATCHED_KERNELS = r"m2l_sym_kernel|m2l_kernel|m2l_mrhs_kernel"
 
 
 def _stale() -> bool:
@@ -35,7 +41,9 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     procs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", f".{os.getpid()}.o"))
-        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
+        extra = ["--no-compress"] if src in PATCHED_SOURCES else []
+        cmd = [NVCC, *FLAGS, *extra, *[f"-D{d}" for d in defines], "-c",
+               os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                             text=True)))
         objs.append(obj)
@@ -56,9 +64,28 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
         for o in objs:
             if os.path.exists(o):
                 os.remove(o)
+    if os.environ.get("PS_NO_SASS_PATCH") != "1":
+        stats = sass_patch(out)
+        if verbose:
+            print(f"SASS reuse patch: {sum(c for _, _, c in stats.values())} DFMAs re-flagged in "
+                  f"{len(stats)} kernels")
     if verbose:
         print(f"built {out} in {time.time() - t0:.1f}s")
     return out
+
+
+def sass_patch(path: str = LIB, dry: bool = False) -> dict:
+    """Apply sass_reuse_patch.py to the DFMA kernels of the library;
+    returns {kernel: (dfma, already_flagged, patched)}."""
+    from . import sass_reuse_patch
+    buf = bytearray(open(path, "rb").read())
+    stats = sass_reuse_patch.patch(buf, PATCHED_KERNELS)
+    if not stats:
+        raise RuntimeError("SASS patch: no DFMA kernel found in the fatbin (compressed?)")
+    if not dry:
+        with open(path, "wb") as fh:
+            fh.write(buf)
+    return stats
 
 
 if __name__ == "__main__":
