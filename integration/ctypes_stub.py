@@ -88,9 +88,9 @@ def _curve_rows(cv):
 class Periscat:
     """ps_ctx owner.  Mirrors the calls solver.solve_full makes."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, lib_path: str = LIB):
         self.rt = _cudart()
-        self.lib = ctypes.CDLL(LIB)
+        self.lib = ctypes.CDLL(lib_path)
         self.lib.ps_last_error.restype = ctypes.c_char_p
         self.ctx = ctypes.c_void_p()
         self._ok(self.lib.ps_create(ctypes.byref(self.ctx), device))

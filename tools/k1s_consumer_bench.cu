@@ -7,6 +7,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xptxas -v \
 //        -o tools/k1s_consumer_bench tools/k1s_consumer_bench.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 template <int V>
@@ -88,6 +89,13 @@ __device__ __forceinline__ void consume(const double2* __restrict__ spe, const d
       for (int i = 0; i < BO; ++i) acc[1][i] = fma(wy[(R0 + u - i + MODB) % BO], bb.y, acc[1][i]);
 #pragma unroll
       for (int i = 0; i < BO; ++i) acc[2][i] = fma(ws[(R0 + u - i + MODB) % BO], bs, acc[2][i]);
+    } else if constexpr (ORD == 3) {   // descending rows: the newest symbol (i = 0) is used last in each run
+#pragma unroll
+      for (int i = BO - 1; i >= 0; --i) acc[0][i] = fma(bb.x, wx[(R0 + u - i + MODB) % BO], acc[0][i]);
+#pragma unroll
+      for (int i = BO - 1; i >= 0; --i) acc[1][i] = fma(bb.y, wy[(R0 + u - i + MODB) % BO], acc[1][i]);
+#pragma unroll
+      for (int i = BO - 1; i >= 0; --i) acc[2][i] = fma(bs, ws[(R0 + u - i + MODB) % BO], acc[2][i]);
     } else if constexpr (ORD == 0) {
 #pragma unroll
       for (int i = 0; i < BO; ++i) acc[0][i] = fma(bb.x, wx[(R0 + u - i + MODB) % BO], acc[0][i]);
@@ -144,7 +152,7 @@ __device__ __forceinline__ void consume(const double2* __restrict__ spe, const d
 
 template <int P, int VB, int SYNC, int ORD = 0, int PF = 0, int NB = 4, int SWAP = 0>
 __global__ void __launch_bounds__(256, 1) bench(const double2* __restrict__ bw, const double* __restrict__ bws,
-                                                int nbat, int nsrc, double* out) {
+                                                int nbat, int nsrc, double* out, int sstride) {
   using S = Sh<P, NB>;
   extern __shared__ double2 smem[];
   double2* sym = smem;
@@ -176,7 +184,7 @@ __global__ void __launch_bounds__(256, 1) bench(const double2* __restrict__ bw, 
     for (int pass = 0; pass < (NB == 4 ? 2 : 1); ++pass) {
       const int s = sl + 4 * pass;
       const int jj = h ? warp : s, mm = h ? s : warp;
-      const int src = (blockIdx.x * 7 + it * 3 + s + 8 * h) % nsrc;
+      const int src = (blockIdx.x * 7 + it * sstride + s + 8 * h) % nsrc;
       const double2* rowp = symc + (size_t)jj * S::SJ + (size_t)(R0 - b * S::BO) * kTT;
       if (VB == 5) {
         const int tsrc = ((blockIdx.x * 7 + it * 3 + h) % (nsrc / kTT));
@@ -199,32 +207,35 @@ __global__ void __launch_bounds__(256, 1) bench(const double2* __restrict__ bw, 
   if (t == 1234.5) out[0] = t;
 }
 
+static int g_stride = 3;   // sources advance per batch: 3 = neighbouring batches share rows (L1 hits), 16 = fresh rows every batch (K1s)
 template <int P, int VB, int SYNC, int ORD = 0, int PF = 0, int NB = 4, int SWAP = 0>
-void run(const char* name, double2* bw, double* bws, int nsrc, int sms, double* out) {
+void run(const char* name, double2* bw, double* bws, int nsrc, int sms, double* out, int threads = 256) {
   using S = Sh<P, NB>;
   const size_t smem = (2 * S::SYM + 16 * S::L) * sizeof(double2) + 16 * S::L * sizeof(double);
   cudaFuncSetAttribute(bench<P, VB, SYNC, ORD, PF, NB, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nbat = 400;
-  bench<P, VB, SYNC, ORD, PF, NB, SWAP><<<sms, 256, smem>>>(bw, bws, 10, nsrc, out);
+  bench<P, VB, SYNC, ORD, PF, NB, SWAP><<<sms, threads, smem>>>(bw, bws, 10, nsrc, out, g_stride);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   float best = 1e30f;
   for (int r = 0; r < 5; ++r) {
     cudaEventRecord(e0);
-    bench<P, VB, SYNC, ORD, PF, NB, SWAP><<<sms, 256, smem>>>(bw, bws, nbat, nsrc, out);
+    bench<P, VB, SYNC, ORD, PF, NB, SWAP><<<sms, threads, smem>>>(bw, bws, nbat, nsrc, out, g_stride);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float t;
     cudaEventElapsedTime(&t, e0, e1);
     if (t < best) best = t;
   }
-  const double dfma = 3.0 * S::BO * S::L * (NB == 4 ? 2 : 1) * nbat * 256.0 * sms;
+  const double dfma = 3.0 * S::BO * S::L * (NB == 4 ? 2 : 1) * nbat * (double)threads * sms;
   printf("%-34s p=%d smem %6zu  %.3f ms  executed DFMA %.2f TF/s  %s\n", name, P, smem, best,
          2.0 * dfma / (best * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) g_stride = atoi(argv[1]);
+  printf("source stride per batch %d\n", g_stride);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int nsrc = 3000;
@@ -237,6 +248,12 @@ int main() {
   cudaMemset(bw, 0, nsrc * 51 * sizeof(double2));
   cudaMemset(bws, 0, nsrc * 51 * sizeof(double));
   run<25, 0, 1>("ldg coef + sync (K1s)", bw, bws, nsrc, sms, out);
+  run<25, 0, 1, 3>("descending rows", bw, bws, nsrc, sms, out);
+  run<25, 0, 1>("same, 1 warp per SMSP", bw, bws, nsrc, sms, out, 128);
+  run<25, 0, 0>("same, no sync", bw, bws, nsrc, sms, out);
+  run<25, 0, 0>("same, no sync, 1 warp per SMSP", bw, bws, nsrc, sms, out, 128);
+  run<25, 2, 0>("fixed coef regs, no sync", bw, bws, nsrc, sms, out);
+  run<25, 2, 0>("fixed coef regs, no sync, 1 warp", bw, bws, nsrc, sms, out, 128);
   run<25, 6, 1>("ldg, chunked runtime loop", bw, bws, nsrc, sms, out);
   run<20, 0, 1>("ldg coef + sync (K1s)", bw, bws, nsrc, sms, out);
   run<20, 6, 1>("ldg, chunked runtime loop", bw, bws, nsrc, sms, out);
