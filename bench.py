@@ -424,8 +424,9 @@ def run_ours(args):
                                          "translation; the geometry-only translation symbols "
                                          "come from the precomputed symbol store (TMA bulk "
                                          "copies; generated in the kernel when the store does "
-                                         "not fit); 'achieved' counts the 8(2p+1)^2 "
-                                         "algorithmic flops",
+                                         "not fit); the DFMA sweeps carry operand-reuse "
+                                         "flags set post-link (sass_reuse_patch.py); "
+                                         "'achieved' counts the 8(2p+1)^2 algorithmic flops",
                              "peak_source": "max of the two FP64 chain microbenchmarks measured on "
                                             "this GPU in this run (MEASURED_PEAKS.json has no FP64 "
                                             "entry): ps_dfma_peak (DFMA chains, 8 CTAs/SM) and "
