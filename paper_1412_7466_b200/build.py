@@ -16,12 +16,16 @@ SOURCES = ["m2l.cu", "m2l_mrhs.cu", "m2l_sym.cu", "m2l_symh.cu", "m2l_mma.cu", "
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
-# The DFMA sweeps of these sources get a post-link SASS scheduling patch
+# The DFMA sweeps of K1s get a post-link SASS scheduling patch
 # (sass_reuse_patch.py: operand-reuse flags through the coefficient runs
-# instead of ptxas's mid-run yield hints); their device code must therefore sit
+# instead of ptxas's mid-run yield hints); its device code must therefore sit
 # uncompressed in the fatbin.  PS_NO_SASS_PATCH=1 builds the unpatched library.
-PATCHED_SOURCES = {"m2l.cu", "m2l_mrhs.cu", "m2l_sym.cu"}
-PATCHED_KERNELS = r"m2l_sym_kernel|m2l_kernel|m2l_mrhs_kernel"
+# Measured per kernel family (tools/probe_patch_gain.py, cfg3): K1s fed by the
+# symbol store 1918 -> 1853 us, K1s generating its symbols 2117 -> 2117 us,
+# but the tiled K1 2375 -> 2558 us -- its producer warps need the issue slots
+# the yields gave them -- so only K1s is patched.
+PATCHED_SOURCES = {"m2l_sym.cu"}
+PATCHED_KERNELS = r"m2l_sym_kernel"
 
 
 def _stale() -> bool:
