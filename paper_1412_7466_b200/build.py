@@ -25,7 +25,7 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 # but the tiled K1 2375 -> 2558 us -- its producer warps need the issue slots
 # the yields gave them -- so only K1s is patched.
 PATCHED_SOURCES = {"m2l_sym.cu"}
-PATCHED_KERNELS = r"m2l_sym_kernel"
+PATCHED_KERNELS = r"m2l_sym_(stage_)?kernel"
 
 
 def _stale() -> bool:

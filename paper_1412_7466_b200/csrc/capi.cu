@@ -1,6 +1,8 @@
 // extern "C" entry points of include/periscat_b200.h.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <cmath>
 #include <complex>
 #include <cstring>
@@ -172,6 +174,7 @@ int ps_create(ps_ctx** out, int device) {
   int sms = 0;
   PS_CUDA_TRY(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   c->sm_count = sms;
+  if (const char* e = getenv("PS_K1S_STAGE")) c->k1s_stage = e[0] != '0';   // experiment switch
   c->rhs.resize(1);
   return upload_blochpow(c);
 }

@@ -97,6 +97,7 @@ struct Ctx {
   int sst_geom = -1, sst_p = -1;
   int geom_gen = 0;                 // bumped by ps_set_geometry
   double symstore_max_gb = 32.0;    // 0: regenerate the symbols in every launch
+  bool k1s_stage = true;            // store-fed K1s stages its coefficient rows in shared memory (env PS_K1S_STAGE=0: off)
 
   // workspaces
   double2* d_partial = nullptr;

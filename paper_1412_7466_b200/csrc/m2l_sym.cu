@@ -123,7 +123,7 @@ __device__ __forceinline__ void produce_s(const ArgsS& a, int A, int B, int li, 
 // so a complex MAC costs 3 DFMA instead of 4; t.x + t.y is formed once per
 // symbol as it enters the register window (1 DADD per step, shared by the
 // BO rows) and c.x + c.y is precomputed per source (bws / bwsr).
-template <int P>
+template <int P, bool SMEMCOEF = false>
 __device__ __forceinline__ void consume_s(const double2* __restrict__ spe,
                                           const double2* __restrict__ spo,
                                           const double2* __restrict__ bsrc,
@@ -151,8 +151,15 @@ __device__ __forceinline__ void consume_s(const double2* __restrict__ spe,
     constexpr int n = decltype(n_c)::value;
     constexpr int u = n % BO;
     const double2 nxt = ld(IC<n + 1>{});
-    const double2 bb = __ldg(bsrc + n);
-    const double bs = __ldg(ssrc + n);
+    double2 bb;
+    double bs;
+    if constexpr (SMEMCOEF) {        // rows staged in shared memory (m2l_sym_stage_kernel)
+      bb = bsrc[n];
+      bs = ssrc[n];
+    } else {
+      bb = __ldg(bsrc + n);
+      bs = __ldg(ssrc + n);
+    }
 #pragma unroll
     for (int i = 0; i < BO; ++i) acc[0][i] = fma(bb.x, wx[(R0 + u - i + MODB) % BO], acc[0][i]);
 #pragma unroll
@@ -384,9 +391,232 @@ __global__ void __launch_bounds__(kThreads, 1) m2l_sym_kernel(ArgsS a) {
   }
 }
 
+// K1s fed by the symbol store, with the batch's coefficient rows staged in
+// shared memory as well.  The consumers of m2l_sym_kernel read their
+// Bloch-weighted coefficient rows with __ldg; every batch touches 16 fresh
+// rows, the 28 KB of L1 left beside 211 KB of shared memory do not hold them
+// across batches, and the first loads after the batch barrier wait on L2 with
+// nothing to hide behind (ncu: long-scoreboard 8.6% of the consumers' time).
+// Here the lead producer lane bulk-copies (TMA) the 8 rows of each sweep --
+// forward rows of sources B*8 + s, reverse rows of sources A*8 + s, s = 4 pass
+// .. 4 pass + 3 -- one sweep ahead:
+//   X (first sweep of batch t+1) is refilled once every consumer has left the
+//     first sweep of batch t (named barrier 1: consumers arrive, lead waits),
+//   Y (second sweep of batch t) right after the batch barrier that ends batch
+//     t-1; the consumers wait on its mbarrier before their second sweep.
+// Row strides in shared memory (816 B coefficients, 432 B sums) make the
+// 8-row LDS.128 / LDS.64 of a warp bank-conflict-free.  The arithmetic and
+// its order are those of m2l_sym_kernel: results are bitwise the same.
+template <int P>
+struct StageS {
+  static constexpr int L = 2 * P + 1;
+  // global row stride (doubles) of bws / bwsr: a 16-byte multiple for TMA; the
+  // sums share a region of 2 L doubles per row, so L + 1 always fits
+  static constexpr int LSG = L + 1;
+  // shared row stride (doubles) of the sums: = 2 (mod 4), so the 8 rows of a
+  // warp's LDS.64 fall in 8 distinct bank pairs (the coefficient rows' 4 L
+  // words are = 4 (mod 8) for every odd L: LDS.128 conflict-free as they are)
+  static constexpr int LSS = (L + 1) % 4 == 2 ? L + 1 : L + 3;
+  static constexpr size_t COEF = 2 * 8 * (size_t)L * sizeof(double2);      // X, Y: [8][L]
+  static constexpr size_t SUMS = 2 * 8 * (size_t)LSS * sizeof(double);     // X, Y: [8][LSS]
+  static constexpr size_t SMEM = ShapeS<P>::SMEM + COEF + SUMS;
+  static constexpr unsigned ROWB = (unsigned)(L * sizeof(double2));        // bytes per coefficient row
+  static constexpr unsigned SUMB = (unsigned)(LSG * sizeof(double));       // L sums + 1 pad
+};
+
+template <int P>
+__global__ void __launch_bounds__(kThreads, 1) m2l_sym_stage_kernel(ArgsS a) {
+  using S = ShapeS<P>;
+  using G = StageS<P>;
+  constexpr int BO = S::BO, L = S::L;
+  extern __shared__ double2 smem[];
+  double2* sym0 = smem;
+  double2* sym1 = smem + S::SYM;
+  double2* cbx = smem + 2 * S::SYM;                 // X rows, then Y rows
+  double* csx = reinterpret_cast<double*>(cbx + 16 * L);
+  __shared__ __align__(8) unsigned long long sbar[2];   // symbol buffers
+  __shared__ __align__(8) unsigned long long cbar[2];   // X, Y coefficient rows
+  const long long k0 = a.kb0 + (a.nb * blockIdx.x) / gridDim.x;
+  const long long k1 = a.kb0 + (a.nb * (blockIdx.x + 1)) / gridDim.x;
+  if (k0 >= k1) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp >= kCW;
+  const int nbat = (int)(k1 - k0) * a.ncp;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 2; ++q) {
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(
+          (unsigned)__cvta_generic_to_shared(&sbar[q])));
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(
+          (unsigned)__cvta_generic_to_shared(&cbar[q])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto wait = [&](unsigned long long* b, unsigned parity) {
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(b);
+    asm volatile(
+        "{ .reg .pred p; W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1; @!p bra W; }" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+  };
+
+  if (producer) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
+    const int pw = warp - kCW;
+    if (pw != 0) {                                   // the other producer warps only keep the barrier count
+      for (int it = 0; it <= nbat; ++it) __syncthreads();
+      return;
+    }
+    const bool lead = lane == 0;
+    const size_t g0 = (size_t)(k0 - a.kb0) * a.ncp;
+    unsigned long long pol = 0;
+    if (lead) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    auto fetch_sym = [&](size_t g, double2* dst, int q) {
+      const unsigned bar = (unsigned)__cvta_generic_to_shared(&sbar[q]);
+      constexpr unsigned kBytes = (unsigned)(S::SYM * sizeof(double2));
+      constexpr unsigned kChunk = 32768;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(kBytes)
+                   : "memory");
+      const char* src = reinterpret_cast<const char*>(a.symstore + g * S::SYM);
+      const unsigned d0 = (unsigned)__cvta_generic_to_shared(dst);
+      for (unsigned off = 0; off < kBytes; off += kChunk) {
+        const unsigned n = kBytes - off < kChunk ? kBytes - off : kChunk;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1], %2, [%3], %4;" ::"r"(d0 + off),
+            "l"(src + off), "r"(n), "r"(bar), "l"(pol)
+            : "memory");
+      }
+    };
+    // the 8 coefficient rows (+ sums) of sweep q of batch (A_, B_, li_) into X (q = 0) or Y (q = 1)
+    auto fetch_rows = [&](int q, int A_, int B_, int li_) {
+      const unsigned bar = (unsigned)__cvta_generic_to_shared(&cbar[q]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"(8u * (G::ROWB + G::SUMB))
+                   : "memory");
+      for (int r = 0; r < 8; ++r) {
+        const int hh = r >> 2, s = (r & 3) + 4 * q;
+        const int src = min((hh ? A_ : B_) * kTT + s, a.M - 1);
+        const int img = hh ? 2 * a.copies - li_ : li_;
+        const size_t row = (size_t)src * a.ncp + img;
+        const double2* gb = (hh ? a.bwr : a.bw) + row * L;
+        const double* gs = (hh ? a.bwsr : a.bws) + row * G::LSG;
+        const unsigned db = (unsigned)__cvta_generic_to_shared(cbx + (q * 8 + r) * L);
+        const unsigned ds = (unsigned)__cvta_generic_to_shared(csx + (q * 8 + r) * G::LSS);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                "r"(db), "l"(gb), "r"(G::ROWB), "r"(bar)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                "r"(ds), "l"(gs), "r"(G::SUMB), "r"(bar)
+            : "memory");
+      }
+    };
+    int A, B;
+    block_ab(k0, a.T, A, B);
+    int li = 0;
+    if (lead) {
+      fetch_sym(g0, sym0, 0);
+      fetch_rows(0, A, B, li);
+      fetch_rows(1, A, B, li);
+      wait(&sbar[0], 0);
+      wait(&cbar[0], 0);
+    }
+    __syncwarp();
+    __syncthreads();
+    for (int it = 0; it < nbat; ++it) {
+      int An = A, Bn = B, lin = li + 1;               // batch it + 1
+      if (lin == a.ncp) {
+        lin = 0;
+        if (++Bn == a.T) Bn = ++An;
+      }
+      if (lead) {
+        if (it > 0) fetch_rows(1, A, B, li);           // Y(it): batch it - 1 is behind the barrier
+        if (it + 1 < nbat) fetch_sym(g0 + it + 1, ((it + 1) & 1) ? sym1 : sym0, (it + 1) & 1);
+      }
+      __syncwarp();
+      asm volatile("bar.sync 1, %0;" ::"n"((kCW + 1) * 32) : "memory");   // consumers left sweep 0
+      if (lead && it + 1 < nbat) {
+        fetch_rows(0, An, Bn, lin);                    // X(it + 1)
+        wait(&sbar[(it + 1) & 1], ((it + 1) >> 1) & 1);
+        wait(&cbar[0], (it + 1) & 1);
+      }
+      __syncwarp();
+      __syncthreads();
+      A = An;
+      B = Bn;
+      li = lin;
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
+  __syncthreads();
+
+  const int h = lane >> 4, b = (lane >> 2) & 3, sl = lane & 3;
+  const unsigned hmask = h ? 0xffff0000u : 0x0000ffffu;
+  double acc[3][BO];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int i = 0; i < BO; ++i) acc[c][i] = 0.0;
+  constexpr int R0 = S::FP + 2 * P;
+  const int sw_e = 4 * (b & 1), sw_o = 4 * ((b & 1) ^ 1);
+  const int crow = h * 4 + sl;                       // this lane's staged row in X / Y
+  const double2* cb0 = cbx + crow * L;
+  const double2* cb1 = cbx + (8 + crow) * L;
+  const double* cs0 = csx + crow * G::LSS;
+  const double* cs1 = csx + (8 + crow) * G::LSS;
+  int A, B;
+  block_ab(k0, a.T, A, B);
+  const int A0 = A;
+  long long blk = k0;
+  int li = 0;
+  for (int it = 0; it < nbat; ++it) {
+    const double2* symc = (it & 1) ? sym1 : sym0;
+    const bool act = h == 0 || A != B;               // diagonal blocks run forward only
+    if (act) {
+      const int jj = h ? warp : sl, mm = h ? sl : warp;
+      const double2* rowp = symc + (size_t)jj * S::SJ + (size_t)(R0 - b * BO) * kTT;
+      consume_s<P, true>(rowp + (mm ^ sw_e), rowp + (mm ^ sw_o), cb0, cs0, acc);
+    }
+    __syncwarp();
+    asm volatile("bar.arrive 1, %0;" ::"n"((kCW + 1) * 32) : "memory");   // X may be refilled
+    wait(&cbar[1], it & 1);                                            // Y(it) has landed
+    if (act) {
+      const int s = sl + 4;
+      const int jj = h ? warp : s, mm = h ? s : warp;
+      const double2* rowp = symc + (size_t)jj * S::SJ + (size_t)(R0 - b * BO) * kTT;
+      consume_s<P, true>(rowp + (mm ^ sw_e), rowp + (mm ^ sw_o), cb1, cs1, acc);
+    }
+    if (li == a.ncp - 1) {                     // block complete
+      const bool cross = A != B;
+      const long long bdone = blk;
+      ++blk;
+      li = 0;
+      const int Aold = A;
+      if (++B == a.T) {
+        ++A;
+        B = A;
+      }
+      if (h) {
+        if (cross) flush_s<P>(acc, a.bpart + ((size_t)bdone * kTT + warp) * L, b, sl, true, hmask);
+      } else if (A != Aold || it + 1 == nbat) {   // block row finished (or CTA done)
+        flush_s<P>(acc, a.apart + (((size_t)blockIdx.x * a.maxseg + (Aold - A0)) * kTT + warp) * L,
+                   b, sl, false, hmask);
+      }
+    } else {
+      ++li;
+    }
+    __syncthreads();
+  }
+}
+
 // bw[g][n] = bloch^{l(g)} beta[j(g)][n]
 __global__ void bloch_weight_1(const double2* __restrict__ beta, const double2* __restrict__ bpow,
-                               int M, int L, int ncp, double2* __restrict__ bw,
+                               int M, int L, int ncp, int lds, double2* __restrict__ bw,
                                double* __restrict__ bws, double2* __restrict__ bwr,
                                double* __restrict__ bwsr) {
   const long long total = (long long)M * ncp * L;
@@ -399,10 +629,11 @@ __global__ void bloch_weight_1(const double2* __restrict__ beta, const double2* 
     const double2 wv = bpow[1 + li];
     const double2 v = make_double2(fma(bv.x, wv.x, -bv.y * wv.y), fma(bv.x, wv.y, bv.y * wv.x));
     bw[i] = v;
-    bws[i] = v.x + v.y;
+    const long long is = g * lds + n;                        // sums: row stride lds >= L
+    bws[is] = v.x + v.y;
     const bool odd = (n - (L - 1) / 2) & 1;                  // (-1)^{order n}
     bwr[i] = odd ? make_double2(-v.x, -v.y) : v;
-    bwsr[i] = odd ? -(v.x + v.y) : v.x + v.y;
+    bwsr[is] = odd ? -(v.x + v.y) : v.x + v.y;
   }
 }
 
@@ -624,19 +855,29 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
     a.bws = bws;
     a.bwr = bwr;
     a.bwsr = bwsr;
-    bloch_weight_1<<<2 * ctx->sm_count, 256, 0, ks>>>(beta, bpow - 1, ctx->M, S::L, a.ncp, bw, bws,
-                                                      bwr, bwsr);
-    PS_CUDA_TRY(ctx, cudaGetLastError());
   }
-  if (ov) PS_CUDA_TRY(ctx, cudaEventRecord(ov->bw_done, ks));
   if (!hmma) {
     if (int rc = symbol_store<P>(ctx, a, ks)) return rc;
     a.symstore = ctx->d_symstore;
   }
+  // with the symbol store the coefficient rows are staged in shared memory
+  // too (m2l_sym_stage_kernel): their sums then sit at a 16-byte-multiple stride
+  const bool stage = !hmma && a.symstore != nullptr && ctx->k1s_stage;
+  if (!hmma) {
+    bloch_weight_1<<<2 * ctx->sm_count, 256, 0, ks>>>(beta, bpow - 1, ctx->M, S::L, a.ncp,
+                                                      stage ? StageS<P>::LSG : S::L, bw,
+                                                      const_cast<double*>(a.bws), const_cast<double2*>(a.bwr),
+                                                      const_cast<double*>(a.bwsr));
+    PS_CUDA_TRY(ctx, cudaGetLastError());
+  }
+  if (ov) PS_CUDA_TRY(ctx, cudaEventRecord(ov->bw_done, ks));
   static unsigned long long attr_mask = 0;
   if (first_on_device(&attr_mask, ctx->device)) {
     PS_CUDA_TRY(ctx, cudaFuncSetAttribute(m2l_sym_kernel<P>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+    PS_CUDA_TRY(ctx, cudaFuncSetAttribute(m2l_sym_stage_kernel<P>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)StageS<P>::SMEM));
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (ctx->profile) {
@@ -646,6 +887,9 @@ int launch_s(Ctx* ctx, const double2* beta, const double2* bpow, double2* out, i
   }
   if (ctx->k1_variant == 3) {                   // K1h: DMMA consumers (m2l_symh.cu)
     PS_CUDA_TRY(ctx, (cudaError_t)symh_kernel(P, a, G, ks, ctx->device));
+  } else if (stage) {
+    m2l_sym_stage_kernel<P><<<G, kThreads, StageS<P>::SMEM, ks>>>(a);
+    PS_CUDA_TRY(ctx, cudaGetLastError());
   } else {
     m2l_sym_kernel<P><<<G, kThreads, S::SMEM, ks>>>(a);
     PS_CUDA_TRY(ctx, cudaGetLastError());
