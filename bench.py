@@ -414,7 +414,9 @@ def run_ours(args):
                 "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak,
                              "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                              "traffic": traffic,
-                             "kernel": "m2l_sym_kernel (K1s, symmetric single-RHS M2L)"
+                             "kernel": "m2l_sym_stage_kernel (K1s, symmetric single-RHS M2L fed by "
+                                       "the symbol store, coefficient rows staged in shared "
+                                       "memory; m2l_sym_kernel when the store does not fit)"
                                        if world == 1 or sharded.mode == "pairs"
                                        else "m2l_kernel (K1, tiled; target shard)",
                              "k1_avg_ms": k1_avg_ms,

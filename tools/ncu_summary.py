@@ -87,8 +87,8 @@ def launches(path, out):
     # launches (setup, GMRES, SVD, peaks and torch's L2-flush fills excluded),
     # each kernel's total time divided by the number of steps (= K1s launches)
     step_re = re.compile(r"bloch_weight_1|ct_gemv|sum_parts|pinv_gemv|pinv_uh|pinv_v|b_gemv|"
-                         r"m2l_sym_kernel|k1s_reduce")
-    nsteps = sum(len(v) for k, v in agg.items() if "m2l_sym_kernel" in k) or 1
+                         r"m2l_sym_kernel|m2l_sym_stage_kernel|k1s_reduce")
+    nsteps = sum(len(v) for k, v in agg.items() if "m2l_sym_kernel" in k or "m2l_sym_stage_kernel" in k) or 1
     step = {k: v for k, v in agg.items() if step_re.search(k)}
     ts = sum(sum(v) for v in step.values()) / nsteps
     lines += ["", f"per Schur step ({nsteps} steps = K1s launches; every step kernel's total time / "
