@@ -133,7 +133,7 @@ int ps_set_mrhs_variant(ps_ctx* ctx, int variant);
  * pre-assembled coupling blocks: the M2L runs on (SM count - sms) CTAs in a
  * high-priority stream while the HBM-bound C -> A^+ -> B chain streams on the
  * other SMs (sms = 0: only the M2L tail is shared); sms < 0 runs them back
- * to back.  Default 2 (best at cfg3). */
+ * to back.  Default 4 (best at cfg3). */
 int ps_set_overlap(ps_ctx* ctx, int sms);
 /* Queue order of that SM partitioning: 0 (default) the coupling chain at the
  * step's fork, 1 behind K1s (K1s' CTAs dispatched first; slower at cfg3). */

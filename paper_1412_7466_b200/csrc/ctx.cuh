@@ -78,7 +78,7 @@ struct Ctx {
   // chain streams on the remaining SMs in a low-priority stream
   int sym_part = 0, sym_nparts = 1;   // K1s block range (ps_apply_T_blocks)
   int k1_reserve_sms = 0;   // single-RHS M2L grids leave this many SMs free (multi-GPU overlap)
-  int overlap_sms = 2;      // < 0: serial (swept with tools/probe_k1.py: 2 is best at cfg3)
+  int overlap_sms = 4;      // < 0: serial (swept with tools/probe_timeline.py at cfg3: 2 was best with the 1.92 ms K1s, 4 with the 1.74 ms staged one)
   int overlap_k1_first = 0; // 1: queue the coupling chain behind K1s (see schur_overlapped)
   cudaStream_t s_hi = nullptr, s_lo = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_k1 = nullptr, ev_cpl = nullptr, ev_bw = nullptr;
