@@ -18,7 +18,7 @@ def stripped_lib(tmp_path_factory):
     from paper_1412_7466_b200 import _lib, build, sass_reuse_patch as sp
     buf = bytearray(open(_lib.LIB_PATH, "rb").read())
     # strip every DFMA kernel family, patched or not
-    assert sp.strip_hints(buf, r"m2l_sym_kernel|m2l_kernel|m2l_mrhs_kernel") > 10000
+    assert sp.strip_hints(buf, r"m2l_sym_(stage_)?kernel|m2l_kernel|m2l_mrhs_kernel") > 10000
     path = str(tmp_path_factory.mktemp("lib") / "libperiscat_b200_nohints.so")
     with open(path, "wb") as fh:
         fh.write(buf)
