@@ -174,8 +174,8 @@ class ShardedSchur:
         self.s_range = (self.t0, self.t1)     # own sources for the C partial sum
         if mode == "auto":
             # measured per-rank compute at cfg3 (tools/probe_shard.py, K1s
-            # with its symbol store): pairs wins at 2, 4 and 8 ranks (1.11 vs
-            # 1.33 ms, 0.62 vs 0.70 ms, 0.352 vs 0.376 ms); without the store
+            # with its symbol store): pairs wins at 2, 4 and 8 ranks (1.02 vs
+            # 1.33 ms, 0.57 vs 0.70 ms, 0.325 vs 0.377 ms); without the store
             # the tiled target split won at 8 -> pairs while M / world >= 100
             mode = "pairs" if (op.nrhs == 1 and self.world > 1 and op.M >= 512
                                and op.M >= 100 * self.world) else "targets"
