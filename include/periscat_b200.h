@@ -120,7 +120,9 @@ int ps_set_k1_variant(ps_ctx* ctx, int variant);
  * t_nu(x_m - x_j - l d) of every tile-pair batch depend only on the geometry,
  * so the first launch after ps_set_geometry writes them to device memory in
  * the kernel's shared-memory layout (2.5 GB at BASELINE cfg3) and every later
- * launch bulk-copies them instead of regenerating them.  max_gb bounds the
+ * launch bulk-copies them instead of regenerating them (that store-fed kernel
+ * also stages each sweep's coefficient rows in shared memory by TMA; the
+ * environment variable PS_K1S_STAGE=0 keeps them as global loads).  max_gb bounds the
  * store (default 32; 0 regenerates the symbols in every launch); the store is
  * also skipped when it exceeds half the free device memory.  max_gb < 0 only
  * queries; *bytes (optional) = current store size. */
